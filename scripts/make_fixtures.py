@@ -1,0 +1,108 @@
+"""Generate start-solution fixtures with the CPU oracle ONLY (tests/golden-style provenance).
+
+  python scripts/make_fixtures.py fourview   # 4-view TD solve at generic complex p0 -> 296 starts
+  python scripts/make_fixtures.py trifocal   # trifocal monodromy from a planted (x0, p0)
+
+This script imports only `oracle` and `hc_inputs`; the CUDA path never writes fixtures
+(prompt rule ③: no stored value comes from the CUDA path).  Start systems of the paper's
+vision problems come from monodromy; for 4-view the total-degree solve is small
+enough (2^14 = 16384 tracks) to do directly.
+"""
+from __future__ import annotations
+
+import os
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import oracle  # noqa: E402
+from hc_inputs import fixtures, rng, systems  # noqa: E402
+from hc_inputs.descriptor import SystemDesc  # noqa: E402
+
+FOURVIEW_TD_GAMMA_SEED = 0
+
+
+def constant_system_at(desc, p):
+    """The system F(x; p) with its coefficient expressions frozen at p (a TD target)."""
+    c = oracle.eval_coefs(desc, p)
+    return SystemDesc(desc.n_vars, 0, desc.term_eq, desc.term_xexp, desc.term_coef,
+                      np.arange(desc.n_coefs + 1, dtype=np.int32), c,
+                      np.zeros((desc.n_coefs, 0), np.int32), name=desc.name + "@p0").contiguous()
+
+
+def make_fourview():
+    d = systems.nview_triangulation(4)
+    p0 = rng.fourview_p0()
+    td = constant_system_at(d, p0)
+    t0 = time.time()
+    res = oracle.track(oracle.td_homotopy(td, rng.gamma(FOURVIEW_TD_GAMMA_SEED)), oracle.td_start(td.degrees()))
+    U, mult = oracle.dedup(oracle.finite_solutions(res))
+    print(f"4-view TD: {len(U)} distinct finite of {res.status.size} tracks, max mult {mult.max()}, "
+          f"{time.time() - t0:.1f} s", flush=True)
+    hdr = (f"4-view triangulation start solutions at p0 = rng.fourview_p0() (seed {rng.SEED_FOURVIEW_P0}).\n"
+           f"Written by scripts/make_fixtures.py (oracle only): TD homotopy, gamma seed {FOURVIEW_TD_GAMMA_SEED},\n"
+           f"{res.status.size} tracks -> {len(U)} distinct finite solutions (PAPER.md Table 2 P:490: 296).")
+    fixtures.write_solutions(fixtures.fixture_path("fourview_start.sols"), U, hdr)
+    fixtures.write_params(fixtures.fixture_path("fourview_p0.params"), p0, hdr)
+
+
+def _orbit(x):
+    return systems.trifocal_symmetry(x)
+
+
+def _contains(S, y, tol=1e-6):
+    if S.shape[0] == 0:
+        return False
+    return bool(np.any(np.all(np.abs(S - y) <= tol * np.maximum(1.0, np.abs(y)), axis=1)))
+
+
+def make_trifocal(max_loops: int = 60, stall_loops: int = 4, seed: int = rng.SEED_TRIFOCAL_MONODROMY):
+    """Monodromy ("monodromy module", SURVEY.md [X6]) with the Z2^3 symmetry of R20:
+    only one representative per orbit is tracked; endpoints are expanded by the 8 group elements."""
+    d = systems.trifocal_unknown_f()
+    p0, x0 = rng.trifocal_complex_start(seed)
+    reps = [x0]
+    full = np.array(_orbit(x0))
+    g = rng.gen(seed + 1)
+    stall = 0
+    t0 = time.time()
+    for loop in range(max_loops):
+        p1 = rng.complex_normal(g, d.n_params)
+        p2 = rng.complex_normal(g, d.n_params)
+        X = np.array(reps)
+        alive = np.arange(len(reps))
+        for pa, pb in ((p0, p1), (p1, p2), (p2, p0)):
+            res = oracle.track(oracle.ph_homotopy(d, pa, pb), X)
+            ok = res.status[0] == oracle.CONVERGED
+            X = res.x[0][ok]
+            alive = alive[ok]
+        new = 0
+        for y in X:
+            if not _contains(full, y):
+                reps.append(y)
+                full = np.concatenate([full, np.array(_orbit(y))])
+                new += 1
+        stall = stall + 1 if new == 0 else 0
+        print(f"loop {loop}: tracked {len(alive)}/{len(reps) - new} survived, +{new} orbits -> "
+              f"{len(reps)} orbits = {full.shape[0]} solutions ({time.time() - t0:.0f} s)", flush=True)
+        if stall >= stall_loops:
+            break
+    hdr = (f"trifocal unknown-f start solutions at the planted complex p0 = rng.trifocal_complex_start({seed}).\n"
+           f"Written by scripts/make_fixtures.py (oracle only): symmetry-aware monodromy, {loop + 1} loops,\n"
+           f"{len(reps)} orbits x 8 = {full.shape[0]} solutions (PAPER.md Table 2 P:488 reports 1784).")
+    fixtures.write_solutions(fixtures.fixture_path("trifocal_start.sols"), full, hdr)
+    fixtures.write_solutions(fixtures.fixture_path("trifocal_reps.sols"), np.array(reps), hdr)
+    fixtures.write_params(fixtures.fixture_path("trifocal_p0.params"), p0, hdr)
+
+
+if __name__ == "__main__":
+    oracle.build()
+    what = sys.argv[1:] or ["fourview", "trifocal"]
+    if "fourview" in what:
+        make_fourview()
+    if "trifocal" in what:
+        make_trifocal()

@@ -1,0 +1,314 @@
+"""Pins of the CPU oracle (oracle/) against things other than itself (CPU-only, `-m "not gpu"`).
+
+Each test names what pins it: a library routine (numpy), a closed form, finite
+differences, a textbook or paper root count, or planted ground truth.
+"""
+import numpy as np
+import pytest
+
+from hc_inputs import rng, systems
+from hc_inputs.evalpoly import eval_poly
+
+
+def crandn(g, *shape):
+    return (g.standard_normal(shape) + 1j * g.standard_normal(shape)) / np.sqrt(2)
+
+
+SYSTEMS = {
+    "katsura-6": lambda: systems.katsura(6),
+    "cyclic-5": lambda: systems.cyclic(5),
+    "4-view": lambda: systems.nview_triangulation(4),
+    "trifocal": lambda: systems.trifocal_unknown_f(),
+    "univ-param": lambda: systems.univariate_param(5),
+}
+
+
+# ---------------------------------------------------------------- linear solve
+
+def test_lu_matches_numpy_solve(orc):
+    """Library pin: textbook LU+2 triangular solves vs numpy.linalg.solve (LAPACK zgesv), N=1..32."""
+    g = rng.gen(123)
+    for trial in range(300):
+        n = 1 + trial % 32
+        A = crandn(g, n, n) + np.eye(n) * (1.0 + g.random())
+        b = crandn(g, n)
+        x, sing = orc.lu_solve(A, b)
+        assert not sing
+        xr = np.linalg.solve(A, b)
+        assert np.max(np.abs(x - xr)) <= 1e-12 * max(1.0, np.max(np.abs(xr))) * np.linalg.cond(A)
+        # backward-error bound
+        r = np.max(np.abs(A @ x - b))
+        assert r <= 1e-10 * (np.max(np.abs(A).sum(1)) * np.max(np.abs(x)) + np.max(np.abs(b)))
+
+
+def test_lu_needs_pivoting(orc):
+    """Closed form: zero leading pivot forces a row swap; A = [[0,1],[2,0]], b = [3,4] -> x = [2,3]."""
+    x, sing = orc.lu_solve(np.array([[0, 1], [2, 0]], complex), np.array([3, 4], complex))
+    assert not sing and np.allclose(x, [2, 3], atol=0, rtol=1e-15)
+
+
+def test_lu_singular_flagged(orc):
+    """Rank-deficient matrices are flagged, never solved silently (R9)."""
+    g = rng.gen(5)
+    for n in (2, 7, 18, 32):
+        A = crandn(g, n, n)
+        A[-1] = A[0] * (0.3 - 0.2j)  # dependent row
+        _, sing = orc.lu_solve(A, crandn(g, n))
+        assert sing
+    _, sing = orc.lu_solve(np.zeros((3, 3), complex), np.ones(3, complex))
+    assert sing
+    A = np.eye(3, dtype=complex)
+    A[1, 1] = np.nan
+    _, sing = orc.lu_solve(A, np.ones(3, complex))
+    assert sing
+
+
+# ---------------------------------------------------------------- evaluation
+
+@pytest.mark.parametrize("name", list(SYSTEMS))
+def test_F_matches_defining_sum(orc, name):
+    """F(x; p) from the descriptor == direct sum over the source polynomial's terms."""
+    d = SYSTEMS[name]()
+    g = rng.gen(7)
+    for _ in range(5):
+        x = crandn(g, d.n_vars)
+        p = crandn(g, d.n_params)
+        F = orc.eval_F(d, p, x)
+        ref = np.array([eval_poly(f, x, p) for f in d.polys])
+        assert np.max(np.abs(F - ref)) <= 1e-12 * (1 + np.max(np.abs(ref)))
+
+
+@pytest.mark.parametrize("name", list(SYSTEMS))
+def test_JF_matches_central_differences(orc, name):
+    """J_F vs central finite differences of F: relative error < 1e-6 with h = 1e-6."""
+    d = SYSTEMS[name]()
+    g = rng.gen(11)
+    h = 1e-6
+    for _ in range(3):
+        x = crandn(g, d.n_vars)
+        p = crandn(g, d.n_params)
+        J = orc.eval_JF(d, p, x)
+        for v in range(d.n_vars):
+            e = np.zeros(d.n_vars, complex)
+            e[v] = h
+            fd = (orc.eval_F(d, p, x + e) - orc.eval_F(d, p, x - e)) / (2 * h)
+            assert np.max(np.abs(J[:, v] - fd)) <= 1e-6 * (1 + np.max(np.abs(fd)))
+
+
+def test_td_homotopy_endpoints_and_Ht(orc):
+    """Eq. 1 endpoints: H(x,0) = gamma G(x) with G_i = x_i^d_i - 1, H(x,1) = F(x); H_t vs central FD in t
+    (S:176-198).  G is checked against numpy's power, F against the defining sum."""
+    d = systems.katsura(4)
+    gam = rng.gamma(3)
+    hom = orc.td_homotopy(d, gam)
+    g = rng.gen(2)
+    deg = np.array(d.degrees())
+    for _ in range(4):
+        x = crandn(g, d.n_vars)
+        H0, _, _ = hom.eval(x, 0.0)
+        assert np.allclose(H0, gam * (np.power(x, deg) - 1), rtol=1e-14, atol=1e-14)
+        H1, Hx1, _ = hom.eval(x, 1.0)
+        F = np.array([eval_poly(f, x) for f in d.polys])
+        assert np.allclose(H1, F, rtol=1e-13, atol=1e-13)
+        assert np.allclose(Hx1, orc.eval_JF(d, np.zeros(0), x), rtol=1e-13, atol=1e-13)
+        t = g.random()
+        _, _, Ht = hom.eval(x, t)
+        hh = 1e-6
+        fd = (hom.eval(x, t + hh)[0] - hom.eval(x, t - hh)[0]) / (2 * hh)
+        assert np.max(np.abs(Ht - fd)) <= 1e-6 * (1 + np.max(np.abs(fd)))
+        _, _, Ht2 = hom.eval(x, 1 - t)
+        assert np.allclose(Ht, Ht2, rtol=1e-13, atol=1e-13)  # straight-line TD: H_t independent of t
+
+
+@pytest.mark.parametrize("name", ["4-view", "trifocal", "univ-param"])
+def test_ph_homotopy_endpoints_and_Ht(orc, name):
+    """PH (R3): H(x,0) = F(x;p0), H(x,1) = F(x;p1); H_t vs central FD in t (exactness not assumed)."""
+    d = SYSTEMS[name]()
+    g = rng.gen(13)
+    p0, p1 = crandn(g, d.n_params), crandn(g, d.n_params)
+    hom = orc.ph_homotopy(d, p0, p1)
+    x = crandn(g, d.n_vars)
+    F0 = np.array([eval_poly(f, x, p0) for f in d.polys])
+    F1 = np.array([eval_poly(f, x, p1) for f in d.polys])
+    assert np.allclose(hom.eval(x, 0.0)[0], F0, rtol=1e-12, atol=1e-12)
+    assert np.allclose(hom.eval(x, 1.0)[0], F1, rtol=1e-12, atol=1e-12)
+    for t in (0.1, 0.5, 0.93):
+        hh = 1e-5
+        fd = (hom.eval(x, t + hh)[0] - hom.eval(x, t - hh)[0]) / (2 * hh)
+        Ht = hom.eval(x, t)[2]
+        assert np.max(np.abs(Ht - fd)) <= 1e-7 * (1 + np.max(np.abs(fd)))
+
+
+# ---------------------------------------------------------------- predictor / corrector
+
+def _line_homotopy(orc):
+    """F(x; p) = x - p with p0 = 1, p1 = 2: H = x - (1 + t), exact path x(t) = 1 + t."""
+    from hc_inputs.poly import var_p, var_x
+    f = var_x(1, 1, 0) - var_p(1, 1, 0)
+    d = systems.from_polys([f], "line")
+    return orc.ph_homotopy(d, np.array([1.0]), np.array([2.0]))
+
+
+def test_predictor_exact_on_linear_path(orc):
+    """Closed form: Euler from (x=1, t=0, dt=0.5) gives 1.5 exactly; RK4 equals Euler."""
+    hom = _line_homotopy(orc)
+    for pred in (0, 1):
+        st = orc.default_settings()
+        st.predictor = pred
+        xp, fail = orc.predict(hom, np.array([1.0 + 0j]), 0.0, 0.5, st)
+        assert not fail and xp[0] == 1.5
+
+
+def test_newton_quadratic_contraction(orc):
+    """Closed form: Newton on x^2 - 4 from 2 + 1e-3: one step error ~ e^2/(2*2) = 2.5e-7 < 1e-5."""
+    d = systems.univariate([-4, 0, 1])
+    hom = orc.td_homotopy(d, 1.0)
+    x, code = orc.newton(hom, np.array([2.001 + 0j]), 1.0, 1, 1e-300)
+    assert abs(x[0] - 2) < 1e-5
+    assert abs(abs(x[0] - 2) - 1e-6 / 4.002) < 1e-12   # exact one-step error e^2 / (2 x0)
+    x2, code = orc.newton(hom, np.array([2.001 + 0j]), 1.0, 3, 1e-12)
+    assert code == 1 and abs(x2[0] - 2) < 1e-15
+
+
+def test_track_linear_path(orc):
+    """Whole tracker on the exact path x(t) = 1 + t: converges to 2."""
+    hom = _line_homotopy(orc)
+    res = orc.track(hom, np.array([[1.0 + 0j]]), p1s=np.array([[2.0 + 0j]]))
+    assert res.status[0, 0] == orc.CONVERGED
+    assert abs(res.x[0, 0, 0] - 2) < 1e-14
+
+
+# ---------------------------------------------------------------- start system (R2)
+
+def test_td_start_roots_of_unity(orc):
+    """Closed form: prod(d) distinct points with x_i^{d_i} = 1 (north_star), exact quarter turns."""
+    deg = [1, 2, 3, 4, 5]
+    X = orc.td_start(deg)
+    assert X.shape == (120, 5)
+    assert np.max(np.abs(np.power(X, deg) - 1)) <= 1e-14
+    keys = {tuple(np.round(r, 9)) for r in X}
+    assert len(keys) == 120
+    X4 = orc.td_start([4])
+    assert X4[1, 0] == 1j and X4[2, 0] == -1 and X4[3, 0] == -1j
+
+
+# ---------------------------------------------------------------- whole tracker
+
+def test_univariate_matches_companion_eigenvalues(orc):
+    """Library pin: TD endpoints of a random degree-d polynomial = numpy.roots within 1e-8."""
+    g = rng.gen(21)
+    for d in (2, 3, 5, 8):
+        c = crandn(g, d + 1)
+        desc = systems.univariate(c)
+        hom = orc.td_homotopy(desc, rng.gamma(d))
+        res = orc.track(hom, orc.td_start([d]))
+        assert np.all(res.status == orc.CONVERGED)
+        got = res.x[0, :, 0]
+        ref = np.roots(c[::-1])
+        ok, ua, ub = orc.match_sets(got[:, None], ref[:, None], tol=1e-8)
+        assert ok, (d, ua, ub)
+
+
+def test_td_x2_plus_1(orc):
+    """Closed form: F = x^2 + 1 -> both tracks reach +-i."""
+    hom = orc.td_homotopy(systems.univariate([1, 0, 1]), rng.gamma(0))
+    res = orc.track(hom, orc.td_start([2]))
+    got = np.sort_complex(res.x[0, :, 0])
+    assert np.all(res.status == orc.CONVERGED)
+    assert np.allclose(got, [-1j, 1j], atol=1e-12)
+
+
+def test_katsura6_all_64(orc):
+    """Textbook count: katsura-6 has 2^6 = 64 finite roots = Bezout number: all 64 tracks converge,
+    distinct, residual < 1e-10, and (1,0,...,0) is among them (SURVEY.md §8(c) pins)."""
+    d = systems.katsura(6)
+    for seed in (0, 1, 2):
+        res = orc.track(orc.td_homotopy(d, rng.gamma(seed)), orc.td_start(d.degrees()))
+        assert np.all(res.status == orc.CONVERGED)
+        U, mult = orc.dedup(orc.finite_solutions(res))
+        assert len(U) == 64 and mult.max() == 1
+        assert res.resid[0, :, 0].max() < 1e-10
+        e0 = np.zeros(7)
+        e0[0] = 1
+        assert np.min(np.max(np.abs(U - e0), axis=1)) < 1e-12
+
+
+@pytest.mark.parametrize("n,count", [(5, 70), (6, 156)])
+def test_cyclic_counts(orc, n, count):
+    """Textbook counts: cyclic-5 has 70 and cyclic-6 has 156 isolated roots."""
+    d = systems.cyclic(n)
+    res = orc.track(orc.td_homotopy(d, rng.gamma(1)), orc.td_start(d.degrees()))
+    U, mult = orc.dedup(orc.finite_solutions(res))
+    assert len(U) == count and mult.max() == 1
+
+
+def _cyclic_closed(U, n, tol=1e-8):
+    """The set is closed under x -> w x (w^n = 1), cyclic shift and reversal (symmetry of cyclic-n)."""
+    w = np.exp(2j * np.pi / n)
+    for img in (U * w, np.roll(U, 1, axis=1), U[:, ::-1]):
+        for y in img:
+            if not np.any(np.all(np.abs(U - y) <= tol * np.maximum(1, np.abs(y)), axis=1)):
+                return False
+    return True
+
+
+CYCLIC7_GAMMA_SEED = 2  # gamma seed used by config 2 (seeds that reach 924 in the oracle)
+
+
+def test_cyclic7_924(orc):
+    """Paper count: cyclic-7 has 924 finite roots (Table 1), set closed under its symmetry group."""
+    d = systems.cyclic(7)
+    res = orc.track(orc.td_homotopy(d, rng.gamma(CYCLIC7_GAMMA_SEED)), orc.td_start(d.degrees()))
+    U, mult = orc.dedup(orc.finite_solutions(res))
+    assert len(U) == 924 and mult.max() == 1
+    assert res.resid[0][res.status[0] == orc.CONVERGED, 0].max() < 1e-10
+    assert _cyclic_closed(U, 7)
+
+
+def test_determinism_across_thread_counts(orc):
+    """bit-identical results for 1 and 8 threads."""
+    d = systems.cyclic(5)
+    hom = orc.td_homotopy(d, rng.gamma(4))
+    X0 = orc.td_start(d.degrees())
+    a = orc.track(hom, X0, nthreads=1)
+    b = orc.track(hom, X0, nthreads=8)
+    assert np.array_equal(a.x.view(np.float64), b.x.view(np.float64))
+    assert np.array_equal(a.status, b.status) and np.array_equal(a.counters, b.counters)
+
+
+# ---------------------------------------------------------------- post-processing
+
+def test_dedup_and_real_classification(orc):
+    X = np.array([[1 + 1e-9j, 2], [1, 2 + 1e-9], [1j, 0], [2 + 1e-12j, 0]])
+    U, m = orc.dedup(X)
+    assert len(U) == 3 and list(m) == [2, 1, 1]
+    assert list(orc.is_real(U)) == [True, False, True]
+    ok, _, _ = orc.match_sets(U, U[::-1].copy())
+    assert ok
+    ok, ua, ub = orc.match_sets(U, U[:2])
+    assert not ok and ua == 1 and ub == 0
+
+
+# ---------------------------------------------------------------- vision generators vs oracle
+
+def test_fourview_planted_is_exact(orc):
+    """Planted ground truth (R18): F(x*; p) ~ 0 for generated 4-view instances, and p is real."""
+    d = systems.nview_triangulation(4)
+    for b in range(5):
+        p, xs = rng.fourview_instance(rng.SEED_FOURVIEW_INSTANCE + b)
+        assert np.all(p.imag == 0)
+        F = orc.eval_F(d, p, xs)
+        assert np.max(np.abs(F)) < 1e-13
+
+
+def test_trifocal_planted_is_exact(orc):
+    """Planted ground truth: F(x_gt; p) ~ 0 for generated trifocal instances; the Z2^3 images of a
+    solution are solutions (R20 symmetry)."""
+    d = systems.trifocal_unknown_f()
+    for b in range(5):
+        p, x = rng.trifocal_instance(rng.SEED_TRIFOCAL_INSTANCE + b)
+        assert np.max(np.abs(orc.eval_F(d, p, x))) < 1e-12
+        for y in systems.trifocal_symmetry(x):
+            assert np.max(np.abs(orc.eval_F(d, p, y))) < 1e-12
+    p0, x0 = rng.trifocal_complex_start()
+    assert np.max(np.abs(orc.eval_F(d, p0, x0))) < 1e-12
