@@ -23,7 +23,7 @@ def write_solutions(path: str, X: np.ndarray, header_comment: str = "") -> None:
         fh.write(f"{n} {S}\n")
         for s in range(S):
             for v in range(n):
-                fh.write(f"{X[s, v].real!r} {X[s, v].imag!r}\n")
+                fh.write(f"{float(X[s, v].real)!r} {float(X[s, v].imag)!r}\n")
 
 
 def read_solutions(path: str) -> np.ndarray:
@@ -46,7 +46,7 @@ def write_params(path: str, p: np.ndarray, header_comment: str = "") -> None:
                 fh.write(f"# {line}\n")
         fh.write(f"{p.shape[0]}\n")
         for z in p:
-            fh.write(f"{z.real!r} {z.imag!r}\n")
+            fh.write(f"{float(z.real)!r} {float(z.imag)!r}\n")
 
 
 def read_params(path: str) -> np.ndarray:
@@ -67,3 +67,12 @@ def fixture_path(name: str) -> str:
 
 def have_fixture(name: str) -> bool:
     return os.path.exists(fixture_path(name))
+
+
+def trifocal_start():
+    """(start solutions [S, 18], p0 [24]) of the trifocal fixture: the orbit representatives written by
+    scripts/make_fixtures.py expanded by the Z2^3 symmetry in the same order the script used."""
+    from . import systems
+    reps = read_solutions(fixture_path("trifocal_reps.sols"))
+    full = np.concatenate([np.array(systems.trifocal_symmetry(r)) for r in reps])
+    return full, read_params(fixture_path("trifocal_p0.params"))

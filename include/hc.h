@@ -1,0 +1,215 @@
+/*
+ * hc.h -- C ABI of the B200-native batched homotopy-continuation path tracker.
+ *
+ * Method: GPU-HC (Chien et al., arXiv 2112.03444; /root/reference/PAPER.md, cited "P:<line>").
+ * For every start solution x0 of a start system and every problem instance, track the
+ * solution path x(t) of H(x, t) = 0 from t = 0 to t = 1 (Eq. 1) with a
+ * Runge-Kutta predictor on the Davidenko ODE  (dH/dx) dx/dt = -dH/dt  (Eq. 3, P:166-169;
+ * RK4 P:175) and a Newton corrector (Eq. 5-6), adaptive step control, and
+ * endpoint classification; complex FP64 throughout, N <= 32 unknowns.
+ *
+ * Homotopies: every homotopy is a parameter homotopy H(x,t) = F(x; (1-t) p0 + t p1)
+ * ("coefficients ... are linear interpolation of corresponding elements in the start and
+ * target systems").  A total-degree homotopy with the gamma
+ * trick, H = (1-t) gamma G + t F with G_i = x_i^{d_i} - 1, is expressed in that form by
+ * hc_system_create_total_degree + hc_total_degree_params (SURVEY.md §8(b) convention).
+ *
+ * Conventions
+ *  - extern "C"; no C++ exception crosses this boundary; every call returns hc_status.
+ *  - hc_complex is layout-compatible with std::complex<double>, cuDoubleComplex and
+ *    torch.complex128 (interleaved re, im).
+ *  - Errors: argument/shape errors return HC_E_INVALID_ARG (N not in [1,32], null pointers,
+ *    non-finite coefficients, inconsistent sizes); unsupported sizes HC_E_TOO_LARGE; CUDA
+ *    failures HC_E_CUDA; allocation failures HC_E_OOM.  hc_last_error() returns a
+ *    thread-local message for the last failing call.  A per-track numerical failure is
+ *    never an error: it is reported in the track's status ("the batch call never fails
+ *    wholesale").
+ *  - Determinism: a track's arithmetic depends only on its inputs, never on scheduling,
+ *    batch size or GPU count: identical inputs give identical output bits.
+ */
+#ifndef HC_H
+#define HC_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define HC_MAX_VARS 32
+#define HC_MAX_FACTORS 8   /* max total degree of one Jacobian/homotopy term after differentiation + 1 */
+
+typedef struct { double re, im; } hc_complex;
+
+typedef enum {
+  HC_OK = 0,
+  HC_E_INVALID_ARG = 1,
+  HC_E_TOO_LARGE = 2,
+  HC_E_CUDA = 3,
+  HC_E_OOM = 4,
+  HC_E_INTERNAL = 5
+} hc_status;
+
+/* Per-track endpoint status (readings R8-R10). */
+typedef enum {
+  HC_CONVERGED = 0,      /* reached t = 1, polished, residual <= res_abs or relative residual <= res_rel */
+  HC_DIVERGED = 1,       /* ||x||_inf > inf_norm during tracking (path to infinity) */
+  HC_STEP_UNDERFLOW = 2, /* step size fell below dt_min */
+  HC_MAX_STEPS = 3,      /* more than max_steps step attempts */
+  HC_SINGULAR = 4,       /* reached t = 1 but the endpoint failed the residual test (singular/ill-conditioned) */
+  HC_NONFINITE = 5       /* non-finite endpoint */
+} hc_track_status;
+
+typedef enum { HC_RK4 = 0, HC_EULER = 1 } hc_predictor;
+typedef enum { HC_MEM_DEVICE = 0, HC_MEM_HOST = 1 } hc_memory;
+
+typedef struct hc_system_s *hc_system;  /* opaque, library-owned */
+typedef struct hc_result_s *hc_result;  /* opaque, library-owned */
+
+/* ---------------------------------------------------------------------------------------------
+ * System description: F(x; p) = 0, N equations in N unknowns, coefficients polynomial in P params.
+ *   F_i(x; p) = sum_{k : term_eq[k] == i} c_{term_coef[k]}(p) * prod_v x_v^{term_xexp[k*N + v]}
+ *   c_j(p)    = sum_{m = coef_ptr[j]}^{coef_ptr[j+1]-1} coef_w[m] * prod_q p_q^{coef_pexp[m*P + q]}
+ * All pointers are host pointers, borrowed for the duration of the call.
+ * --------------------------------------------------------------------------------------------- */
+typedef struct {
+  int32_t n_vars;            /* N, 1..32 */
+  int32_t n_params;          /* P >= 0 */
+  int32_t n_terms;           /* number of (equation, x-monomial) terms */
+  const int32_t *term_eq;    /* [n_terms] equation index in [0, N) */
+  const int32_t *term_xexp;  /* [n_terms * N] exponents of x, >= 0 */
+  const int32_t *term_coef;  /* [n_terms] coefficient-expression id in [0, n_coefs) */
+  int32_t n_coefs;           /* number of coefficient expressions */
+  const int32_t *coef_ptr;   /* [n_coefs + 1] CSR offsets into coef_w / coef_pexp */
+  const hc_complex *coef_w;  /* [nnz] weights (finite) */
+  const int32_t *coef_pexp;  /* [nnz * P] parameter exponents, >= 0 */
+} hc_system_desc;
+
+/* Compile the system (the paper's "indexing system": homogenised term tables for
+ * dH/dx, dH/dt and H, the constant-one slot, lane-balanced op lists) and upload the tables to
+ * `device`.  *out receives a handle owned by the caller until hc_system_destroy. */
+hc_status hc_system_create(const hc_system_desc *desc, int device, hc_system *out);
+
+/* Total-degree homotopy H = (1-t) gamma G + t F, G_i = x_i^{d_i} - 1 (Eq. 1 + gamma trick, R1/R2).
+ * `target` must have constant coefficients (all coef_pexp zero).  The created system has
+ * parameters p = (coefficients of G, coefficients of F); hc_total_degree_params fills the
+ * p0/p1 that make the parameter homotopy equal Eq. 1 with gamma. */
+hc_status hc_system_create_total_degree(const hc_system_desc *target, int device, hc_system *out);
+hc_status hc_total_degree_params(hc_system sys, hc_complex gamma,
+                                 hc_complex *p0 /* host [P] */, hc_complex *p1 /* host [P] */);
+/* Number of total-degree start solutions prod_i d_i (or -1 when > 2^31). */
+int64_t hc_total_degree_count(hc_system sys);
+/* Start solutions x_i = exp(2 pi i k_i / d_i), k_1 fastest (reading R2); host [count * N]. */
+hc_status hc_total_degree_start(hc_system sys, hc_complex *start_x);
+
+typedef struct {
+  int32_t n_vars, n_params, n_coefs;
+  int32_t coef_degree_t;      /* D: degree of the coefficient polynomials in t */
+  int32_t lanes_per_track;    /* L = next power of two >= N */
+  int32_t tracks_per_warp;    /* 32 / L */
+  int32_t op_steps;           /* Q: evaluation op steps per lane (lane-balanced) */
+  int32_t max_factors;        /* M: max factors per op (paper's M) */
+  int32_t n_ops_J, n_ops_rhs; /* real (unpadded) ops of dH/dx and of the H / dH/dt vector */
+  int32_t n_terms;            /* terms of F */
+  int64_t flops_coef;         /* algorithmic FP64 flops per solve: coefficient polynomials at t */
+  int64_t flops_eval;         /* ... evaluating dH/dx and one right-hand side */
+  int64_t flops_lu;           /* ... fused LU + solve on [A | b] (SURVEY.md §8(d) rule) */
+  int64_t flops_solve;        /* total per solve (coef + eval + lu + 8N vector work) */
+  int64_t smem_per_track;     /* bytes of shared memory per track slot */
+} hc_system_info;
+hc_status hc_system_info_get(hc_system sys, hc_system_info *out);
+/* Host-only (no GPU needed): compile `desc` and report its info / its evaluation op table.
+ * Op table layout: op_steps * lanes_per_track records of 4 uint32 (see csrc/hc_internal.h:
+ * x = coef | dest << 16, y = flags | scale << 8, z/w = factor indices), step_nfac [op_steps]
+ * = max factor count of step q.  capacity = number of op records the buffer holds. */
+hc_status hc_system_compile_info(const hc_system_desc *desc, hc_system_info *out);
+hc_status hc_system_compile_ops(const hc_system_desc *desc, uint32_t *ops, uint8_t *step_nfac, int64_t capacity);
+hc_status hc_system_destroy(hc_system sys);
+
+/* ---------------------------------------------------------------------------------------------
+ * Tracker settings (the paper fixes none of them).
+ * --------------------------------------------------------------------------------------------- */
+typedef struct {
+  int32_t predictor;    /* HC_RK4 or HC_EULER (Eq. 4) */
+  double dt_init;       /* initial step (0.01) */
+  double dt_min;        /* STEP_UNDERFLOW below this (1e-14) */
+  double dt_max;        /* (0.1) */
+  int32_t grow_after;   /* consecutive accepted steps before growing (4) */
+  double grow;          /* (2.0) */
+  double shrink;        /* on rejection (0.5) */
+  int32_t max_newton;   /* corrector iterations per step (3) */
+  double newton_tol;    /* converged when ||dx||_inf <= tol * max(1, ||x||_inf) (1e-8) */
+  int32_t max_steps;    /* step attempts (10000) */
+  double inf_norm;      /* DIVERGED when ||x||_inf exceeds it (1e14) */
+  int32_t end_newton;   /* endpoint polish iterations at t = 1 (3) */
+  double end_tol;       /* polish tolerance (1e-12) */
+  double res_abs;       /* CONVERGED if ||F(x)||_inf <= res_abs (1e-10) ... */
+  double res_rel;       /* ... or max_i |F_i| / sum_k |c_ik||m_k(x)| <= res_rel (1e-12) */
+  double pivot_rel;     /* a solve fails when |pivot| <= pivot_rel * max|A_ij| (1e-14) */
+} hc_tracker_settings;
+hc_status hc_tracker_settings_default(hc_tracker_settings *out);
+
+/* ---------------------------------------------------------------------------------------------
+ * One batch: B instances x S start solutions = B*S tracks, track id g = b*S + s.
+ * memory == HC_MEM_DEVICE: every pointer is a device pointer on the system's device; the call
+ *   enqueues work on `stream` and returns immediately; inputs must stay valid until the stream
+ *   passes the batch (hc_result_wait or a stream synchronisation).
+ * memory == HC_MEM_HOST: every pointer is a host pointer; the library stages host->device
+ *   copies, runs, copies results back and returns after completion (end-to-end path).
+ * Output pointers may be NULL: the result then owns device buffers, read with hc_result_get.
+ * --------------------------------------------------------------------------------------------- */
+typedef struct {
+  int64_t n_instances;         /* B >= 1 */
+  int64_t n_start;             /* S >= 1 */
+  const hc_complex *start_x;   /* [S * N] start solutions */
+  const hc_complex *p_start;   /* [P] p0 (may be NULL when P == 0) */
+  const hc_complex *p_target;  /* [B * P] p1 per instance (may be NULL when P == 0) */
+  hc_complex *x_out;           /* [B * S * N] endpoints, or NULL */
+  int32_t *status_out;         /* [B * S] hc_track_status, or NULL */
+  int32_t *counters_out;       /* [B * S * 4]: steps, rejections, newton iterations, solves; or NULL */
+  double *resid_out;           /* [B * S * 2]: ||F||_inf, relative residual; or NULL */
+  int32_t memory;              /* hc_memory */
+  void *stream;                /* cudaStream_t (NULL = default stream) */
+} hc_batch;
+
+/* Enqueue (or, for HC_MEM_HOST, run) one batch.  *out (may be NULL) receives a result handle that
+ * must be released with hc_result_destroy; the system must outlive its results. */
+hc_status hc_track_batch(hc_system sys, const hc_tracker_settings *settings, const hc_batch *batch,
+                         hc_result *out);
+/* Block until the batch finished. */
+hc_status hc_result_wait(hc_result res);
+/* Device time in ms between the start of the coefficient prologue and the end of the tracker
+ * kernel, measured with CUDA events on the batch stream; also each kernel alone. */
+hc_status hc_result_elapsed_ms(hc_result res, float *total_ms, float *prologue_ms, float *tracker_ms);
+
+typedef struct {
+  int32_t status;       /* hc_track_status */
+  int32_t steps, rejections, newton_iters, solves;
+  double resid_abs, resid_rel;
+} hc_track_info;
+/* Copy one track's endpoint (host x [N]) and info; waits for the batch. */
+hc_status hc_result_get(hc_result res, int64_t instance, int64_t track, hc_complex *x, hc_track_info *info);
+hc_status hc_result_destroy(hc_result res);
+
+/* ---------------------------------------------------------------------------------------------
+ * Batched fused LU + solve (kernel fusion, augmented matrix [A b], back-substitution
+ * on the cached U).  Solves A_k x_k = b_k for k < batch; A row-major [batch][n][n], b [batch][n],
+ * x [batch][n], info [batch] (0 ok, 1 singular: pivot <= pivot_rel * max|A_ij| or non-finite).
+ * Device pointers, async on stream.  n in [1, 32].
+ * --------------------------------------------------------------------------------------------- */
+hc_status hc_batched_zgesv(int32_t n, int64_t batch, const hc_complex *A, const hc_complex *b, hc_complex *x,
+                           int32_t *info, double pivot_rel, void *stream);
+
+/* FP64 DFMA throughput probe (SURVEY.md §8(d) "FP64 peak"): runs ~`ms` milliseconds of
+ * independent DFMA chains on every SM of `device`; *tflops receives the achieved FLOP/s / 1e12. */
+hc_status hc_fp64_peak_probe(int device, double *tflops);
+
+/* Thread-local message of the last failing call (never NULL). */
+const char *hc_last_error(void);
+/* Library version string. */
+const char *hc_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HC_H */

@@ -1,0 +1,575 @@
+// abi.cpp -- the C ABI (include/hc.h): system handles, batch launch, results, helpers.
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "../hc_internal.h"
+#include "compiler.h"
+
+namespace hcb {
+// per-N launchers defined in csrc/kernels/tracker_n*.cu
+#define HCB_DECL(N)                                                                                      \
+  cudaError_t launch_tracker_##N(const TrackArgs &, int, cudaStream_t, TrackerPlan *);                  \
+  cudaError_t launch_zgesv_##N(int64_t, const double2 *, const double2 *, double2 *, int32_t *, double, \
+                               cudaStream_t);
+HCB_DECL(1) HCB_DECL(2) HCB_DECL(3) HCB_DECL(4) HCB_DECL(5) HCB_DECL(6) HCB_DECL(7) HCB_DECL(8)
+HCB_DECL(9) HCB_DECL(10) HCB_DECL(11) HCB_DECL(12) HCB_DECL(13) HCB_DECL(14) HCB_DECL(15) HCB_DECL(16)
+HCB_DECL(17) HCB_DECL(18) HCB_DECL(19) HCB_DECL(20) HCB_DECL(21) HCB_DECL(22) HCB_DECL(23) HCB_DECL(24)
+HCB_DECL(25) HCB_DECL(26) HCB_DECL(27) HCB_DECL(28) HCB_DECL(29) HCB_DECL(30) HCB_DECL(31) HCB_DECL(32)
+#undef HCB_DECL
+
+typedef cudaError_t (*zgesv_fn)(int64_t, const double2 *, const double2 *, double2 *, int32_t *, double, cudaStream_t);
+static const tracker_launch_fn kTrackers[33] = {
+    nullptr,            launch_tracker_1,  launch_tracker_2,  launch_tracker_3,  launch_tracker_4,
+    launch_tracker_5,   launch_tracker_6,  launch_tracker_7,  launch_tracker_8,  launch_tracker_9,
+    launch_tracker_10,  launch_tracker_11, launch_tracker_12, launch_tracker_13, launch_tracker_14,
+    launch_tracker_15,  launch_tracker_16, launch_tracker_17, launch_tracker_18, launch_tracker_19,
+    launch_tracker_20,  launch_tracker_21, launch_tracker_22, launch_tracker_23, launch_tracker_24,
+    launch_tracker_25,  launch_tracker_26, launch_tracker_27, launch_tracker_28, launch_tracker_29,
+    launch_tracker_30,  launch_tracker_31, launch_tracker_32};
+static const zgesv_fn kZgesv[33] = {
+    nullptr,          launch_zgesv_1,  launch_zgesv_2,  launch_zgesv_3,  launch_zgesv_4,  launch_zgesv_5,
+    launch_zgesv_6,   launch_zgesv_7,  launch_zgesv_8,  launch_zgesv_9,  launch_zgesv_10, launch_zgesv_11,
+    launch_zgesv_12,  launch_zgesv_13, launch_zgesv_14, launch_zgesv_15, launch_zgesv_16, launch_zgesv_17,
+    launch_zgesv_18,  launch_zgesv_19, launch_zgesv_20, launch_zgesv_21, launch_zgesv_22, launch_zgesv_23,
+    launch_zgesv_24,  launch_zgesv_25, launch_zgesv_26, launch_zgesv_27, launch_zgesv_28, launch_zgesv_29,
+    launch_zgesv_30,  launch_zgesv_31, launch_zgesv_32};
+
+tracker_launch_fn tracker_launcher(int N) { return (N >= 1 && N <= 32) ? kTrackers[N] : nullptr; }
+
+cudaError_t launch_batched_zgesv(int n, int64_t batch, const double2 *A, const double2 *b, double2 *x,
+                                 int32_t *info, double pivot_rel, cudaStream_t s) {
+  if (n < 1 || n > 32) return cudaErrorInvalidValue;
+  if (batch == 0) return cudaSuccess;
+  return kZgesv[n](batch, A, b, x, info, pivot_rel, s);
+}
+}  // namespace hcb
+
+using namespace hcb;
+
+static thread_local std::string g_err;
+
+static hc_status fail(hc_status s, const std::string &msg) {
+  g_err = msg;
+  return s;
+}
+static hc_status cuda_fail(cudaError_t e, const char *where) {
+  g_err = std::string(where) + ": " + cudaGetErrorString(e);
+  return e == cudaErrorMemoryAllocation ? HC_E_OOM : HC_E_CUDA;
+}
+#define CK(call)                                   \
+  do {                                             \
+    cudaError_t _e = (call);                       \
+    if (_e != cudaSuccess) return cuda_fail(_e, #call); \
+  } while (0)
+
+struct hc_system_s {
+  int device = 0;
+  CompiledSystem cs;
+  uint4 *d_ops = nullptr;
+  uint8_t *d_nfac = nullptr;
+  CoefMono *d_mono = nullptr;
+  int32_t *d_mono_ptr = nullptr;
+  // total-degree metadata
+  bool td = false;
+  std::vector<hc_complex> td_fvals;
+  std::vector<int32_t> td_degrees;
+};
+
+struct hc_result_s {
+  hc_system sys = nullptr;   // must outlive the result (documented in hc.h)
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  int64_t B = 0, S = 0, total = 0;
+  int memory = HC_MEM_DEVICE;
+  cudaEvent_t ev[3] = {nullptr, nullptr, nullptr};
+  // device buffers owned by the result (freed on destroy)
+  std::vector<void *> owned;
+  // where the outputs are (device or host)
+  hc_complex *x = nullptr;
+  int32_t *status = nullptr, *counters = nullptr;
+  double *resid = nullptr;
+  bool outputs_on_host = false;
+  bool waited = false;
+};
+
+static void destroy_result(hc_result r) {
+  if (!r) return;
+  cudaSetDevice(r->device);
+  for (void *p : r->owned) cudaFreeAsync(p, r->stream);
+  for (auto &e : r->ev)
+    if (e) cudaEventDestroy(e);
+  if (r->outputs_on_host) {
+  }
+  delete r;
+}
+
+template <class T>
+static hc_status dev_alloc(hc_result r, T **p, size_t count) {
+  void *q = nullptr;
+  cudaError_t e = cudaMallocAsync(&q, std::max<size_t>(1, count) * sizeof(T), r->stream);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaMallocAsync");
+  r->owned.push_back(q);
+  *p = reinterpret_cast<T *>(q);
+  return HC_OK;
+}
+
+extern "C" {
+
+const char *hc_last_error(void) { return g_err.c_str(); }
+const char *hc_version(void) { return "hc-b200 0.1 (sm_100a)"; }
+
+hc_status hc_tracker_settings_default(hc_tracker_settings *s) {
+  if (!s) return fail(HC_E_INVALID_ARG, "null settings");
+  // SURVEY.md §8(c) readings R5-R10 (the paper fixes none of these constants).
+  s->predictor = HC_RK4;
+  s->dt_init = 0.01;
+  s->dt_min = 1e-14;
+  s->dt_max = 0.1;
+  s->grow_after = 4;
+  s->grow = 2.0;
+  s->shrink = 0.5;
+  s->max_newton = 3;
+  s->newton_tol = 1e-8;
+  s->max_steps = 10000;
+  s->inf_norm = 1e14;
+  s->end_newton = 3;
+  s->end_tol = 1e-12;
+  s->res_abs = 1e-10;
+  s->res_rel = 1e-12;
+  s->pivot_rel = 1e-14;
+  return HC_OK;
+}
+
+static hc_status upload_system(hc_system sys) {
+  CompiledSystem &cs = sys->cs;
+  CK(cudaSetDevice(sys->device));
+  CK(cudaMalloc(&sys->d_ops, sizeof(uint4) * std::max<size_t>(1, cs.ops.size())));
+  CK(cudaMalloc(&sys->d_nfac, std::max<size_t>(1, cs.step_nfac.size())));
+  CK(cudaMalloc(&sys->d_mono, sizeof(CoefMono) * std::max<size_t>(1, cs.mono.size())));
+  CK(cudaMalloc(&sys->d_mono_ptr, sizeof(int32_t) * cs.mono_ptr.size()));
+  if (!cs.ops.empty()) CK(cudaMemcpy(sys->d_ops, cs.ops.data(), sizeof(uint4) * cs.ops.size(), cudaMemcpyHostToDevice));
+  if (!cs.step_nfac.empty()) CK(cudaMemcpy(sys->d_nfac, cs.step_nfac.data(), cs.step_nfac.size(), cudaMemcpyHostToDevice));
+  if (!cs.mono.empty())
+    CK(cudaMemcpy(sys->d_mono, cs.mono.data(), sizeof(CoefMono) * cs.mono.size(), cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(sys->d_mono_ptr, cs.mono_ptr.data(), sizeof(int32_t) * cs.mono_ptr.size(), cudaMemcpyHostToDevice));
+  return HC_OK;
+}
+
+static void free_system(hc_system sys) {
+  if (!sys) return;
+  cudaSetDevice(sys->device);
+  cudaFree(sys->d_ops);
+  cudaFree(sys->d_nfac);
+  cudaFree(sys->d_mono);
+  cudaFree(sys->d_mono_ptr);
+  delete sys;
+}
+
+hc_status hc_system_create(const hc_system_desc *desc, int device, hc_system *out) {
+  if (!desc || !out) return fail(HC_E_INVALID_ARG, "null argument");
+  *out = nullptr;
+  hc_system sys = new (std::nothrow) hc_system_s();
+  if (!sys) return fail(HC_E_OOM, "host allocation failed");
+  sys->device = device;
+  std::string err;
+  hc_status s = compile_system(*desc, sys->cs, err);
+  if (s != HC_OK) {
+    delete sys;
+    return fail(s, err);
+  }
+  s = upload_system(sys);
+  if (s != HC_OK) {
+    free_system(sys);
+    return s;
+  }
+  *out = sys;
+  return HC_OK;
+}
+
+hc_status hc_system_create_total_degree(const hc_system_desc *target, int device, hc_system *out) {
+  if (!target || !out) return fail(HC_E_INVALID_ARG, "null argument");
+  *out = nullptr;
+  OwnedDesc od;
+  std::vector<hc_complex> fvals;
+  std::vector<int32_t> degrees;
+  std::string err;
+  hc_status s = total_degree_desc(*target, od, fvals, degrees, err);
+  if (s != HC_OK) return fail(s, err);
+  hc_system_desc v = od.view();
+  s = hc_system_create(&v, device, out);
+  if (s != HC_OK) return s;
+  (*out)->td = true;
+  (*out)->td_fvals = fvals;
+  (*out)->td_degrees = degrees;
+  return HC_OK;
+}
+
+hc_status hc_total_degree_params(hc_system sys, hc_complex gamma, hc_complex *p0, hc_complex *p1) {
+  if (!sys || !p0 || !p1) return fail(HC_E_INVALID_ARG, "null argument");
+  if (!sys->td) return fail(HC_E_INVALID_ARG, "not a total-degree system");
+  if (!std::isfinite(gamma.re) || !std::isfinite(gamma.im) || (gamma.re == 0.0 && gamma.im == 0.0))
+    return fail(HC_E_INVALID_ARG, "gamma must be finite and non-zero");
+  const int N = sys->cs.N, P = sys->cs.P;
+  // H = F~(x; (1-t) p0 + t p1) = (1-t) gamma G + t F  (Eq. 1 with gamma, R1)
+  for (int q = 0; q < P; ++q) p0[q] = p1[q] = hc_complex{0.0, 0.0};
+  for (int i = 0; i < N; ++i) {
+    p0[i] = gamma;                                     // gamma * x_i^{d_i}
+    p0[N + i] = hc_complex{-gamma.re, -gamma.im};      // gamma * (-1)
+  }
+  for (size_t j = 0; j < sys->td_fvals.size(); ++j) p1[2 * N + j] = sys->td_fvals[j];
+  return HC_OK;
+}
+
+int64_t hc_total_degree_count(hc_system sys) {
+  if (!sys || !sys->td) return -1;
+  int64_t c = 1;
+  for (int d : sys->td_degrees) {
+    c *= d;
+    if (c > (1LL << 31)) return -1;
+  }
+  return c;
+}
+
+hc_status hc_total_degree_start(hc_system sys, hc_complex *x) {
+  if (!sys || !x) return fail(HC_E_INVALID_ARG, "null argument");
+  if (!sys->td) return fail(HC_E_INVALID_ARG, "not a total-degree system");
+  const int64_t cnt = hc_total_degree_count(sys);
+  if (cnt < 0) return fail(HC_E_TOO_LARGE, "Bezout number exceeds 2^31");
+  const int N = sys->cs.N;
+  for (int64_t g = 0; g < cnt; ++g) {
+    int64_t rem = g;
+    for (int i = 0; i < N; ++i) {
+      const int d = sys->td_degrees[i];
+      const int k = (int)(rem % d);
+      rem /= d;
+      // exp(2 pi i k / d); quarter turns exact (reading R2)
+      const int num = 4 * k;   // angle in quarter turns = 4k/d
+      double c, s;
+      if (num % d == 0) {
+        const int qt = (num / d) & 3;
+        c = (qt == 0) ? 1.0 : (qt == 2 ? -1.0 : 0.0);
+        s = (qt == 1) ? 1.0 : (qt == 3 ? -1.0 : 0.0);
+      } else {
+        const double ang = 2.0 * M_PI * (double)k / (double)d;
+        c = std::cos(ang);
+        s = std::sin(ang);
+      }
+      x[g * N + i] = hc_complex{c, s};
+    }
+  }
+  return HC_OK;
+}
+
+static void fill_info(const CompiledSystem &cs, hc_system_info *o) {
+  std::memset(o, 0, sizeof(*o));
+  o->n_vars = cs.N;
+  o->n_params = cs.P;
+  o->n_coefs = cs.ncoef;
+  o->coef_degree_t = cs.D;
+  o->lanes_per_track = cs.L;
+  o->tracks_per_warp = 32 / cs.L;
+  o->op_steps = cs.Q;
+  o->max_factors = cs.M;
+  o->n_ops_J = cs.n_ops_J;
+  o->n_ops_rhs = cs.n_ops_rhs;
+  o->n_terms = cs.n_terms;
+  o->flops_coef = cs.flops_coef;
+  o->flops_eval = cs.flops_eval;
+  o->flops_lu = cs.flops_lu;
+  o->flops_solve = cs.flops_solve;
+  const int N = cs.N;
+  o->smem_per_track = (int64_t)(((16 * (2 * cs.ncoef + (N + 1) + N * (N + 1) + (N + 1)) + 8 * N) + 15) & ~15);
+}
+
+hc_status hc_system_info_get(hc_system sys, hc_system_info *o) {
+  if (!sys || !o) return fail(HC_E_INVALID_ARG, "null argument");
+  fill_info(sys->cs, o);
+  return HC_OK;
+}
+
+hc_status hc_system_compile_info(const hc_system_desc *desc, hc_system_info *o) {
+  if (!desc || !o) return fail(HC_E_INVALID_ARG, "null argument");
+  CompiledSystem cs;
+  std::string err;
+  hc_status s = compile_system(*desc, cs, err);
+  if (s != HC_OK) return fail(s, err);
+  fill_info(cs, o);
+  return HC_OK;
+}
+
+hc_status hc_system_compile_ops(const hc_system_desc *desc, uint32_t *ops, uint8_t *step_nfac, int64_t capacity) {
+  if (!desc) return fail(HC_E_INVALID_ARG, "null argument");
+  CompiledSystem cs;
+  std::string err;
+  hc_status s = compile_system(*desc, cs, err);
+  if (s != HC_OK) return fail(s, err);
+  if ((int64_t)cs.ops.size() > capacity) return fail(HC_E_INVALID_ARG, "capacity too small");
+  if (ops) std::memcpy(ops, cs.ops.data(), sizeof(uint4) * cs.ops.size());
+  if (step_nfac) std::memcpy(step_nfac, cs.step_nfac.data(), cs.step_nfac.size());
+  return HC_OK;
+}
+
+hc_status hc_system_destroy(hc_system sys) {
+  free_system(sys);
+  return HC_OK;
+}
+
+static hc_status check_settings(const hc_tracker_settings &s) {
+  if (s.predictor != HC_RK4 && s.predictor != HC_EULER) return fail(HC_E_INVALID_ARG, "predictor");
+  if (!(s.dt_min > 0 && s.dt_min <= s.dt_init && s.dt_init <= s.dt_max && s.dt_max <= 1.0))
+    return fail(HC_E_INVALID_ARG, "need 0 < dt_min <= dt_init <= dt_max <= 1");
+  if (!(s.grow > 1.0) || !(s.shrink > 0.0 && s.shrink < 1.0)) return fail(HC_E_INVALID_ARG, "grow > 1, 0 < shrink < 1");
+  if (s.grow_after < 1 || s.max_newton < 1 || s.max_steps < 1 || s.end_newton < 0)
+    return fail(HC_E_INVALID_ARG, "iteration counts");
+  if (!(s.newton_tol > 0) || !(s.inf_norm > 0) || !(s.end_tol > 0) || !(s.pivot_rel >= 0))
+    return fail(HC_E_INVALID_ARG, "tolerances");
+  return HC_OK;
+}
+
+static bool aligned16(const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
+hc_status hc_track_batch(hc_system sys, const hc_tracker_settings *settings, const hc_batch *bt, hc_result *out) {
+  if (out) *out = nullptr;
+  if (!sys || !bt) return fail(HC_E_INVALID_ARG, "null argument");
+  hc_tracker_settings st;
+  if (settings) st = *settings;
+  else hc_tracker_settings_default(&st);
+  hc_status s = check_settings(st);
+  if (s != HC_OK) return s;
+  const CompiledSystem &cs = sys->cs;
+  const int N = cs.N, P = cs.P;
+  if (bt->n_instances < 1 || bt->n_start < 1) return fail(HC_E_INVALID_ARG, "n_instances and n_start must be >= 1");
+  if (bt->n_instances > (1LL << 40) / bt->n_start) return fail(HC_E_TOO_LARGE, "too many tracks");
+  if (!bt->start_x) return fail(HC_E_INVALID_ARG, "start_x is null");
+  if (P > 0 && (!bt->p_start || !bt->p_target)) return fail(HC_E_INVALID_ARG, "p_start / p_target null with P > 0");
+  if (bt->memory != HC_MEM_DEVICE && bt->memory != HC_MEM_HOST) return fail(HC_E_INVALID_ARG, "memory");
+  const bool host = bt->memory == HC_MEM_HOST;
+  if (!host) {
+    for (const void *p : {(const void *)bt->start_x, (const void *)bt->p_start, (const void *)bt->p_target,
+                          (const void *)bt->x_out, (const void *)bt->counters_out, (const void *)bt->resid_out})
+      if (p && !aligned16(p)) return fail(HC_E_INVALID_ARG, "device buffers must be 16-byte aligned");
+  }
+  const int64_t B = bt->n_instances, S = bt->n_start, total = B * S;
+
+  CK(cudaSetDevice(sys->device));
+  (void)cudaGetLastError();   // clear a stale error left by a foreign caller
+  hc_result r = new (std::nothrow) hc_result_s();
+  if (!r) return fail(HC_E_OOM, "host allocation failed");
+  r->sys = sys;
+  r->device = sys->device;
+  r->stream = reinterpret_cast<cudaStream_t>(bt->stream);
+  r->B = B;
+  r->S = S;
+  r->total = total;
+  r->memory = bt->memory;
+  auto bail = [&](hc_status e) {
+    destroy_result(r);
+    return e;
+  };
+  for (auto &e : r->ev)
+    if (cudaEventCreate(&e) != cudaSuccess) return bail(cuda_fail(cudaGetLastError(), "cudaEventCreate"));
+
+  // ---- inputs on the device ----
+  const double2 *d_start = reinterpret_cast<const double2 *>(bt->start_x);
+  const double2 *d_p0 = reinterpret_cast<const double2 *>(bt->p_start);
+  const double2 *d_p1 = reinterpret_cast<const double2 *>(bt->p_target);
+  double2 *d_x = reinterpret_cast<double2 *>(bt->x_out);
+  int32_t *d_status = bt->status_out, *d_ctr = bt->counters_out;
+  double *d_resid = bt->resid_out;
+  if (host) {
+    double2 *a, *b0 = nullptr, *b1 = nullptr;
+    if ((s = dev_alloc(r, &a, (size_t)S * N)) != HC_OK) return bail(s);
+    if (cudaMemcpyAsync(a, bt->start_x, sizeof(double2) * S * N, cudaMemcpyHostToDevice, r->stream) != cudaSuccess)
+      return bail(cuda_fail(cudaGetLastError(), "H2D start_x"));
+    d_start = a;
+    if (P > 0) {
+      if ((s = dev_alloc(r, &b0, (size_t)P)) != HC_OK) return bail(s);
+      if ((s = dev_alloc(r, &b1, (size_t)B * P)) != HC_OK) return bail(s);
+      if (cudaMemcpyAsync(b0, bt->p_start, sizeof(double2) * P, cudaMemcpyHostToDevice, r->stream) != cudaSuccess ||
+          cudaMemcpyAsync(b1, bt->p_target, sizeof(double2) * B * P, cudaMemcpyHostToDevice, r->stream) != cudaSuccess)
+        return bail(cuda_fail(cudaGetLastError(), "H2D params"));
+      d_p0 = b0;
+      d_p1 = b1;
+    }
+    d_x = nullptr;
+    d_status = nullptr;
+    d_ctr = nullptr;
+    d_resid = nullptr;
+  }
+  if (!d_x && (s = dev_alloc(r, &d_x, (size_t)total * N)) != HC_OK) return bail(s);
+  if (!d_status && (s = dev_alloc(r, &d_status, (size_t)total)) != HC_OK) return bail(s);
+  if (!d_ctr && (s = dev_alloc(r, &d_ctr, (size_t)total * 4)) != HC_OK) return bail(s);
+  if (!d_resid && (s = dev_alloc(r, &d_resid, (size_t)total * 2)) != HC_OK) return bail(s);
+  double2 *d_coef = nullptr;
+  unsigned long long *d_queue = nullptr;
+  if ((s = dev_alloc(r, &d_coef, (size_t)B * (cs.D + 1) * cs.ncoef)) != HC_OK) return bail(s);
+  if ((s = dev_alloc(r, &d_queue, 1)) != HC_OK) return bail(s);
+  if (cudaMemsetAsync(d_queue, 0, sizeof(unsigned long long), r->stream) != cudaSuccess)
+    return bail(cuda_fail(cudaGetLastError(), "memset queue"));
+  // P == 0: coefficients are constants; feed the prologue a dummy parameter vector
+  double2 *d_dummy = nullptr;
+  if (P == 0) {
+    if ((s = dev_alloc(r, &d_dummy, 1)) != HC_OK) return bail(s);
+    d_p0 = d_dummy;
+    d_p1 = d_dummy;
+  }
+
+  // ---- prologue: per-instance coefficient polynomials in t ----
+  PrologueArgs pa{};
+  pa.mono = sys->d_mono;
+  pa.coef_mono_ptr = sys->d_mono_ptr;
+  pa.ncoef = cs.ncoef;
+  pa.D = cs.D;
+  pa.P = P;
+  pa.p0 = d_p0;
+  pa.p1 = d_p1;
+  pa.B = B;
+  pa.coef_t = d_coef;
+  cudaEventRecord(r->ev[0], r->stream);
+  cudaError_t e = launch_prologue(pa, r->stream);
+  if (e != cudaSuccess) return bail(cuda_fail(e, "coef prologue launch"));
+  cudaEventRecord(r->ev[1], r->stream);
+
+  // ---- the fused tracker ----
+  TrackArgs ta{};
+  ta.ops = sys->d_ops;
+  ta.step_nfac = sys->d_nfac;
+  ta.Q = cs.Q;
+  ta.ncoef = cs.ncoef;
+  ta.D = cs.D;
+  ta.coef_t = d_coef;
+  ta.start_x = d_start;
+  ta.S = S;
+  ta.total = total;
+  ta.queue = d_queue;
+  ta.x_out = d_x;
+  ta.status_out = d_status;
+  ta.counters_out = d_ctr;
+  ta.resid_out = d_resid;
+  ta.st.dt_init = st.dt_init;
+  ta.st.dt_min = st.dt_min;
+  ta.st.dt_max = st.dt_max;
+  ta.st.grow = st.grow;
+  ta.st.shrink = st.shrink;
+  ta.st.newton_tol = st.newton_tol;
+  ta.st.inf_norm = st.inf_norm;
+  ta.st.end_tol = st.end_tol;
+  ta.st.res_abs = st.res_abs;
+  ta.st.res_rel = st.res_rel;
+  ta.st.pivot_rel = st.pivot_rel;
+  ta.st.predictor = st.predictor;
+  ta.st.grow_after = st.grow_after;
+  ta.st.max_newton = st.max_newton;
+  ta.st.max_steps = st.max_steps;
+  ta.st.end_newton = st.end_newton;
+  TrackerPlan plan{};
+  e = tracker_launcher(N)(ta, sys->device, r->stream, &plan);
+  if (e != cudaSuccess) return bail(cuda_fail(e, "tracker launch"));
+  cudaEventRecord(r->ev[2], r->stream);
+
+  if (host) {
+    if (bt->x_out &&
+        cudaMemcpyAsync(bt->x_out, d_x, sizeof(double2) * total * N, cudaMemcpyDeviceToHost, r->stream) != cudaSuccess)
+      return bail(cuda_fail(cudaGetLastError(), "D2H x"));
+    if (bt->status_out &&
+        cudaMemcpyAsync(bt->status_out, d_status, sizeof(int32_t) * total, cudaMemcpyDeviceToHost, r->stream) != cudaSuccess)
+      return bail(cuda_fail(cudaGetLastError(), "D2H status"));
+    if (bt->counters_out && cudaMemcpyAsync(bt->counters_out, d_ctr, sizeof(int32_t) * total * 4,
+                                            cudaMemcpyDeviceToHost, r->stream) != cudaSuccess)
+      return bail(cuda_fail(cudaGetLastError(), "D2H counters"));
+    if (bt->resid_out && cudaMemcpyAsync(bt->resid_out, d_resid, sizeof(double) * total * 2,
+                                         cudaMemcpyDeviceToHost, r->stream) != cudaSuccess)
+      return bail(cuda_fail(cudaGetLastError(), "D2H resid"));
+    if (cudaStreamSynchronize(r->stream) != cudaSuccess) return bail(cuda_fail(cudaGetLastError(), "sync"));
+    r->waited = true;
+  }
+  r->x = reinterpret_cast<hc_complex *>(d_x);
+  r->status = d_status;
+  r->counters = d_ctr;
+  r->resid = d_resid;
+  if (out) *out = r;
+  else if (!host) {
+    // fire-and-forget: the caller owns all outputs; release our buffers after the stream passes
+    destroy_result(r);
+  } else {
+    destroy_result(r);
+  }
+  return HC_OK;
+}
+
+hc_status hc_result_wait(hc_result r) {
+  if (!r) return fail(HC_E_INVALID_ARG, "null result");
+  CK(cudaSetDevice(r->device));
+  CK(cudaEventSynchronize(r->ev[2]));
+  r->waited = true;
+  return HC_OK;
+}
+
+hc_status hc_result_elapsed_ms(hc_result r, float *total, float *prologue, float *tracker) {
+  if (!r) return fail(HC_E_INVALID_ARG, "null result");
+  hc_status s = hc_result_wait(r);
+  if (s != HC_OK) return s;
+  float a = 0, b = 0, c = 0;
+  CK(cudaEventElapsedTime(&a, r->ev[0], r->ev[2]));
+  CK(cudaEventElapsedTime(&b, r->ev[0], r->ev[1]));
+  CK(cudaEventElapsedTime(&c, r->ev[1], r->ev[2]));
+  if (total) *total = a;
+  if (prologue) *prologue = b;
+  if (tracker) *tracker = c;
+  return HC_OK;
+}
+
+hc_status hc_result_get(hc_result r, int64_t instance, int64_t track, hc_complex *x, hc_track_info *info) {
+  if (!r) return fail(HC_E_INVALID_ARG, "null result");
+  if (instance < 0 || instance >= r->B || track < 0 || track >= r->S) return fail(HC_E_INVALID_ARG, "index out of range");
+  hc_status s = hc_result_wait(r);
+  if (s != HC_OK) return s;
+  const int N = r->sys->cs.N;
+  const int64_t g = instance * r->S + track;
+  if (x) CK(cudaMemcpy(x, r->x + g * N, sizeof(hc_complex) * N, cudaMemcpyDeviceToHost));
+  if (info) {
+    int32_t c[4], st;
+    double rs[2];
+    CK(cudaMemcpy(&st, r->status + g, sizeof(int32_t), cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(c, r->counters + 4 * g, sizeof(c), cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(rs, r->resid + 2 * g, sizeof(rs), cudaMemcpyDeviceToHost));
+    info->status = st;
+    info->steps = c[0];
+    info->rejections = c[1];
+    info->newton_iters = c[2];
+    info->solves = c[3];
+    info->resid_abs = rs[0];
+    info->resid_rel = rs[1];
+  }
+  return HC_OK;
+}
+
+hc_status hc_result_destroy(hc_result r) {
+  destroy_result(r);
+  return HC_OK;
+}
+
+hc_status hc_batched_zgesv(int32_t n, int64_t batch, const hc_complex *A, const hc_complex *b, hc_complex *x,
+                           int32_t *info, double pivot_rel, void *stream) {
+  if (n < 1 || n > 32) return fail(n > 32 ? HC_E_TOO_LARGE : HC_E_INVALID_ARG, "n must be in [1, 32]");
+  if (batch < 0) return fail(HC_E_INVALID_ARG, "batch < 0");
+  if (batch > 0 && (!A || !b || !x || !info)) return fail(HC_E_INVALID_ARG, "null pointer");
+  cudaError_t e = launch_batched_zgesv(n, batch, reinterpret_cast<const double2 *>(A),
+                                       reinterpret_cast<const double2 *>(b), reinterpret_cast<double2 *>(x), info,
+                                       pivot_rel, reinterpret_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "batched zgesv");
+  return HC_OK;
+}
+
+hc_status hc_fp64_peak_probe(int device, double *tflops) {
+  if (!tflops) return fail(HC_E_INVALID_ARG, "null");
+  cudaError_t e = run_fp64_probe(device, tflops);
+  if (e != cudaSuccess) return cuda_fail(e, "fp64 probe");
+  return HC_OK;
+}
+
+}  // extern "C"

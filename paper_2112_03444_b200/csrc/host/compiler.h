@@ -1,0 +1,42 @@
+// compiler.h -- host-side system compiler: descriptor -> homogenised, lane-balanced evaluation
+// tables (the paper's "indexing system") + coefficient-polynomial monomials.
+#pragma once
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "../hc_internal.h"
+
+namespace hcb {
+
+struct CompiledSystem {
+  int N = 0, P = 0, ncoef = 0, D = 0;
+  int L = 1, Q = 0, M = 0;
+  int n_ops_J = 0, n_ops_rhs = 0, n_terms = 0;
+  std::vector<uint4> ops;          // [Q * L]
+  std::vector<uint8_t> step_nfac;  // [Q]
+  std::vector<CoefMono> mono;      // sorted by coef
+  std::vector<int32_t> mono_ptr;   // [ncoef + 1]
+  std::vector<int32_t> degrees;    // total degree of each equation
+  int64_t flops_coef = 0, flops_eval = 0, flops_lu = 0, flops_solve = 0;
+};
+
+// Returns HC_OK or an error code with a message in `err`.
+hc_status compile_system(const hc_system_desc &d, CompiledSystem &out, std::string &err);
+
+// Descriptor of the total-degree homotopy system built from a constant-coefficient target
+// (SURVEY.md §8(b) "Total degree is a PH"): params = (G x^d coefficients [N], G constants [N],
+// target coefficient values [ncoef]).  `fvals` receives the target's coefficient values.
+struct OwnedDesc {
+  int32_t n_vars = 0, n_params = 0, n_terms = 0, n_coefs = 0;
+  std::vector<int32_t> term_eq, term_xexp, term_coef, coef_ptr, coef_pexp;
+  std::vector<hc_complex> coef_w;
+  hc_system_desc view() const;
+};
+hc_status total_degree_desc(const hc_system_desc &target, OwnedDesc &out, std::vector<hc_complex> &fvals,
+                            std::vector<int32_t> &degrees, std::string &err);
+
+int64_t lu_flops(int N);
+
+}  // namespace hcb

@@ -1,0 +1,444 @@
+// tracker.cuh -- the fused persistent HC path-tracking kernel for sm_100a (one template per N).
+//
+// One sub-warp of L = next_pow2(N) lanes owns one track ("a track to a warp", with
+// sub-warps when N <= 16); lane r owns Jacobian row r, right-hand-side entry r and unknown x_r
+// ("one row per thread").  Every loop iteration performs exactly one
+//     evaluate (dH/dx | rhs)  ->  fused LU + solve on [A | b]
+// per track slot, where the rhs is dH/dt (RK4 stage, Eq. 3 P:168 / P:175) or H (Newton, Eq. 6
+// P:182).  Each slot runs its own state machine (RK stage s, Newton iteration, endpoint polish,
+// residual), so slots of one warp never wait for each other, and the single solve call site keeps
+// the unrolled LU in the instruction cache once.  Finished slots pull the next track id from a
+// global atomic queue (persistent kernel); tracks are ordered instance-major so concurrently
+// running slots share an instance's coefficient table in L1/L2.
+//
+// Evaluation: the host compiler turned dH/dx, H and dH/dt into homogenised terms
+// (coef, scale, factor indices with a constant-one slot) and balanced them over the L lanes; the
+// table sits in shared memory for the whole kernel.  Coefficient values c_j(t), c_j'(t) come from
+// per-instance polynomials in t (prologue kernel) by Horner.  The LU keeps row r in lane r's
+// registers, pivots by a shuffle arg-max of |a|^2 (ties -> lower row), broadcasts the pivot row
+// through shared memory, and back-substitutes on the cached U with the pivot rows still held by
+// their lanes (kernel fusion + augmented matrix).
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "../hc_internal.h"
+
+namespace hcb {
+
+constexpr unsigned FULL = 0xffffffffu;
+constexpr int TRACKER_WARPS = 4;
+
+__device__ __forceinline__ double2 cmul(double2 a, double2 b) {
+  return make_double2(fma(a.x, b.x, -a.y * b.y), fma(a.x, b.y, a.y * b.x));
+}
+// c - a * b
+__device__ __forceinline__ double2 cfms(double2 c, double2 a, double2 b) {
+  return make_double2(fma(-a.x, b.x, fma(a.y, b.y, c.x)), fma(-a.x, b.y, fma(-a.y, b.x, c.y)));
+}
+__device__ __forceinline__ double abs2(double2 a) { return fma(a.x, a.x, a.y * a.y); }
+__device__ __forceinline__ double2 crecip(double2 a) {
+  double d = 1.0 / abs2(a);
+  return make_double2(a.x * d, -a.y * d);
+}
+__device__ __forceinline__ bool cfinite(double2 a) { return isfinite(a.x) && isfinite(a.y); }
+__device__ __forceinline__ double2 shfl2(double2 v, int src, int width) {
+  return make_double2(__shfl_sync(FULL, v.x, src, width), __shfl_sync(FULL, v.y, src, width));
+}
+
+template <int L>
+__device__ __forceinline__ double seg_max(double v) {
+#pragma unroll
+  for (int off = L / 2; off >= 1; off >>= 1) v = fmax(v, __shfl_xor_sync(FULL, v, off));
+  return v;
+}
+template <int L>
+__host__ __device__ constexpr unsigned seg_mask() {
+  if constexpr (L == 32) return FULL;
+  else return (1u << L) - 1u;
+}
+template <int L>
+__device__ __forceinline__ bool seg_all(bool p, int seg) {
+  const unsigned b = __ballot_sync(FULL, p);
+  const unsigned m = seg_mask<L>() << ((L == 32) ? 0 : seg * L);
+  return (b & m) == m;
+}
+
+__host__ __device__ inline size_t align16(size_t b) { return (b + 15) & ~size_t(15); }
+
+// Per-slot shared memory: cval[2*ncoef] (c(t), c'(t)), x[N+1], M[N*(N+1)], prow[N+1], rabs[N]
+__host__ __device__ inline size_t slot_bytes(int N, int ncoef) {
+  return align16(sizeof(double2) * (2 * ncoef + (N + 1) + N * (N + 1) + (N + 1)) + sizeof(double) * N);
+}
+
+enum SlotState : int { ST_RK = 0, ST_NEWTON = 1, ST_POLISH = 2, ST_RESID = 3, ST_DONE = 4 };
+
+// ------------------------------------------------------------------------------------------
+// Fused LU with partial pivoting + back-substitution on [A | b] held one row per lane
+// (a[0..N-1] = row r of A, a[N] = b_r).  Pivot = max |a|^2 over the not-yet-pivoted
+// rows (ties -> lower row, reading R13); the pivot row is broadcast through `prow` (shared);
+// singular when |pivot| <= pivot_rel * max|A_ij| (R9) or anything is non-finite.  Returns the
+// solution component y_r in lane r and a slot-uniform success flag.
+// ------------------------------------------------------------------------------------------
+template <int N, int L>
+__device__ __forceinline__ bool lu_rows(double2 (&a)[N + 1], int r, int seg, double2 *prow, double pivot_rel,
+                                        double2 &y) {
+  bool used = (r >= N);
+  int mystep = used ? N : -1;
+  double2 myinv = make_double2(0.0, 0.0);
+  double am = 0.0;
+#pragma unroll
+  for (int j = 0; j < N; ++j) am = fmax(am, abs2(a[j]));
+  am = seg_max<L>(am);
+  const double thr = pivot_rel * pivot_rel * am;
+  bool sing = !(am < INFINITY);
+#pragma unroll
+  for (int k = 0; k < N; ++k) {
+    double v = used ? -1.0 : abs2(a[k]);
+    if (!(v >= 0.0)) v = -1.0;  // NaN is never a pivot
+    int idx = r;
+#pragma unroll
+    for (int off = L / 2; off >= 1; off >>= 1) {
+      const double ov = __shfl_xor_sync(FULL, v, off);
+      const int oi = __shfl_xor_sync(FULL, idx, off);
+      if (ov > v || (ov == v && oi < idx)) {
+        v = ov;
+        idx = oi;
+      }
+    }
+    sing |= !(v > thr);
+    if (r == idx) {
+#pragma unroll
+      for (int j = k; j <= N; ++j) prow[j] = a[j];
+      used = true;
+      mystep = k;
+    }
+    __syncwarp();
+    const double2 inv = crecip(prow[k]);
+    if (r == idx) myinv = inv;
+    if (!used) {
+      const double2 l = cmul(a[k], inv);
+#pragma unroll
+      for (int j = k + 1; j <= N; ++j) a[j] = cfms(a[j], l, prow[j]);
+    }
+    __syncwarp();
+  }
+  // ---- back-substitution on the cached U: lane with mystep == k holds U row k ----
+  double2 sol = make_double2(0.0, 0.0);
+#pragma unroll
+  for (int k = N - 1; k >= 0; --k) {
+    const unsigned bal = __ballot_sync(FULL, mystep == k);
+    const unsigned segbits = (L == 32) ? bal : ((bal >> (seg * L)) & seg_mask<L>());
+    const int src = __ffs(segbits) - 1;
+    const double2 cand = (mystep == k) ? cmul(a[N], myinv) : make_double2(0.0, 0.0);
+    const double2 xk = shfl2(cand, src < 0 ? 0 : src, L);
+    if (mystep < k) a[N] = cfms(a[N], a[k], xk);
+    if (r == k) sol = xk;
+  }
+  y = sol;
+  return seg_all<L>(!sing && cfinite(sol), seg);
+}
+
+// ------------------------------------------------------------------------------------------
+// Evaluate [dH/dx | rhs] into the slot's M (shared), then fused LU + solve.  Returns the solution
+// component y_r in lane r (r < N) and whether the solve succeeded (uniform over the slot).
+// rhs_off = 0 -> rhs = H (coefficients c(t)); rhs_off = ncoef -> rhs = dH/dt (coefficients c'(t)).
+// When want_abs, rabs[i] = sum_k |c_k m_k(x)| over the rhs terms of row i (relative residual).
+// ------------------------------------------------------------------------------------------
+template <int N, int L>
+__device__ __forceinline__ bool eval_solve(const uint4 *__restrict__ ops_s, const uint8_t *__restrict__ nfac_s,
+                                           int Q, int ncoef, int D, const double2 *__restrict__ ct, double t,
+                                           int rhs_off, bool want_abs, double pivot_rel, double2 *cval,
+                                           double2 *xs, double2 *M, double2 *prow, double *rabs, int r, int seg,
+                                           double2 xr, double2 &y, double2 &fr, double &fabs_r) {
+  // ---- stage x and coefficient values c_j(t), c_j'(t) (Horner on the prologue's polynomials) ----
+  if (r < N) xs[r] = xr;
+  for (int j = r; j < ncoef; j += L) {
+    double2 p = __ldg(&ct[(size_t)D * ncoef + j]);
+    double2 dp = make_double2(0.0, 0.0);
+    for (int d = D - 1; d >= 0; --d) {
+      double2 a = __ldg(&ct[(size_t)d * ncoef + j]);
+      dp = make_double2(fma(dp.x, t, p.x), fma(dp.y, t, p.y));
+      p = make_double2(fma(p.x, t, a.x), fma(p.y, t, a.y));
+    }
+    cval[j] = p;
+    cval[ncoef + j] = dp;
+  }
+  __syncwarp();
+  // ---- homogenised term evaluation, lane-balanced op list ----
+  double2 acc = make_double2(0.0, 0.0);
+  double acc_abs = 0.0;
+  for (int q = 0; q < Q; ++q) {
+    const uint4 op = ops_s[q * L + r];
+    const int nf = nfac_s[q];
+    const int ci = (int)(op.x & 0xFFFFu) + ((op.y & OP_RHS) ? rhs_off : 0);
+    const double sc = (double)((op.y >> 8) & 0xFFu);
+    double2 v = cval[ci];
+    v.x *= sc;
+    v.y *= sc;
+#pragma unroll
+    for (int m = 0; m < MAX_FACTORS; ++m) {
+      if (m < nf) {
+        const uint32_t w = (m < 4) ? op.z : op.w;
+        v = cmul(v, xs[(w >> (8 * (m & 3))) & 0xFFu]);
+      }
+    }
+    acc.x += v.x;
+    acc.y += v.y;
+    if (want_abs) acc_abs += sqrt(abs2(v));
+    if (op.y & OP_LAST) {
+      const uint32_t dest = op.x >> 16;
+      M[dest] = acc;
+      if (want_abs && (op.y & OP_RHS)) rabs[dest / (N + 1)] = acc_abs;
+      acc = make_double2(0.0, 0.0);
+      acc_abs = 0.0;
+    }
+  }
+  __syncwarp();
+  // ---- load row r of [A | b] into registers ----
+  double2 a[N + 1];
+#pragma unroll
+  for (int j = 0; j <= N; ++j) a[j] = (r < N) ? M[r * (N + 1) + j] : make_double2(0.0, 0.0);
+  fr = a[N];
+  fabs_r = (r < N && want_abs) ? rabs[r] : 0.0;
+  return lu_rows<N, L>(a, r, seg, prow, pivot_rel, y);
+}
+
+// ------------------------------------------------------------------------------------------
+// The persistent tracker kernel.
+// ------------------------------------------------------------------------------------------
+template <int N>
+__global__ void __launch_bounds__(TRACKER_WARPS * 32) hc_track_kernel(const TrackArgs A) {
+  constexpr int L = (N <= 1) ? 1 : (N <= 2) ? 2 : (N <= 4) ? 4 : (N <= 8) ? 8 : (N <= 16) ? 16 : 32;
+  constexpr int TPW = 32 / L;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+
+  // ---- stage the op table in shared memory (constant for the whole kernel) ----
+  uint4 *ops_s = reinterpret_cast<uint4 *>(smem_raw);
+  const int nops = A.Q * L;
+  for (int i = threadIdx.x; i < nops; i += blockDim.x) ops_s[i] = __ldg(&A.ops[i]);
+  uint8_t *nfac_s = reinterpret_cast<uint8_t *>(ops_s + nops);
+  for (int i = threadIdx.x; i < A.Q; i += blockDim.x) nfac_s[i] = A.step_nfac[i];
+  unsigned char *slots_base = smem_raw + align16(sizeof(uint4) * nops + A.Q);
+
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int seg = lane / L, r = lane % L;
+  const int slot = warp * TPW + seg;
+  const int ncoef = A.ncoef, D = A.D;
+  unsigned char *sb = slots_base + (size_t)slot * slot_bytes(N, ncoef);
+  double2 *cval = reinterpret_cast<double2 *>(sb);
+  double2 *xs = cval + 2 * ncoef;
+  double2 *M = xs + (N + 1);
+  double2 *prow = M + N * (N + 1);
+  double *rabs = reinterpret_cast<double *>(prow + (N + 1));
+  // structural zeros of [A | b] are never written by the op list: zero M once.
+  for (int i = r; i < N * (N + 1); i += L) M[i] = make_double2(0.0, 0.0);
+  if (r == 0) xs[N] = make_double2(1.0, 0.0);   // constant-one slot
+  __syncthreads();
+
+  const DevSettings &st = A.st;
+  const int n_rk = (st.predictor == HC_EULER) ? 1 : 4;
+
+  // ---- slot state (replicated over the slot's lanes) ----
+  int state = ST_DONE;
+  long long g = -1;
+  const double2 *ct = A.coef_t;   // instance coefficient table
+  double t = 0.0, dt = 0.0, h = 0.0, t1 = 0.0;
+  int stage = 0, it = 0, acc = 0, steps = 0, rej = 0, newt = 0, solves = 0;
+  double2 x = make_double2(0.0, 0.0), kacc = x, kprev = x, xc = x;
+  bool need_track = true;
+
+  // begin a step attempt from (x, t) with dt; returns false when max_steps is exhausted
+  auto begin_step = [&]() -> bool {
+    if (steps >= st.max_steps) return false;
+    ++steps;
+    h = dt;
+    t1 = t + dt;
+    if (t1 >= 1.0) {
+      t1 = 1.0;
+      h = 1.0 - t;
+    }
+    stage = 0;
+    kacc = make_double2(0.0, 0.0);
+    kprev = make_double2(0.0, 0.0);
+    state = ST_RK;
+    return true;
+  };
+  auto finish = [&](int status, double ra, double rr) {
+    if (r < N) A.x_out[(size_t)g * N + r] = x;
+    if (r == 0) {
+      A.status_out[g] = status;
+      int4 c = make_int4(steps, rej, newt, solves);
+      reinterpret_cast<int4 *>(A.counters_out)[g] = c;
+      reinterpret_cast<double2 *>(A.resid_out)[g] = make_double2(ra, rr);
+    }
+    need_track = true;
+    state = ST_DONE;
+  };
+
+  for (;;) {
+    // ---- refill: slots without a track pull the next id (instance-major).  The shuffle runs on
+    //      all 32 lanes (warp collectives are never inside slot-divergent branches). ----
+    {
+      unsigned long long got = 0;
+      if (need_track && r == 0) got = atomicAdd(A.queue, 1ULL);
+      got = __shfl_sync(FULL, got, seg * L);
+      if (need_track) {
+        need_track = false;
+        if ((long long)got < A.total) {
+          g = (long long)got;
+          const long long b = g / A.S, s = g % A.S;
+          ct = A.coef_t + (size_t)b * (D + 1) * ncoef;
+          x = (r < N) ? A.start_x[s * N + r] : make_double2(0.0, 0.0);
+          t = 0.0;
+          dt = st.dt_init;
+          acc = steps = rej = newt = solves = 0;
+          begin_step();
+        } else {
+          state = ST_DONE;
+          ct = A.coef_t;
+          g = -1;
+        }
+      }
+    }
+    if (__all_sync(FULL, state == ST_DONE)) break;
+
+    // ---- what this slot evaluates in this iteration ----
+    double te;
+    double2 xe;
+    int rhs_off = 0;
+    if (state == ST_RK) {
+      const double c = (stage == 0) ? 0.0 : (stage == 3 ? 1.0 : 0.5);
+      te = t + c * h;
+      xe = make_double2(fma(c * h, kprev.x, x.x), fma(c * h, kprev.y, x.y));
+      rhs_off = ncoef;  // rhs = dH/dt
+    } else if (state == ST_NEWTON) {
+      te = t1;
+      xe = xc;
+    } else if (state == ST_POLISH || state == ST_RESID) {
+      te = 1.0;
+      xe = x;
+    } else {
+      te = 0.0;
+      xe = make_double2(0.0, 0.0);
+    }
+    const bool want_abs = __any_sync(FULL, state == ST_RESID);
+    double2 yv, fr;
+    double fa;
+    const bool ok = eval_solve<N, L>(ops_s, nfac_s, A.Q, ncoef, D, ct, te, rhs_off, want_abs, st.pivot_rel, cval,
+                                     xs, M, prow, rabs, r, seg, xe, yv, fr, fa);
+
+    // ---- slot-uniform reductions, computed on all lanes before any slot-divergent branch ----
+    const double2 base = (state == ST_POLISH) ? x : xc;
+    const double2 cand = make_double2(base.x - yv.x, base.y - yv.y);   // Newton update x - dx
+    const bool cand_fin = seg_all<L>(cfinite(cand), seg);
+    const double d2 = seg_max<L>(abs2(yv));
+    const double c2 = seg_max<L>(abs2(cand));
+    const double fm = (r < N) ? sqrt(abs2(fr)) : 0.0;
+    const double fq = (r < N) ? (fa > 0.0 ? fm / fa : (fm == 0.0 ? 0.0 : INFINITY)) : 0.0;
+    const double res_abs = seg_max<L>(fm), res_rel = seg_max<L>(fq);
+
+    // ---- advance the slot's state machine ----
+    if (state == ST_DONE) continue;
+    if (state != ST_RESID) ++solves;
+    bool accept = false, reject = false;
+    if (state == ST_RK) {
+      if (!ok) {
+        reject = true;
+      } else {
+        const double2 k = make_double2(-yv.x, -yv.y);
+        const double w = (stage == 0 || stage == 3) ? 1.0 : 2.0;
+        kacc = make_double2(fma(w, k.x, kacc.x), fma(w, k.y, kacc.y));
+        kprev = k;
+        if (stage + 1 < n_rk) {
+          ++stage;
+        } else {
+          if (n_rk == 1) {
+            xc = make_double2(fma(h, k.x, x.x), fma(h, k.y, x.y));
+          } else {
+            const double h6 = h / 6.0;
+            xc = make_double2(fma(h6, kacc.x, x.x), fma(h6, kacc.y, x.y));
+          }
+          state = ST_NEWTON;
+          it = 0;
+        }
+      }
+    } else if (state == ST_NEWTON) {
+      ++newt;
+      if (!ok || !cand_fin) {
+        reject = true;
+      } else {
+        xc = cand;
+        if (d2 <= st.newton_tol * st.newton_tol * fmax(1.0, c2)) accept = true;
+        else if (++it >= st.max_newton) reject = true;
+      }
+    } else if (state == ST_POLISH) {
+      if (!ok) {
+        state = ST_RESID;
+      } else {
+        x = cand;
+        if (!cand_fin) {
+          finish(HC_NONFINITE, INFINITY, INFINITY);
+        } else if (d2 <= st.end_tol * st.end_tol * fmax(1.0, c2) || ++it >= st.end_newton) {
+          state = ST_RESID;
+        }
+      }
+    } else {  // ST_RESID: classify the endpoint (reading R10)
+      const int status = (res_abs <= st.res_abs || res_rel <= st.res_rel) ? HC_CONVERGED : HC_SINGULAR;
+      finish(status, res_abs, res_rel);
+    }
+    if (accept) {
+      x = xc;
+      t = t1;
+      if (++acc >= st.grow_after) {
+        dt = fmin(dt * st.grow, st.dt_max);
+        acc = 0;
+      }
+      if (c2 > st.inf_norm * st.inf_norm) {   // c2 = ||xc||^2 of the accepted point
+        finish(HC_DIVERGED, INFINITY, INFINITY);
+      } else if (t >= 1.0) {
+        state = ST_POLISH;
+        it = 0;
+      } else if (!begin_step()) {
+        finish(HC_MAX_STEPS, INFINITY, INFINITY);
+      }
+    } else if (reject) {
+      ++rej;
+      acc = 0;
+      dt *= st.shrink;
+      if (dt < st.dt_min) finish(HC_STEP_UNDERFLOW, INFINITY, INFINITY);
+      else if (!begin_step()) finish(HC_MAX_STEPS, INFINITY, INFINITY);
+    }
+  }
+}
+
+template <int N>
+cudaError_t launch_tracker_n(const TrackArgs &A, int device, cudaStream_t stream, TrackerPlan *plan) {
+  constexpr int L = (N <= 1) ? 1 : (N <= 2) ? 2 : (N <= 4) ? 4 : (N <= 8) ? 8 : (N <= 16) ? 16 : 32;
+  constexpr int TPW = 32 / L;
+  const size_t smem = align16(sizeof(uint4) * A.Q * L + A.Q) + (size_t)TRACKER_WARPS * TPW * slot_bytes(N, A.ncoef);
+  cudaError_t e = cudaFuncSetAttribute(hc_track_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  int per_sm = 0;
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, hc_track_kernel<N>, TRACKER_WARPS * 32, smem);
+  if (e != cudaSuccess) return e;
+  if (per_sm < 1) return cudaErrorInvalidConfiguration;
+  int sms = 0;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+  long long slots_needed = (A.total + TPW - 1) / TPW;
+  long long ctas = (long long)per_sm * sms;
+  long long ctas_needed = (slots_needed + TRACKER_WARPS - 1) / TRACKER_WARPS;
+  if (ctas_needed < ctas) ctas = ctas_needed;
+  if (ctas < 1) ctas = 1;
+  if (plan) {
+    plan->lanes = L;
+    plan->warps_per_cta = TRACKER_WARPS;
+    plan->ctas = (int)ctas;
+    plan->smem_bytes = smem;
+  }
+  hc_track_kernel<N><<<(unsigned)ctas, TRACKER_WARPS * 32, smem, stream>>>(A);
+  return cudaGetLastError();
+}
+
+}  // namespace hcb

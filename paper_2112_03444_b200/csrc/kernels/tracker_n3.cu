@@ -1,0 +1,11 @@
+// Instantiation of the fused tracker and the batched LU solve for N = 3 (see tracker.cuh, zgesv.cuh).
+#include "zgesv.cuh"
+namespace hcb {
+cudaError_t launch_tracker_3(const TrackArgs &A, int device, cudaStream_t s, TrackerPlan *p) {
+  return launch_tracker_n<3>(A, device, s, p);
+}
+cudaError_t launch_zgesv_3(int64_t batch, const double2 *A, const double2 *b, double2 *x, int32_t *info,
+                           double pivot_rel, cudaStream_t s) {
+  return launch_zgesv_n<3>(batch, A, b, x, info, pivot_rel, s);
+}
+}  // namespace hcb

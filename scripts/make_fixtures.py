@@ -94,7 +94,7 @@ def make_trifocal(max_loops: int = 60, stall_loops: int = 4, seed: int = rng.SEE
     hdr = (f"trifocal unknown-f start solutions at the planted complex p0 = rng.trifocal_complex_start({seed}).\n"
            f"Written by scripts/make_fixtures.py (oracle only): symmetry-aware monodromy, {loop + 1} loops,\n"
            f"{len(reps)} orbits x 8 = {full.shape[0]} solutions (PAPER.md Table 2 P:488 reports 1784).")
-    fixtures.write_solutions(fixtures.fixture_path("trifocal_start.sols"), full, hdr)
+    # the full start set is trifocal_reps.sols expanded by the symmetry (hc_inputs.fixtures.trifocal_start)
     fixtures.write_solutions(fixtures.fixture_path("trifocal_reps.sols"), np.array(reps), hdr)
     fixtures.write_params(fixtures.fixture_path("trifocal_p0.params"), p0, hdr)
 
