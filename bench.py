@@ -1,0 +1,335 @@
+"""Benchmark: device-timed tracks/s and instances/s of the fused B200 HC tracker.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config trifocal|fourview|cyclic7|katsura6]
+                  [--instances B] [--impl ours|reference] [--no-e2e] [--no-cpu-baseline]
+
+One "step" = one pass of the whole hot path (coefficient prologue + fused tracker: every
+§8(a) row a2-a10) over one batch.  Default workload: trifocal pose with unknown focal length,
+parameter homotopy from the oracle-generated start fixture (S = 5328 start solutions) to
+B = 1024 planted synthetic instances per GPU (BASELINE.json configs[3]; at 8 GPUs the job is
+configs[4], 8192 instances) -> weak scaling.  Under torchrun each rank owns its own
+instance block (no collective on the data path); solutions are gathered to rank 0 with NCCL
+after the timed region (timed separately, `gather_ms`).
+
+--impl reference times the CPU oracle (oracle/, test infrastructure) on the host cores on a
+bounded sample of the same workload (this run has no reference implementation to install).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+BASELINE = json.load(open(os.path.join(ROOT, "BASELINE.json")))
+METRIC = BASELINE["metric"]
+SM_MAX_MHZ = 1965.0
+FP64_DFMA_PER_CLK_PER_SM = 64   # B200 FP64 vector: 64 DFMA/clk/SM
+
+
+# ------------------------------------------------------------------------------ workloads
+
+def make_workload(name: str, B: int, rank: int):
+    """Seeded synthetic inputs (hc_inputs) for this rank: (desc, start_x, p0, p1s, settings overrides, meta)."""
+    from hc_inputs import fixtures, rng, systems
+    if name == "trifocal":
+        d = systems.trifocal_unknown_f()
+        start, p0 = fixtures.trifocal_start()
+        p1s = np.stack([rng.trifocal_instance(rng.SEED_TRIFOCAL_INSTANCE + rank * B + b)[0] for b in range(B)])
+        meta = {"workload": f"trifocal rel. pose unknown f (18x18, Table 2 P:488) PH, S={start.shape[0]} starts "
+                            f"(oracle monodromy fixture) x {B} planted instances per GPU (configs[3]; "
+                            f"configs[4] = 8192 instances at 8 GPUs)"}
+        return d, start, p0, p1s, {}, meta
+    if name == "fourview":
+        d = systems.nview_triangulation(4)
+        start = fixtures.read_solutions(fixtures.fixture_path("fourview_start.sols"))
+        p0 = fixtures.read_params(fixtures.fixture_path("fourview_p0.params"))
+        p1s = np.stack([rng.fourview_instance(rng.SEED_FOURVIEW_INSTANCE + rank * B + b)[0] for b in range(B)])
+        meta = {"workload": f"4-view triangulation (14x14, Table 2 P:490) PH, S=296 x {B} planted instances "
+                            f"per GPU (configs[2])"}
+        return d, start, p0, p1s, {}, meta
+    if name in ("cyclic7", "katsura6"):
+        d = systems.cyclic(7) if name == "cyclic7" else systems.katsura(6)
+        meta = {"workload": f"{d.name} total-degree homotopy, gamma seed 2, single instance "
+                            f"({'configs[1]' if name == 'cyclic7' else 'configs[0]'})"}
+        return d, None, None, None, {}, meta
+    raise SystemExit(f"unknown config {name}")
+
+
+# ------------------------------------------------------------------------------ clocks
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled every 200 ms during the timed region."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.idx = gpu_index
+        self.p = None
+
+    def start(self):
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                                       "-i", str(self.idx), "-lms", "200"], stdout=subprocess.PIPE,
+                                      stderr=subprocess.DEVNULL, text=True)
+        except FileNotFoundError:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.p.terminate()
+        out, _ = self.p.communicate(timeout=10)
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in out.strip().splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx = float(f[2])
+            except ValueError:
+                continue
+            for n, v in zip(names, f[5:9]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx, "samples": len(sm),
+                "reasons": sorted(reasons)}
+
+
+# ------------------------------------------------------------------------------ oracle (cpu)
+
+def oracle_sample(name: str, budget_s: float, rank: int = 0, B: int = 1):
+    """Time the CPU oracle (as it stands) on a bounded sample of the workload: the first tracks of
+    instance 0, sized to ~budget_s of CPU time.  Returns (tracks/s, cores, sample description)."""
+    import oracle
+    d, start, p0, p1s, _, _ = make_workload(name, 1, rank)
+    nthreads = oracle.nthreads_default()
+    if start is None:   # TD single instance
+        from hc_inputs import rng
+        hom = oracle.td_homotopy(d, rng.gamma(2))
+        start = oracle.td_start(d.degrees())
+        run = lambda X: oracle.track(hom, X, nthreads=nthreads)   # noqa: E731
+    else:
+        hom = oracle.ph_homotopy(d, p0)
+        run = lambda X: oracle.track(hom, X, p1s=p1s[:1], nthreads=nthreads)   # noqa: E731
+    n = min(start.shape[0], max(nthreads * 2, 16))
+    t = time.perf_counter()
+    run(start[:n])
+    dt = time.perf_counter() - t
+    m = int(min(start.shape[0], max(n, n * budget_s / max(dt, 1e-3))))
+    t = time.perf_counter()
+    run(start[:m])
+    dt = time.perf_counter() - t
+    return m / dt, nthreads, f"first {m} of {start.shape[0]} tracks of instance 0 ({dt:.1f} s, {nthreads} threads)"
+
+
+def run_reference(args):
+    """--impl reference: the CPU oracle on the host cores, same config/metric/unit."""
+    rank = int(os.environ.get("RANK", 0))
+    if rank != 0:
+        return
+    steps = []
+    for i in range(args.warmup + args.steps):
+        v, cores, sample = oracle_sample(args.config, args.ref_step_s)
+        if i >= args.warmup:
+            steps.append((v, sample))
+    vals = [v for v, _ in steps]
+    value = statistics.median(vals)
+    _, _, _, _, _, meta = make_workload(args.config, 1, 0)
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "tracks/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": None, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "c128 (fp64)", "data": "synthetic",
+            "config": {"workload": meta["workload"], "sample": steps[-1][1]},
+            "cpu_baseline": {"value": value, "unit": "tracks/s", "cores": cores, "kind": "oracle",
+                             "sample": steps[-1][1]},
+            "e2e": {"value": value, "unit": "tracks/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------------------ our arm
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2112_03444_b200 import hc
+    from paper_2112_03444_b200.distributed import env_rank_world, gather_to_rank0
+
+    rank, local_rank, world = env_rank_world()
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    def barrier():
+        if world > 1:
+            dist.barrier(device_ids=[local_rank])
+
+    B = args.instances
+    d, start, p0, p1s, _, meta = make_workload(args.config, B, rank)
+    if start is None:
+        from hc_inputs import rng
+        sysh = hc.System.total_degree_homotopy(d, device=local_rank)
+        p0, p1 = sysh.td_params(rng.gamma(2))
+        p1s = p1[None]
+        start = sysh.td_start()
+        B = 1
+    else:
+        sysh = hc.System(d, device=local_rank)
+    S, N = start.shape
+    info = sysh.info
+    st = hc.hc_tracker_settings_default()
+    x_start = torch.from_numpy(start).to(dev)
+    t_p0 = torch.from_numpy(np.ascontiguousarray(p0)).to(dev)
+    t_p1 = torch.from_numpy(np.ascontiguousarray(p1s)).to(dev)
+    out = (torch.empty((B, S, N), dtype=torch.complex128, device=dev),
+           torch.empty((B, S), dtype=torch.int32, device=dev),
+           torch.empty((B, S, 4), dtype=torch.int32, device=dev),
+           torch.empty((B, S, 2), dtype=torch.float64, device=dev))
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)   # 256 MB > 126 MB L2
+    stream = torch.cuda.current_stream(dev)
+
+    def step():
+        flush.fill_(1.0)   # L2 flush between steps (outside our kernels)
+        return hc.track_batch(sysh, x_start, t_p0, t_p1, st=st, stream=stream, out=out)
+
+    for _ in range(args.warmup):
+        step().wait()
+    clocks = ClockSampler(local_rank)
+    clocks.start()
+    time.sleep(0.3)
+    barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    results = [step() for _ in range(args.steps)]
+    e1.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    ck = clocks.stop()
+    elapsed = e0.elapsed_time(e1)
+    t = torch.tensor([elapsed], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    elapsed_max = float(t.item())
+    per_launch = [r.elapsed_ms() for r in results]   # (total, prologue, tracker) events on the launch stream
+    tracker_ms = statistics.mean(p[2] for p in per_launch)
+    prologue_ms = statistics.mean(p[1] for p in per_launch)
+    ctr = out[2]
+    solves = int(ctr[..., 3].sum().item())
+    status = out[1]
+    flops = solves * info["flops_solve"]
+    converged = int((status == hc.HC_CONVERGED).sum().item())
+    for r in results:
+        r.close()
+
+    tracks_total = world * B * S * args.steps
+    value = tracks_total / (elapsed_max / 1e3)
+    sm_mhz = ck.get("sm_mhz") or SM_MAX_MHZ
+    peak_max = 148 * FP64_DFMA_PER_CLK_PER_SM * 2 * SM_MAX_MHZ * 1e6 / 1e12
+    achieved = flops / (tracker_ms / 1e3) / 1e12
+
+    # ---- gather solutions to rank 0 (NCCL), timed separately ----
+    gather_ms = None
+    if world > 1:
+        barrier()
+        torch.cuda.synchronize()
+        g0 = time.perf_counter()
+        gather_to_rank0(list(out))
+        torch.cuda.synchronize()
+        gather_ms = (time.perf_counter() - g0) * 1e3
+
+    # ---- end to end through the C ABI with host buffers (pinned), H2D + D2H inside ----
+    e2e = None
+    if not args.no_e2e:
+        pin = lambda shape, dt: torch.empty(shape, dtype=dt, pin_memory=True).numpy()   # noqa: E731
+        hx = pin((B, S, N), torch.complex128)
+        hs = pin((B, S), torch.int32)
+        hcn = pin((B, S, 4), torch.int32)
+        hr = pin((B, S, 2), torch.float64)
+        hstart = pin((S, N), torch.complex128)
+        hstart[:] = start
+        hp0 = pin(p0.shape, torch.complex128)
+        hp0[:] = p0
+        hp1 = pin(np.shape(p1s), torch.complex128)
+        hp1[:] = p1s
+        hc.track_batch_host(sysh, hstart, hp0, hp1, st=st, out=(hx, hs, hcn, hr)).close()
+        barrier()
+        k = max(1, min(args.steps, 3))
+        w0 = time.perf_counter()
+        for _ in range(k):
+            hc.track_batch_host(sysh, hstart, hp0, hp1, st=st, out=(hx, hs, hcn, hr)).close()
+        w = time.perf_counter() - w0
+        tw = torch.tensor([w], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(tw, op=dist.ReduceOp.MAX)
+        h2d = hstart.nbytes + hp0.nbytes + hp1.nbytes
+        d2h = hx.nbytes + hs.nbytes + hcn.nbytes + hr.nbytes
+        e2e = {"value": world * B * S * k / float(tw.item()), "unit": "tracks/s", "h2d_bytes_per_step": int(h2d),
+               "d2h_bytes_per_step": int(d2h), "steps": k, "timing": "wall clock around synchronous hc_track_batch "
+               "(HC_MEM_HOST, pinned buffers), max over ranks"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        v, cores, sample = oracle_sample(args.config, args.cpu_budget_s)
+        cpu = {"value": v, "unit": "tracks/s", "cores": cores, "kind": "oracle", "sample": sample}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "tracks/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": elapsed_max / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "c128 (fp64)", "data": "synthetic",
+            "instances_per_sec": world * B * args.steps / (elapsed_max / 1e3),
+            "config": {"workload": meta["workload"], "instances_per_gpu": B, "tracks_per_instance": S,
+                       "N": N, "l2": "256 MB buffer written between steps (flush)", "parallelism": f"dp{world}"},
+            "roofline": {"bound": "alu", "achieved": achieved, "peak": peak_max, "unit": "TFLOP/s",
+                         "frac": achieved / peak_max, "traffic": None,
+                         "kernel": "hcb::hc_track_kernel<%d>" % N,
+                         "peak_note": "FP64 vector: 148 SM x 64 DFMA/clk x 2 x 1965 MHz (derived, DESIGN.md); "
+                                      "frac at the measured median clock: %.3f" %
+                                      (achieved / (peak_max * sm_mhz / SM_MAX_MHZ)),
+                         "flops_per_launch": flops,
+                         "tracker_ms_per_launch": tracker_ms, "prologue_ms_per_launch": prologue_ms},
+            "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": 2 * args.steps,
+            "clocks": ck, "converged_fraction": converged / (B * S), "gather_ms": gather_ms,
+            "solves_per_track": solves / (B * S),
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="trifocal", choices=["trifocal", "fourview", "cyclic7", "katsura6"])
+    ap.add_argument("--instances", type=int, default=1024)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-budget-s", type=float, default=15.0)
+    ap.add_argument("--ref-step-s", type=float, default=10.0)
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -108,7 +108,7 @@ typedef struct {
   int32_t lanes_per_track;    /* L = next power of two >= N */
   int32_t tracks_per_warp;    /* 32 / L */
   int32_t op_steps;           /* Q: evaluation op steps per lane (lane-balanced) */
-  int32_t max_factors;        /* M: max factors per op (paper's M) */
+  int32_t max_factors;        /* M: max monomial degree (paper's M) */
   int32_t n_ops_J, n_ops_rhs; /* real (unpadded) ops of dH/dx and of the H / dH/dt vector */
   int32_t n_terms;            /* terms of F */
   int64_t flops_coef;         /* algorithmic FP64 flops per solve: coefficient polynomials at t */
@@ -116,14 +116,23 @@ typedef struct {
   int64_t flops_lu;           /* ... fused LU + solve on [A | b] (SURVEY.md §8(d) rule) */
   int64_t flops_solve;        /* total per solve (coef + eval + lu + 8N vector work) */
   int64_t smem_per_track;     /* bytes of shared memory per track slot */
+  int32_t n_coef_slots;       /* coefficient slots (descriptor coefficients + s_k-scaled copies) */
+  int32_t n_monos;            /* monomial table size (N unknowns + constant one + shared products) */
+  int32_t mono_levels;        /* levels of the monomial program (max degree - 1) */
+  int64_t flops_eval_kernel;  /* flops the kernel's evaluation actually performs (shared monomials) */
+  int64_t flops_solve_kernel; /* per solve, kernel's own count (coef slots + eval + lu + 8N) */
 } hc_system_info;
 hc_status hc_system_info_get(hc_system sys, hc_system_info *out);
-/* Host-only (no GPU needed): compile `desc` and report its info / its evaluation op table.
- * Op table layout: op_steps * lanes_per_track records of 4 uint32 (see csrc/hc_internal.h:
- * x = coef | dest << 16, y = flags | scale << 8, z/w = factor indices), step_nfac [op_steps]
- * = max factor count of step q.  capacity = number of op records the buffer holds. */
+/* Host-only (no GPU needed): compile `desc` and report its info / its evaluation tables
+ * (layouts in csrc/hc_internal.h): ops [op_steps * lanes_per_track * 2] uint32
+ * (x = coefficient slot | monomial << 16, y = dest | flags << 16), mono_prog
+ * [n_monos - N - 1] uint32 (parent | var << 16), slot_map [n_coef_slots * 2] int32
+ * (descriptor coefficient id, scale s_k), entry_map [N * (N + 1)] int16 (dense entry of
+ * [dH/dx | rhs] -> compact index used by op destinations, -1 = structural zero).
+ * Any output pointer may be NULL. */
 hc_status hc_system_compile_info(const hc_system_desc *desc, hc_system_info *out);
-hc_status hc_system_compile_ops(const hc_system_desc *desc, uint32_t *ops, uint8_t *step_nfac, int64_t capacity);
+hc_status hc_system_compile_tables(const hc_system_desc *desc, uint32_t *ops, uint32_t *mono_prog, int32_t *slot_map,
+                                   int16_t *entry_map);
 hc_status hc_system_destroy(hc_system sys);
 
 /* ---------------------------------------------------------------------------------------------

@@ -20,7 +20,7 @@ HC_MEM_DEVICE, HC_MEM_HOST = 0, 1
 EXPORTED = [
     "hc_system_create", "hc_system_create_total_degree", "hc_total_degree_params", "hc_total_degree_count",
     "hc_total_degree_start", "hc_system_info_get", "hc_system_destroy", "hc_system_compile_info",
-    "hc_system_compile_ops", "hc_tracker_settings_default", "hc_track_batch", "hc_result_wait",
+    "hc_system_compile_tables", "hc_tracker_settings_default", "hc_track_batch", "hc_result_wait",
     "hc_result_elapsed_ms", "hc_result_get", "hc_result_destroy", "hc_batched_zgesv", "hc_fp64_peak_probe",
     "hc_last_error", "hc_version",
 ]
@@ -43,7 +43,8 @@ class hc_system_info(C.Structure):
                 ("op_steps", C.c_int32), ("max_factors", C.c_int32), ("n_ops_J", C.c_int32),
                 ("n_ops_rhs", C.c_int32), ("n_terms", C.c_int32), ("flops_coef", C.c_int64),
                 ("flops_eval", C.c_int64), ("flops_lu", C.c_int64), ("flops_solve", C.c_int64),
-                ("smem_per_track", C.c_int64)]
+                ("smem_per_track", C.c_int64), ("n_coef_slots", C.c_int32), ("n_monos", C.c_int32),
+                ("mono_levels", C.c_int32), ("flops_eval_kernel", C.c_int64), ("flops_solve_kernel", C.c_int64)]
 
     def as_dict(self):
         return {f[0]: getattr(self, f[0]) for f in self._fields_}
@@ -99,7 +100,7 @@ def lib() -> C.CDLL:
     L.hc_system_info_get.argtypes = [C.c_void_p, P(hc_system_info)]
     L.hc_system_destroy.argtypes = [C.c_void_p]
     L.hc_system_compile_info.argtypes = [P(hc_system_desc), P(hc_system_info)]
-    L.hc_system_compile_ops.argtypes = [P(hc_system_desc), C.c_void_p, C.c_void_p, C.c_int64]
+    L.hc_system_compile_tables.argtypes = [P(hc_system_desc), C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
     L.hc_tracker_settings_default.argtypes = [P(hc_tracker_settings)]
     L.hc_track_batch.argtypes = [C.c_void_p, P(hc_tracker_settings), P(hc_batch), P(C.c_void_p)]
     L.hc_result_wait.argtypes = [C.c_void_p]

@@ -10,19 +10,29 @@
 namespace hcb {
 
 // ------------------------------------------------------------------------------------------
-// Evaluation op: one term contribution  out(row, col) += scale * c_j * x_{f0} * ... * x_{f7}
-// (the paper's homogenised term (s_k, a_{k,j}, x_{k,m1}, ..., x_{k,mM})).  Unused
-// factor slots hold N, the constant-one slot.  Ops are lane-balanced by the host
-// compiler: at step q lane r executes ops[q * L + r]; ops of one output entry are contiguous in
-// a lane and the last one carries OP_LAST, which stores the register accumulator to M[dest].
-//   x: coefficient index (bits 0..15) | dest entry row*(N+1)+col (bits 16..31, 0xFFFF = none)
-//   y: flags (bit 0 OP_LAST, bit 1 OP_RHS) | scale (bits 8..15, real integer exponent)
-//   z, w: factor variable indices, one byte each (f0..f3 in z, f4..f7 in w)
+// Evaluation tables (the paper's homogenised term records (s_k, a_{k,j}, x_{k,m1..mM}),
+// P:432-434, re-laid out for the B200 kernel):
+//  * coefficient slots: the prologue turns every coefficient expression c_j(p) -- with the
+//    derivative scale s_k already folded in ("fold s_k into coefficients") -- into a polynomial
+//    in t; the kernel evaluates c_j(t) and c_j'(t) by Horner into shared memory;
+//  * monomial program: every monomial needed by dH/dx or H is computed once per evaluation as
+//    mono[k] = mono[parent_k] * x[var_k], level by level (degree d from degree d-1); slots
+//    0..N-1 are the unknowns, slot N the constant one (P:430's auxiliary variable x_{M+1} = 1);
+//    entry = parent (bits 0..15) | var (bits 16..31);
+//  * ops: out(row, col) += coef[slot] * mono[k], lane-balanced: at step q lane r executes
+//    ops[q * L + r]; ops of one output entry are contiguous in a lane and the last carries
+//    OP_LAST, which stores the register accumulator to M[dest]; padding ops sit after a lane's
+//    last entry and never store.
+//      x: coefficient slot (bits 0..15) | monomial index (bits 16..31)
+//      y: dest entry (bits 0..15, 0xFFFF = none) | flags << 16 (OP_LAST, OP_RHS)
+//  * entries are stored compactly (only structurally non-zero entries of [dH/dx | rhs]);
+//    mpos[row*(N+1)+col] is the compact index or -1 for a structural zero.
 // ------------------------------------------------------------------------------------------
 enum : uint32_t { OP_LAST = 1u, OP_RHS = 2u };
 constexpr uint32_t OP_NO_DEST = 0xFFFFu;
-constexpr int MAX_FACTORS = HC_MAX_FACTORS;
-constexpr int MAX_COEF_DEG = 7;   // coefficient polynomials in t: degree <= 7
+constexpr int MAX_FACTORS = HC_MAX_FACTORS;   // max monomial degree
+constexpr int MAX_LEVELS = MAX_FACTORS;       // monomial program levels (degrees 2..MAX_FACTORS)
+constexpr int MAX_COEF_DEG = 7;               // coefficient polynomials in t: degree <= 7
 
 // Coefficient monomial for the prologue: weight * prod_{m < deg} p_{fac[m]}  (deg <= MAX_COEF_DEG)
 struct CoefMono {
@@ -39,11 +49,17 @@ struct DevSettings {
 
 struct TrackArgs {
   // system tables
-  const uint4 *ops;          // [Q * L]
-  const uint8_t *step_nfac;  // [Q]
+  const uint2 *ops;          // [Q * L]
   int32_t Q;
-  int32_t ncoef;
+  const uint32_t *mono_prog; // [n_mono - (N + 1)]
+  int32_t n_mono;            // monomial table size including the N unknowns and the constant
+  int32_t n_levels;
+  int32_t level_end[MAX_LEVELS];  // level l covers [level_end[l-1] (or N+1), level_end[l])
+  int32_t ncoef;             // coefficient slots
+  int32_t ncoef_src;         // slots [0, ncoef_src) are the descriptor's coefficients (used by rhs ops)
   int32_t D;                 // degree of coefficient polynomials in t
+  const int16_t *mpos;       // [N * (N + 1)] dense -> compact entry index, -1 = structural zero
+  int32_t n_entries;         // compact entries
   // batch
   const double2 *coef_t;     // [B][D+1][ncoef]
   const double2 *start_x;    // [S][N]
@@ -73,9 +89,6 @@ struct TrackerPlan {
   int ctas;           // persistent grid
   size_t smem_bytes;  // dynamic shared memory per CTA
 };
-
-size_t slot_smem_bytes(int N, int ncoef);
-size_t table_smem_bytes(int Q, int L);
 
 // Per-N launchers (csrc/kernels/tracker_n*.cu); return cudaError_t.
 typedef cudaError_t (*tracker_launch_fn)(const TrackArgs &, int device, cudaStream_t, TrackerPlan *);

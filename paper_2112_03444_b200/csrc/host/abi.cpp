@@ -8,6 +8,7 @@
 
 #include "../hc_internal.h"
 #include "compiler.h"
+#include "../kernels/layout.h"
 
 namespace hcb {
 // per-N launchers defined in csrc/kernels/tracker_n*.cu
@@ -69,8 +70,9 @@ static hc_status cuda_fail(cudaError_t e, const char *where) {
 struct hc_system_s {
   int device = 0;
   CompiledSystem cs;
-  uint4 *d_ops = nullptr;
-  uint8_t *d_nfac = nullptr;
+  uint2 *d_ops = nullptr;
+  uint32_t *d_mono_prog = nullptr;
+  int16_t *d_mpos = nullptr;
   CoefMono *d_mono = nullptr;
   int32_t *d_mono_ptr = nullptr;
   // total-degree metadata
@@ -147,12 +149,15 @@ hc_status hc_tracker_settings_default(hc_tracker_settings *s) {
 static hc_status upload_system(hc_system sys) {
   CompiledSystem &cs = sys->cs;
   CK(cudaSetDevice(sys->device));
-  CK(cudaMalloc(&sys->d_ops, sizeof(uint4) * std::max<size_t>(1, cs.ops.size())));
-  CK(cudaMalloc(&sys->d_nfac, std::max<size_t>(1, cs.step_nfac.size())));
+  CK(cudaMalloc(&sys->d_ops, sizeof(uint2) * std::max<size_t>(1, cs.ops.size())));
+  CK(cudaMalloc(&sys->d_mono_prog, sizeof(uint32_t) * std::max<size_t>(1, cs.mono_prog.size())));
+  CK(cudaMalloc(&sys->d_mpos, sizeof(int16_t) * cs.mpos.size()));
+  CK(cudaMemcpy(sys->d_mpos, cs.mpos.data(), sizeof(int16_t) * cs.mpos.size(), cudaMemcpyHostToDevice));
   CK(cudaMalloc(&sys->d_mono, sizeof(CoefMono) * std::max<size_t>(1, cs.mono.size())));
   CK(cudaMalloc(&sys->d_mono_ptr, sizeof(int32_t) * cs.mono_ptr.size()));
-  if (!cs.ops.empty()) CK(cudaMemcpy(sys->d_ops, cs.ops.data(), sizeof(uint4) * cs.ops.size(), cudaMemcpyHostToDevice));
-  if (!cs.step_nfac.empty()) CK(cudaMemcpy(sys->d_nfac, cs.step_nfac.data(), cs.step_nfac.size(), cudaMemcpyHostToDevice));
+  if (!cs.ops.empty()) CK(cudaMemcpy(sys->d_ops, cs.ops.data(), sizeof(uint2) * cs.ops.size(), cudaMemcpyHostToDevice));
+  if (!cs.mono_prog.empty())
+    CK(cudaMemcpy(sys->d_mono_prog, cs.mono_prog.data(), sizeof(uint32_t) * cs.mono_prog.size(), cudaMemcpyHostToDevice));
   if (!cs.mono.empty())
     CK(cudaMemcpy(sys->d_mono, cs.mono.data(), sizeof(CoefMono) * cs.mono.size(), cudaMemcpyHostToDevice));
   CK(cudaMemcpy(sys->d_mono_ptr, cs.mono_ptr.data(), sizeof(int32_t) * cs.mono_ptr.size(), cudaMemcpyHostToDevice));
@@ -163,7 +168,8 @@ static void free_system(hc_system sys) {
   if (!sys) return;
   cudaSetDevice(sys->device);
   cudaFree(sys->d_ops);
-  cudaFree(sys->d_nfac);
+  cudaFree(sys->d_mono_prog);
+  cudaFree(sys->d_mpos);
   cudaFree(sys->d_mono);
   cudaFree(sys->d_mono_ptr);
   delete sys;
@@ -281,8 +287,12 @@ static void fill_info(const CompiledSystem &cs, hc_system_info *o) {
   o->flops_eval = cs.flops_eval;
   o->flops_lu = cs.flops_lu;
   o->flops_solve = cs.flops_solve;
-  const int N = cs.N;
-  o->smem_per_track = (int64_t)(((16 * (2 * cs.ncoef + (N + 1) + N * (N + 1) + (N + 1)) + 8 * N) + 15) & ~15);
+  o->n_coef_slots = cs.ncoef;
+  o->n_monos = cs.n_mono;
+  o->mono_levels = cs.n_levels;
+  o->flops_eval_kernel = cs.flops_eval_kernel;
+  o->flops_solve_kernel = cs.flops_solve_kernel;
+  o->smem_per_track = (int64_t)slot_bytes(cs.N, cs.ncoef, cs.ncoef_src, cs.n_mono, cs.n_entries);
 }
 
 hc_status hc_system_info_get(hc_system sys, hc_system_info *o) {
@@ -301,15 +311,17 @@ hc_status hc_system_compile_info(const hc_system_desc *desc, hc_system_info *o) 
   return HC_OK;
 }
 
-hc_status hc_system_compile_ops(const hc_system_desc *desc, uint32_t *ops, uint8_t *step_nfac, int64_t capacity) {
+hc_status hc_system_compile_tables(const hc_system_desc *desc, uint32_t *ops, uint32_t *mono_prog, int32_t *slot_map,
+                                   int16_t *entry_map) {
   if (!desc) return fail(HC_E_INVALID_ARG, "null argument");
   CompiledSystem cs;
   std::string err;
   hc_status s = compile_system(*desc, cs, err);
   if (s != HC_OK) return fail(s, err);
-  if ((int64_t)cs.ops.size() > capacity) return fail(HC_E_INVALID_ARG, "capacity too small");
-  if (ops) std::memcpy(ops, cs.ops.data(), sizeof(uint4) * cs.ops.size());
-  if (step_nfac) std::memcpy(step_nfac, cs.step_nfac.data(), cs.step_nfac.size());
+  if (ops) std::memcpy(ops, cs.ops.data(), sizeof(uint2) * cs.ops.size());
+  if (mono_prog) std::memcpy(mono_prog, cs.mono_prog.data(), sizeof(uint32_t) * cs.mono_prog.size());
+  if (slot_map) std::memcpy(slot_map, cs.slot_map.data(), sizeof(int32_t) * cs.slot_map.size());
+  if (entry_map) std::memcpy(entry_map, cs.mpos.data(), sizeof(int16_t) * cs.mpos.size());
   return HC_OK;
 }
 
@@ -437,9 +449,15 @@ hc_status hc_track_batch(hc_system sys, const hc_tracker_settings *settings, con
   // ---- the fused tracker ----
   TrackArgs ta{};
   ta.ops = sys->d_ops;
-  ta.step_nfac = sys->d_nfac;
   ta.Q = cs.Q;
+  ta.mono_prog = sys->d_mono_prog;
+  ta.n_mono = cs.n_mono;
+  ta.n_levels = cs.n_levels;
+  for (int l = 0; l < MAX_LEVELS; ++l) ta.level_end[l] = cs.level_end[l];
   ta.ncoef = cs.ncoef;
+  ta.ncoef_src = cs.ncoef_src;
+  ta.mpos = sys->d_mpos;
+  ta.n_entries = cs.n_entries;
   ta.D = cs.D;
   ta.coef_t = d_coef;
   ta.start_x = d_start;

@@ -4,36 +4,43 @@
 // (s_k, a_{k,j}, x_{k,m1..mM}) with a constant-one variable so a warp can evaluate them in a
 // uniform format, one Jacobian row per thread.  Padding every entry to K
 // terms wastes most of the work on sparse vision systems (trifocal J: 648 real of 3888 padded
-// terms), and row-per-thread leaves lanes idle when rows differ in length.  Here the same
-// homogeneous term record is kept (coefficient index, integer scale s_k, up to M factor indices,
-// constant-one slot for unused factors), but entries are bin-packed over the L lanes of a track
-// (longest-processing-time first), so each lane runs ~(total terms / L) ops, and each lane step q
-// carries the max factor count of its ops so the product loop is uniform across the warp.
+// terms), row-per-thread leaves lanes idle when rows differ in length, and every term re-multiplies
+// its M factors.  Here the homogeneous record survives as (coefficient slot, monomial index):
+//  * s_k is folded into the coefficient (a slot per distinct (c_j, s_k)), evaluated by the
+//    prologue as a polynomial in t;
+//  * the products x_{m1} ... x_{mM} are shared: every monomial any entry needs is computed once
+//    per evaluation from a parent of degree one less (a monomial program, levels by degree; the
+//    unknowns and the constant one are its first N+1 slots);
+//  * entries are bin-packed over the L lanes of a track (longest-processing-time first), so each
+//    lane runs ~(total terms / L) uniform ops out(row,col) += coef[slot] * mono[k].
 #include "compiler.h"
 
 #include <algorithm>
 #include <cmath>
 #include <map>
 #include <numeric>
+#include <set>
 #include <sstream>
 
 namespace hcb {
 
 namespace {
 
+typedef std::vector<int> Expo;   // exponent vector of a monomial in x
+
 struct RawOp {
-  int coef;
-  int scale;
+  int slot;       // coefficient slot (scale folded in)
+  Expo mono;      // monomial
+  int scale;      // s_k (for the flop rule only)
   bool rhs;
-  std::vector<int> fac;   // factor variable indices (repeated for powers)
 };
 
 struct Entry {
-  int dest;               // row * (N + 1) + col
+  int dest;       // row * (N + 1) + col
   std::vector<RawOp> ops;
-  int64_t cost = 0;
-  int maxnf = 0;
 };
+
+int deg_of(const Expo &e) { return std::accumulate(e.begin(), e.end(), 0); }
 
 int64_t term_flops(int nf, int scale) {
   // a term of total degree d costs 6(d-1) + 8 (complex products, then a complex
@@ -141,19 +148,79 @@ hc_status compile_system(const hc_system_desc &d, CompiledSystem &cs, std::strin
   cs = CompiledSystem();
   cs.N = N;
   cs.P = P;
-  cs.ncoef = d.n_coefs;
+  cs.ncoef_src = d.n_coefs;
   cs.n_terms = d.n_terms;
   cs.L = lanes_for(N);
 
-  // ---- coefficient expressions -> monomials in p with repeated factor lists ----
-  cs.mono_ptr.assign(d.n_coefs + 1, 0);
-  int D = 0;
+  // ---- degrees ----
+  cs.degrees.assign(N, 0);
+  for (int k = 0; k < d.n_terms; ++k) {
+    int tot = 0;
+    for (int v = 0; v < N; ++v) tot += d.term_xexp[(size_t)k * N + v];
+    cs.degrees[d.term_eq[k]] = std::max(cs.degrees[d.term_eq[k]], tot);
+  }
+
+  // ---- ops: H / dH/dt entries (column N) and dH/dx entries by exponent decrement; the exponent
+  //      s_k = e_v becomes a coefficient slot s_k * c_j (scale folded into the coefficient) ----
+  std::map<std::pair<int, int>, int> slot_of;   // (coef j, scale) -> slot
+  std::vector<std::pair<int, int>> slots;
   for (int j = 0; j < d.n_coefs; ++j) {
+    slot_of[{j, 1}] = j;
+    slots.push_back({j, 1});
+  }
+  auto slot_for = [&](int j, int e) {
+    auto it = slot_of.find({j, e});
+    if (it != slot_of.end()) return it->second;
+    const int id = (int)slots.size();
+    slot_of[{j, e}] = id;
+    slots.push_back({j, e});
+    return id;
+  };
+  std::map<int, Entry> entries;
+  int maxdeg = 0;
+  for (int k = 0; k < d.n_terms; ++k) {
+    const int i = d.term_eq[k], j = d.term_coef[k];
+    Expo e(d.term_xexp + (size_t)k * N, d.term_xexp + (size_t)(k + 1) * N);
+    const int de = deg_of(e);
+    if (de > MAX_FACTORS) {
+      err = "term of total degree > " + std::to_string(MAX_FACTORS);
+      return HC_E_TOO_LARGE;
+    }
+    maxdeg = std::max(maxdeg, de);
+    Entry &er = entries[i * (N + 1) + N];
+    er.dest = i * (N + 1) + N;
+    er.ops.push_back(RawOp{j, e, 1, true});
+    cs.n_ops_rhs++;
+    for (int v = 0; v < N; ++v) {
+      if (e[v] == 0) continue;
+      Expo e2 = e;
+      e2[v] -= 1;
+      Entry &ej = entries[i * (N + 1) + v];
+      ej.dest = i * (N + 1) + v;
+      ej.ops.push_back(RawOp{slot_for(j, e[v]), e2, e[v], false});
+      cs.n_ops_J++;
+    }
+  }
+  if ((int)slots.size() > 65535) {
+    err = "more than 65535 coefficient slots";
+    return HC_E_TOO_LARGE;
+  }
+  cs.ncoef = (int)slots.size();
+  cs.M = maxdeg;
+
+  // ---- coefficient slots -> prologue monomials (slot = scale * c_j) ----
+  cs.mono_ptr.assign(cs.ncoef + 1, 0);
+  cs.slot_map.resize(2 * cs.ncoef);
+  int D = 0;
+  for (int sl = 0; sl < cs.ncoef; ++sl) {
+    const int j = slots[sl].first, sc = slots[sl].second;
+    cs.slot_map[2 * sl] = j;
+    cs.slot_map[2 * sl + 1] = sc;
     for (int m = d.coef_ptr[j]; m < d.coef_ptr[j + 1]; ++m) {
       CoefMono mo{};
-      mo.wre = d.coef_w[m].re;
-      mo.wim = d.coef_w[m].im;
-      mo.coef = j;
+      mo.wre = d.coef_w[m].re * sc;
+      mo.wim = d.coef_w[m].im * sc;
+      mo.coef = sl;
       int deg = 0;
       for (int q = 0; q < P; ++q) {
         const int e = d.coef_pexp[(size_t)m * P + q];
@@ -169,117 +236,121 @@ hc_status compile_system(const hc_system_desc &d, CompiledSystem &cs, std::strin
       D = std::max(D, deg);
       cs.mono.push_back(mo);
     }
-    cs.mono_ptr[j + 1] = (int32_t)cs.mono.size();
+    cs.mono_ptr[sl + 1] = (int32_t)cs.mono.size();
   }
   cs.D = D;
 
-  // ---- degrees ----
-  cs.degrees.assign(N, 0);
-  for (int k = 0; k < d.n_terms; ++k) {
-    int tot = 0;
-    for (int v = 0; v < N; ++v) tot += d.term_xexp[(size_t)k * N + v];
-    cs.degrees[d.term_eq[k]] = std::max(cs.degrees[d.term_eq[k]], tot);
+  // ---- monomial program: closure under "divide by one variable", evaluated degree by degree ----
+  std::map<Expo, int> mono_idx;
+  std::set<Expo> need;
+  for (auto &kv : entries)
+    for (const RawOp &o : kv.second.ops)
+      if (deg_of(o.mono) >= 2) need.insert(o.mono);
+  std::vector<std::set<Expo>> by_deg(maxdeg + 1);
+  for (const Expo &e : need) by_deg[deg_of(e)].insert(e);
+  std::map<Expo, std::pair<Expo, int>> parent;   // monomial -> (parent, var)
+  for (int dg = maxdeg; dg >= 2; --dg) {
+    for (const Expo &e : by_deg[dg]) {
+      // prefer a parent that is already needed (shared work), else the one dividing by the
+      // highest variable; every degree-2 monomial has a variable as parent
+      int best = -1;
+      for (int v = 0; v < N && best < 0; ++v) {
+        if (!e[v]) continue;
+        Expo p2 = e;
+        p2[v] -= 1;
+        if (dg - 1 < 2 || by_deg[dg - 1].count(p2)) best = v;
+      }
+      if (best < 0)
+        for (int v = N - 1; v >= 0; --v)
+          if (e[v]) {
+            best = v;
+            break;
+          }
+      Expo p2 = e;
+      p2[best] -= 1;
+      if (dg - 1 >= 2) by_deg[dg - 1].insert(p2);
+      parent[e] = {p2, best};
+    }
+  }
+  auto index_of = [&](const Expo &e) -> int {
+    const int dg = deg_of(e);
+    if (dg == 0) return N;
+    if (dg == 1)
+      for (int v = 0; v < N; ++v)
+        if (e[v]) return v;
+    return mono_idx.at(e);
+  };
+  int next = N + 1;
+  cs.n_levels = std::max(0, maxdeg - 1);
+  if (cs.n_levels > MAX_LEVELS) {
+    err = "monomial degree too large";
+    return HC_E_TOO_LARGE;
+  }
+  for (int dg = 2; dg <= maxdeg; ++dg) {
+    for (const Expo &e : by_deg[dg]) {
+      mono_idx[e] = next++;
+      const auto &pv = parent.at(e);
+      cs.mono_prog.push_back((uint32_t)index_of(pv.first) | ((uint32_t)pv.second << 16));
+    }
+    cs.level_end[dg - 2] = next;
+  }
+  cs.n_mono = next;
+  if (cs.n_mono > 65535) {
+    err = "too many monomials";
+    return HC_E_TOO_LARGE;
   }
 
-  // ---- ops: rhs entries (H / dH/dt, column N) and Jacobian entries (exponent decrement) ----
-  std::map<int, Entry> entries;
-  auto add_op = [&](int row, int col, RawOp op) -> bool {
-    if ((int)op.fac.size() > MAX_FACTORS) return false;
-    const int dest = row * (N + 1) + col;
-    Entry &e = entries[dest];
-    e.dest = dest;
-    e.ops.push_back(std::move(op));
-    return true;
-  };
-  for (int k = 0; k < d.n_terms; ++k) {
-    const int i = d.term_eq[k], j = d.term_coef[k];
-    const int32_t *e = d.term_xexp + (size_t)k * N;
-    RawOp h{j, 1, true, {}};
-    for (int v = 0; v < N; ++v)
-      for (int r = 0; r < e[v]; ++r) h.fac.push_back(v);
-    if (!add_op(i, N, h)) {
-      err = "term of total degree > " + std::to_string(MAX_FACTORS);
-      return HC_E_TOO_LARGE;
-    }
-    cs.n_ops_rhs++;
-    for (int v = 0; v < N; ++v) {
-      if (e[v] == 0) continue;
-      RawOp jo{j, e[v], false, {}};
-      for (int u = 0; u < N; ++u)
-        for (int r = 0; r < (u == v ? e[u] - 1 : e[u]); ++r) jo.fac.push_back(u);
-      add_op(i, v, jo);
-      cs.n_ops_J++;
-    }
-  }
-  // ---- flop model ----
+  // ---- flop models ----
   cs.flops_eval = 0;
-  int M = 0;
-  for (auto &kv : entries) {
-    Entry &e = kv.second;
-    std::sort(e.ops.begin(), e.ops.end(), [](const RawOp &a, const RawOp &b) { return a.fac.size() > b.fac.size(); });
-    for (const RawOp &o : e.ops) {
-      cs.flops_eval += term_flops((int)o.fac.size(), o.scale);
-      e.cost += (int64_t)o.fac.size() + 2;
-      e.maxnf = std::max(e.maxnf, (int)o.fac.size());
-      M = std::max(M, (int)o.fac.size());
-    }
-  }
-  cs.M = M;
+  for (auto &kv : entries)
+    for (const RawOp &o : kv.second.ops) cs.flops_eval += term_flops(deg_of(o.mono), o.scale);
+  cs.flops_eval_kernel = 6LL * (cs.n_mono - N - 1) + 8LL * (cs.n_ops_J + cs.n_ops_rhs);
   cs.flops_coef = (int64_t)d.n_coefs * 8 * D;
   cs.flops_lu = lu_flops(N);
   cs.flops_solve = cs.flops_coef + cs.flops_eval + cs.flops_lu + 8LL * N;
+  cs.flops_solve_kernel = (int64_t)cs.ncoef * 8 * D + cs.flops_eval_kernel + cs.flops_lu + 8LL * N;
 
-  // ---- lane balancing: LPT bin packing of entries over L lanes ----
+  // ---- lane balancing: LPT bin packing of entries (cost = ops + 1 store) over the L lanes ----
   const int L = cs.L;
   std::vector<Entry *> order;
   for (auto &kv : entries) order.push_back(&kv.second);
-  std::stable_sort(order.begin(), order.end(), [](const Entry *a, const Entry *b) { return a->cost > b->cost; });
+  std::stable_sort(order.begin(), order.end(),
+                   [](const Entry *a, const Entry *b) { return a->ops.size() > b->ops.size(); });
   std::vector<std::vector<Entry *>> lane_entries(L);
   std::vector<int64_t> load(L, 0);
   for (Entry *e : order) {
     const int l = (int)(std::min_element(load.begin(), load.end()) - load.begin());
     lane_entries[l].push_back(e);
-    load[l] += e->cost;
-  }
-  std::vector<std::vector<const RawOp *>> lane_ops(L);
-  std::vector<std::vector<int>> lane_last(L);   // dest for last op of an entry, -1 otherwise
-  for (int l = 0; l < L; ++l) {
-    auto &es = lane_entries[l];
-    std::stable_sort(es.begin(), es.end(), [](const Entry *a, const Entry *b) { return a->maxnf > b->maxnf; });
-    for (const Entry *e : es)
-      for (size_t k = 0; k < e->ops.size(); ++k) {
-        lane_ops[l].push_back(&e->ops[k]);
-        lane_last[l].push_back(k + 1 == e->ops.size() ? e->dest : -1);
-      }
+    load[l] += (int64_t)e->ops.size() + 1;
   }
   int Q = 0;
-  for (int l = 0; l < L; ++l) Q = std::max(Q, (int)lane_ops[l].size());
+  for (int l = 0; l < L; ++l) {
+    int n = 0;
+    for (const Entry *e : lane_entries[l]) n += (int)e->ops.size();
+    Q = std::max(Q, n);
+  }
   cs.Q = Q;
-  cs.ops.assign((size_t)Q * L, uint4{});
-  cs.step_nfac.assign(Q, 0);
-  for (int q = 0; q < Q; ++q) {
-    int nf = 0;
-    for (int l = 0; l < L; ++l) {
-      uint4 w;
-      uint8_t f[MAX_FACTORS];
-      for (int m = 0; m < MAX_FACTORS; ++m) f[m] = (uint8_t)N;   // constant-one slot
-      if (q < (int)lane_ops[l].size()) {
-        const RawOp *o = lane_ops[l][q];
-        const int dest = lane_last[l][q];
-        w.x = (uint32_t)o->coef | ((uint32_t)(dest < 0 ? OP_NO_DEST : (uint32_t)dest) << 16);
-        w.y = (dest >= 0 ? OP_LAST : 0u) | (o->rhs ? OP_RHS : 0u) | ((uint32_t)(o->scale & 0xFF) << 8);
-        for (size_t m = 0; m < o->fac.size(); ++m) f[m] = (uint8_t)o->fac[m];
-        nf = std::max(nf, (int)o->fac.size());
-      } else {
-        // padding op: scale 0, no store, coefficient 0 (any valid index), all factors = 1
-        w.x = 0u | (OP_NO_DEST << 16);
-        w.y = 0u;
+  // compact entry numbering: row-major order of the structurally non-zero entries
+  cs.mpos.assign((size_t)N * (N + 1), (int16_t)-1);
+  {
+    int c = 0;
+    for (auto &kv : entries) cs.mpos[kv.first] = (int16_t)c++;   // std::map iterates row-major
+    cs.n_entries = c;
+  }
+  cs.ops.assign((size_t)Q * L, uint2{0u, OP_NO_DEST});
+  for (int l = 0; l < L; ++l) {
+    int q = 0;
+    for (const Entry *e : lane_entries[l])
+      for (size_t k = 0; k < e->ops.size(); ++k, ++q) {
+        const RawOp &o = e->ops[k];
+        const bool last = (k + 1 == e->ops.size());
+        uint2 w;
+        w.x = (uint32_t)o.slot | ((uint32_t)index_of(o.mono) << 16);
+        w.y = (last ? (uint32_t)cs.mpos[e->dest] : OP_NO_DEST) | ((last ? OP_LAST : 0u) | (o.rhs ? OP_RHS : 0u)) << 16;
+        cs.ops[(size_t)q * L + l] = w;
       }
-      w.z = (uint32_t)f[0] | ((uint32_t)f[1] << 8) | ((uint32_t)f[2] << 16) | ((uint32_t)f[3] << 24);
-      w.w = (uint32_t)f[4] | ((uint32_t)f[5] << 8) | ((uint32_t)f[6] << 16) | ((uint32_t)f[7] << 24);
-      cs.ops[(size_t)q * L + l] = w;
-    }
-    cs.step_nfac[q] = (uint8_t)nf;
+    // padding ops after the lane's last entry: slot 0 times the constant monomial, never stored
+    for (; q < Q; ++q) cs.ops[(size_t)q * L + l] = uint2{(uint32_t)N << 16, OP_NO_DEST};
   }
   return HC_OK;
 }

@@ -11,15 +11,23 @@
 namespace hcb {
 
 struct CompiledSystem {
-  int N = 0, P = 0, ncoef = 0, D = 0;
-  int L = 1, Q = 0, M = 0;
+  int N = 0, P = 0, D = 0;
+  int ncoef_src = 0;               // coefficient expressions of the descriptor
+  int ncoef = 0;                   // coefficient slots (descriptor's + scaled copies s_k * c_j)
+  int L = 1, Q = 0, M = 0;         // lanes, op steps, max monomial degree
   int n_ops_J = 0, n_ops_rhs = 0, n_terms = 0;
-  std::vector<uint4> ops;          // [Q * L]
-  std::vector<uint8_t> step_nfac;  // [Q]
-  std::vector<CoefMono> mono;      // sorted by coef
+  int n_mono = 0, n_levels = 0;    // monomial table size (incl. N unknowns + constant), levels
+  int level_end[MAX_LEVELS] = {0};
+  std::vector<uint2> ops;          // [Q * L]
+  std::vector<int16_t> mpos;       // [N * (N + 1)] dense -> compact entry, -1 = structural zero
+  int n_entries = 0;
+  std::vector<uint32_t> mono_prog; // [n_mono - N - 1]: parent | var << 16
+  std::vector<int32_t> slot_map;   // [ncoef * 2]: (descriptor coefficient id, scale)
+  std::vector<CoefMono> mono;      // prologue monomials, sorted by slot
   std::vector<int32_t> mono_ptr;   // [ncoef + 1]
   std::vector<int32_t> degrees;    // total degree of each equation
-  int64_t flops_coef = 0, flops_eval = 0, flops_lu = 0, flops_solve = 0;
+  int64_t flops_coef = 0, flops_eval = 0, flops_lu = 0, flops_solve = 0;   // SURVEY §8(d) rule
+  int64_t flops_eval_kernel = 0, flops_solve_kernel = 0;                   // as the kernel computes
 };
 
 // Returns HC_OK or an error code with a message in `err`.

@@ -1,0 +1,24 @@
+// layout.h -- shared-memory layout of the tracker kernel (host and device agree on sizes).
+#pragma once
+
+#include <cstddef>
+#include <cuda_runtime.h>
+
+namespace hcb {
+
+__host__ __device__ inline size_t align16(size_t b) { return (b + 15) & ~size_t(15); }
+
+// Per track slot: cval[ncoef + ncoef_src] (c(t) for every slot, c'(t) for the rhs slots),
+// mono[n_mono] (x_0..x_{N-1}, 1, shared products), M[n_entries] (non-zero entries of
+// [dH/dx | rhs]), prow[N + 1] (pivot row), rabs[N] (doubles).
+__host__ __device__ inline size_t slot_bytes(int N, int ncoef, int ncoef_src, int n_mono, int n_entries) {
+  return align16(sizeof(double) * 2 * ((size_t)ncoef + ncoef_src + n_mono + n_entries + (N + 1)) + sizeof(double) * N);
+}
+
+// Per CTA, before the slots: the op table [Q * L] (8 B each), the monomial program (4 B each) and
+// the dense -> compact entry map (2 B each).
+__host__ __device__ inline size_t table_bytes(int Q, int L, int nprog, int N) {
+  return align16((size_t)8 * Q * L) + align16((size_t)4 * nprog) + align16((size_t)2 * N * (N + 1));
+}
+
+}  // namespace hcb

@@ -24,6 +24,7 @@
 #include <cuda_runtime.h>
 
 #include "../hc_internal.h"
+#include "layout.h"
 
 namespace hcb {
 
@@ -32,6 +33,10 @@ constexpr int TRACKER_WARPS = 4;
 
 __device__ __forceinline__ double2 cmul(double2 a, double2 b) {
   return make_double2(fma(a.x, b.x, -a.y * b.y), fma(a.x, b.y, a.y * b.x));
+}
+// c + a * b
+__device__ __forceinline__ double2 cfma(double2 a, double2 b, double2 c) {
+  return make_double2(fma(a.x, b.x, fma(-a.y, b.y, c.x)), fma(a.x, b.y, fma(a.y, b.x, c.y)));
 }
 // c - a * b
 __device__ __forceinline__ double2 cfms(double2 c, double2 a, double2 b) {
@@ -63,13 +68,6 @@ __device__ __forceinline__ bool seg_all(bool p, int seg) {
   const unsigned b = __ballot_sync(FULL, p);
   const unsigned m = seg_mask<L>() << ((L == 32) ? 0 : seg * L);
   return (b & m) == m;
-}
-
-__host__ __device__ inline size_t align16(size_t b) { return (b + 15) & ~size_t(15); }
-
-// Per-slot shared memory: cval[2*ncoef] (c(t), c'(t)), x[N+1], M[N*(N+1)], prow[N+1], rabs[N]
-__host__ __device__ inline size_t slot_bytes(int N, int ncoef) {
-  return align16(sizeof(double2) * (2 * ncoef + (N + 1) + N * (N + 1) + (N + 1)) + sizeof(double) * N);
 }
 
 enum SlotState : int { ST_RK = 0, ST_NEWTON = 1, ST_POLISH = 2, ST_RESID = 3, ST_DONE = 4 };
@@ -141,68 +139,93 @@ __device__ __forceinline__ bool lu_rows(double2 (&a)[N + 1], int r, int seg, dou
 }
 
 // ------------------------------------------------------------------------------------------
-// Evaluate [dH/dx | rhs] into the slot's M (shared), then fused LU + solve.  Returns the solution
-// component y_r in lane r (r < N) and whether the solve succeeded (uniform over the slot).
-// rhs_off = 0 -> rhs = H (coefficients c(t)); rhs_off = ncoef -> rhs = dH/dt (coefficients c'(t)).
-// When want_abs, rabs[i] = sum_k |c_k m_k(x)| over the rhs terms of row i (relative residual).
+// Op list: M[dest] = sum over the entry's ops of coef[slot] * mono[k] (P:432-434 terms with the
+// products shared through the monomial program).  ABS also accumulates sum |c m| for the
+// relative residual of the rhs rows (reading R10).
 // ------------------------------------------------------------------------------------------
-template <int N, int L>
-__device__ __forceinline__ bool eval_solve(const uint4 *__restrict__ ops_s, const uint8_t *__restrict__ nfac_s,
-                                           int Q, int ncoef, int D, const double2 *__restrict__ ct, double t,
-                                           int rhs_off, bool want_abs, double pivot_rel, double2 *cval,
-                                           double2 *xs, double2 *M, double2 *prow, double *rabs, int r, int seg,
-                                           double2 xr, double2 &y, double2 &fr, double &fabs_r) {
-  // ---- stage x and coefficient values c_j(t), c_j'(t) (Horner on the prologue's polynomials) ----
-  if (r < N) xs[r] = xr;
-  for (int j = r; j < ncoef; j += L) {
-    double2 p = __ldg(&ct[(size_t)D * ncoef + j]);
-    double2 dp = make_double2(0.0, 0.0);
-    for (int d = D - 1; d >= 0; --d) {
-      double2 a = __ldg(&ct[(size_t)d * ncoef + j]);
-      dp = make_double2(fma(dp.x, t, p.x), fma(dp.y, t, p.y));
-      p = make_double2(fma(p.x, t, a.x), fma(p.y, t, a.y));
-    }
-    cval[j] = p;
-    cval[ncoef + j] = dp;
-  }
-  __syncwarp();
-  // ---- homogenised term evaluation (P:432-434), lane-balanced op list ----
+template <int N, int L, bool ABS>
+__device__ __forceinline__ void run_ops(const uint2 *__restrict__ ops_s, int Q, int rhs_off,
+                                        const double2 *__restrict__ cval, const double2 *__restrict__ mono,
+                                        double2 *__restrict__ M, double *__restrict__ rabs, const int16_t *row_of,
+                                        int r) {
   double2 acc = make_double2(0.0, 0.0);
   double acc_abs = 0.0;
   for (int q = 0; q < Q; ++q) {
-    const uint4 op = ops_s[q * L + r];
-    const int nf = nfac_s[q];
-    const int ci = (int)(op.x & 0xFFFFu) + ((op.y & OP_RHS) ? rhs_off : 0);
-    const double sc = (double)((op.y >> 8) & 0xFFu);
-    double2 v = cval[ci];
-    v.x *= sc;
-    v.y *= sc;
-#pragma unroll
-    for (int m = 0; m < MAX_FACTORS; ++m) {
-      if (m < nf) {
-        const uint32_t w = (m < 4) ? op.z : op.w;
-        v = cmul(v, xs[(w >> (8 * (m & 3))) & 0xFFu]);
-      }
+    const uint2 op = ops_s[q * L + r];
+    const uint32_t fl = op.y >> 16;
+    const double2 c = cval[(int)(op.x & 0xFFFFu) + ((fl & OP_RHS) ? rhs_off : 0)];
+    const double2 m = mono[op.x >> 16];
+    if (ABS) {
+      const double2 v = cmul(c, m);
+      acc.x += v.x;
+      acc.y += v.y;
+      acc_abs += sqrt(abs2(v));
+    } else {
+      acc = cfma(c, m, acc);
     }
-    acc.x += v.x;
-    acc.y += v.y;
-    if (want_abs) acc_abs += sqrt(abs2(v));
-    if (op.y & OP_LAST) {
-      const uint32_t dest = op.x >> 16;
+    if (fl & OP_LAST) {
+      const uint32_t dest = op.y & 0xFFFFu;
       M[dest] = acc;
-      if (want_abs && (op.y & OP_RHS)) rabs[dest / (N + 1)] = acc_abs;
+      if (ABS && (fl & OP_RHS)) rabs[row_of[dest]] = acc_abs;
       acc = make_double2(0.0, 0.0);
       acc_abs = 0.0;
     }
   }
+}
+
+// ------------------------------------------------------------------------------------------
+// Evaluate [dH/dx | rhs] into the slot's M (shared), then fused LU + solve.  Returns the solution
+// component y_r in lane r (r < N) and whether the solve succeeded (uniform over the slot).
+// rhs_off = 0 -> rhs = H (coefficients c(t)); rhs_off = ncoef -> rhs = dH/dt (coefficients c'(t)).
+// ------------------------------------------------------------------------------------------
+template <int N, int L>
+__device__ __forceinline__ bool eval_solve(const TrackArgs &A, const uint2 *__restrict__ ops_s,
+                                           const uint32_t *__restrict__ prog_s, const int16_t *__restrict__ mpos_s,
+                                           const int16_t *__restrict__ row_of, const double2 *__restrict__ ct,
+                                           double t, int rhs_off, bool want_abs, double2 *cval, double2 *mono,
+                                           double2 *M, double2 *prow, double *rabs, int r, int seg, double2 xr,
+                                           double2 &y, double2 &fr, double &fabs_r) {
+  const int ncoef = A.ncoef, D = A.D;
+  // ---- stage x (monomial slots 0..N-1) and coefficient values c(t) (all slots), c'(t) (rhs
+  //      slots) by Horner on the prologue's polynomials in t ----
+  if (r < N) mono[r] = xr;
+  for (int j = r; j < ncoef; j += L) {
+    double2 p = __ldg(&ct[(size_t)D * ncoef + j]);
+    double2 dp = make_double2(0.0, 0.0);
+    for (int d = D - 1; d >= 0; --d) {
+      const double2 a = __ldg(&ct[(size_t)d * ncoef + j]);
+      dp = make_double2(fma(dp.x, t, p.x), fma(dp.y, t, p.y));
+      p = make_double2(fma(p.x, t, a.x), fma(p.y, t, a.y));
+    }
+    cval[j] = p;
+    if (j < A.ncoef_src) cval[ncoef + j] = dp;
+  }
   __syncwarp();
-  // ---- load row r of [A | b] into registers ----
+  // ---- monomial program: degree d products from degree d-1 (shared by all entries) ----
+  int lo = N + 1;
+  for (int l = 0; l < A.n_levels; ++l) {
+    const int hi = A.level_end[l];
+    for (int k = lo + r; k < hi; k += L) {
+      const uint32_t e = prog_s[k - (N + 1)];
+      mono[k] = cmul(mono[e & 0xFFFFu], mono[e >> 16]);
+    }
+    lo = hi;
+    __syncwarp();
+  }
+  // ---- homogenised term evaluation (P:432-434), lane-balanced op list ----
+  if (want_abs) run_ops<N, L, true>(ops_s, A.Q, rhs_off, cval, mono, M, rabs, row_of, r);
+  else run_ops<N, L, false>(ops_s, A.Q, rhs_off, cval, mono, M, rabs, row_of, r);
+  __syncwarp();
+  // ---- load row r of [A | b] into registers (structural zeros from the compact map) ----
   double2 a[N + 1];
 #pragma unroll
-  for (int j = 0; j <= N; ++j) a[j] = (r < N) ? M[r * (N + 1) + j] : make_double2(0.0, 0.0);
+  for (int j = 0; j <= N; ++j) {
+    const int mp = (r < N) ? mpos_s[r * (N + 1) + j] : -1;
+    a[j] = (mp >= 0) ? M[mp] : make_double2(0.0, 0.0);
+  }
   fr = a[N];
   fabs_r = (r < N && want_abs) ? rabs[r] : 0.0;
-  return lu_rows<N, L>(a, r, seg, prow, pivot_rel, y);
+  return lu_rows<N, L>(a, r, seg, prow, A.st.pivot_rel, y);
 }
 
 // ------------------------------------------------------------------------------------------
@@ -214,27 +237,32 @@ __global__ void __launch_bounds__(TRACKER_WARPS * 32) hc_track_kernel(const Trac
   constexpr int TPW = 32 / L;
   extern __shared__ __align__(16) unsigned char smem_raw[];
 
-  // ---- stage the op table in shared memory (constant for the whole kernel) ----
-  uint4 *ops_s = reinterpret_cast<uint4 *>(smem_raw);
+  // ---- stage the op table and the monomial program in shared memory (constant for the kernel) ----
+  uint2 *ops_s = reinterpret_cast<uint2 *>(smem_raw);
   const int nops = A.Q * L;
   for (int i = threadIdx.x; i < nops; i += blockDim.x) ops_s[i] = __ldg(&A.ops[i]);
-  uint8_t *nfac_s = reinterpret_cast<uint8_t *>(ops_s + nops);
-  for (int i = threadIdx.x; i < A.Q; i += blockDim.x) nfac_s[i] = A.step_nfac[i];
-  unsigned char *slots_base = smem_raw + align16(sizeof(uint4) * nops + A.Q);
+  const int nprog = A.n_mono - (N + 1);
+  uint32_t *prog_s = reinterpret_cast<uint32_t *>(smem_raw + align16((size_t)8 * nops));
+  for (int i = threadIdx.x; i < nprog; i += blockDim.x) prog_s[i] = __ldg(&A.mono_prog[i]);
+  int16_t *mpos_s = reinterpret_cast<int16_t *>(smem_raw + align16((size_t)8 * nops) + align16((size_t)4 * nprog));
+  for (int i = threadIdx.x; i < N * (N + 1); i += blockDim.x) mpos_s[i] = __ldg(&A.mpos[i]);
+  unsigned char *slots_base = smem_raw + table_bytes(A.Q, L, nprog, N) + align16((size_t)2 * A.n_entries);
+  // compact entry -> row (for the relative residual of rhs entries)
+  int16_t *row_of = reinterpret_cast<int16_t *>(smem_raw + table_bytes(A.Q, L, nprog, N));
+  for (int i = threadIdx.x; i < N * (N + 1); i += blockDim.x)
+    if (A.mpos[i] >= 0) row_of[A.mpos[i]] = (int16_t)(i / (N + 1));
 
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int seg = lane / L, r = lane % L;
   const int slot = warp * TPW + seg;
   const int ncoef = A.ncoef, D = A.D;
-  unsigned char *sb = slots_base + (size_t)slot * slot_bytes(N, ncoef);
+  unsigned char *sb = slots_base + (size_t)slot * slot_bytes(N, ncoef, A.ncoef_src, A.n_mono, A.n_entries);
   double2 *cval = reinterpret_cast<double2 *>(sb);
-  double2 *xs = cval + 2 * ncoef;
-  double2 *M = xs + (N + 1);
-  double2 *prow = M + N * (N + 1);
+  double2 *mono = cval + ncoef + A.ncoef_src;
+  double2 *M = mono + A.n_mono;
+  double2 *prow = M + A.n_entries;
   double *rabs = reinterpret_cast<double *>(prow + (N + 1));
-  // structural zeros of [A | b] are never written by the op list: zero M once.
-  for (int i = r; i < N * (N + 1); i += L) M[i] = make_double2(0.0, 0.0);
-  if (r == 0) xs[N] = make_double2(1.0, 0.0);   // constant-one slot
+  if (r == 0) mono[N] = make_double2(1.0, 0.0);   // constant-one slot
   __syncthreads();
 
   const DevSettings &st = A.st;
@@ -326,8 +354,8 @@ __global__ void __launch_bounds__(TRACKER_WARPS * 32) hc_track_kernel(const Trac
     const bool want_abs = __any_sync(FULL, state == ST_RESID);
     double2 yv, fr;
     double fa;
-    const bool ok = eval_solve<N, L>(ops_s, nfac_s, A.Q, ncoef, D, ct, te, rhs_off, want_abs, st.pivot_rel, cval,
-                                     xs, M, prow, rabs, r, seg, xe, yv, fr, fa);
+    const bool ok = eval_solve<N, L>(A, ops_s, prog_s, mpos_s, row_of, ct, te, rhs_off, want_abs, cval, mono, M, prow, rabs,
+                                     r, seg, xe, yv, fr, fa);
 
     // ---- slot-uniform reductions, computed on all lanes before any slot-divergent branch ----
     const double2 base = (state == ST_POLISH) ? x : xc;
@@ -417,7 +445,8 @@ template <int N>
 cudaError_t launch_tracker_n(const TrackArgs &A, int device, cudaStream_t stream, TrackerPlan *plan) {
   constexpr int L = (N <= 1) ? 1 : (N <= 2) ? 2 : (N <= 4) ? 4 : (N <= 8) ? 8 : (N <= 16) ? 16 : 32;
   constexpr int TPW = 32 / L;
-  const size_t smem = align16(sizeof(uint4) * A.Q * L + A.Q) + (size_t)TRACKER_WARPS * TPW * slot_bytes(N, A.ncoef);
+  const size_t smem = table_bytes(A.Q, L, A.n_mono - (N + 1), N) + align16((size_t)2 * A.n_entries) +
+                      (size_t)TRACKER_WARPS * TPW * slot_bytes(N, A.ncoef, A.ncoef_src, A.n_mono, A.n_entries);
   cudaError_t e = cudaFuncSetAttribute(hc_track_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   int per_sm = 0;

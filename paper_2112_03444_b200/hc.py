@@ -65,15 +65,22 @@ def hc_system_compile_info(desc) -> dict:
     return info.as_dict()
 
 
-def hc_system_compile_ops(desc):
-    """Host-only: the compiled evaluation op table ([Q, L, 4] uint32) and step factor counts [Q]."""
+def hc_system_compile_tables(desc):
+    """Host-only: the compiled evaluation tables (layouts in csrc/hc_internal.h).
+
+    Returns (ops [Q, L, 2] uint32, mono_prog [n_monos - N - 1] uint32, slot_map [n_coef_slots, 2] int32,
+    entry_map [N, N + 1] int16, info)."""
     info = hc_system_compile_info(desc)
     Q, Ln = info["op_steps"], info["lanes_per_track"]
-    ops = np.zeros((Q, Ln, 4), np.uint32)
-    nfac = np.zeros(Q, np.uint8)
+    ops = np.zeros((Q, Ln, 2), np.uint32)
+    prog = np.zeros(max(0, info["n_monos"] - info["n_vars"] - 1), np.uint32)
+    smap = np.zeros((info["n_coef_slots"], 2), np.int32)
+    N = info["n_vars"]
+    emap = np.zeros((N, N + 1), np.int16)
     d = _Desc(desc)
-    check(L.lib().hc_system_compile_ops(C.byref(d.c), _ptr(ops), _ptr(nfac), Q * Ln), "hc_system_compile_ops")
-    return ops, nfac, info
+    check(L.lib().hc_system_compile_tables(C.byref(d.c), _ptr(ops), _ptr(prog), _ptr(smap), _ptr(emap)),
+          "hc_system_compile_tables")
+    return ops, prog, smap, emap, info
 
 
 class System:
@@ -195,9 +202,10 @@ def track_batch(system: System, start_x, p0=None, p1=None, st: L.hc_tracker_sett
 
 
 def track_batch_host(system: System, start_x, p0=None, p1=None, st: L.hc_tracker_settings | None = None,
-                     stream=None) -> BatchResult:
+                     stream=None, out=None) -> BatchResult:
     """End-to-end call with HOST buffers (HC_MEM_HOST): the library copies inputs to the device,
-    tracks, copies results back and returns when done.  numpy in, numpy out."""
+    tracks, copies results back and returns when done.  numpy in, numpy out (`out` may supply
+    preallocated, e.g. pinned, output arrays (x, status, counters, resid))."""
     start_x = _c128(start_x)
     S, N = start_x.shape
     if system.P > 0:
@@ -206,13 +214,15 @@ def track_batch_host(system: System, start_x, p0=None, p1=None, st: L.hc_tracker
         B = p1.shape[0]
     else:
         B = 1
-    x = np.empty((B, S, N), np.complex128)
-    status = np.empty((B, S), np.int32)
-    ctr = np.empty((B, S, 4), np.int32)
-    resid = np.empty((B, S, 2), np.float64)
-    sp = None
-    if stream is not None:
-        sp = stream.cuda_stream
+    if out is None:
+        x = np.empty((B, S, N), np.complex128)
+        status = np.empty((B, S), np.int32)
+        ctr = np.empty((B, S, 4), np.int32)
+        resid = np.empty((B, S, 2), np.float64)
+    else:
+        x, status, ctr, resid = out
+        assert x.shape == (B, S, N) and x.dtype == np.complex128 and x.flags.c_contiguous
+    sp = stream.cuda_stream if stream is not None else None
     b = L.hc_batch(B, S, _ptr(start_x), _ptr(p0) if system.P else None, _ptr(p1) if system.P else None, _ptr(x),
                    _ptr(status), _ptr(ctr), _ptr(resid), HC_MEM_HOST, sp)
     h = C.c_void_p()

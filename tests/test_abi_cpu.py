@@ -43,40 +43,50 @@ def test_settings_defaults_match_readings(hc):
     assert (s.max_newton, s.newton_tol, s.max_steps, s.inf_norm, s.end_newton) == (3, 1e-8, 10000, 1e14, 3)
 
 
-def _decode(ops, nfac, N):
-    """Interpret the op table: list of (lane, dest, coef, scale, rhs, last, factors)."""
-    out = []
-    Q, Lanes, _ = ops.shape
-    for q in range(Q):
-        for ln in range(Lanes):
-            x, y, z, w = (int(v) for v in ops[q, ln])
-            facs = [(z >> (8 * m)) & 0xFF for m in range(4)] + [(w >> (8 * m)) & 0xFF for m in range(4)]
-            out.append(dict(q=q, lane=ln, coef=x & 0xFFFF, dest=x >> 16, last=bool(y & 1), rhs=bool(y & 2),
-                            scale=(y >> 8) & 0xFF, fac=facs[: int(nfac[q])], allfac=facs))
-    return out
+def mono_factors(prog, N):
+    """Variable multiset of every monomial-table entry: k < N -> [k], k == N -> [] (constant one),
+    k > N -> factors(parent) + [var] (program order is by degree, parents first)."""
+    f = [[k] for k in range(N)] + [[]]
+    for e in prog:
+        f.append(f[int(e) & 0xFFFF] + [int(e) >> 16])
+    return f
 
 
-def eval_ops(ops, nfac, N, cvals, cdvals, x, rhs_dt=False):
-    """Direct interpretation of the compiled table (independent of the CUDA kernel):
-    returns [A | b] with b = H (rhs_dt False) or dH/dt (True)."""
-    xs = np.concatenate([x, [1.0]])
-    M = np.zeros((N, N + 1), complex)
+def decode_ops(ops, N):
+    """Per lane, the op records as dicts (slot, mono, dest, last, rhs)."""
     Q, Lanes, _ = ops.shape
+    lanes = []
     for ln in range(Lanes):
-        acc = 0j
+        rs = []
         for q in range(Q):
-            x_, y_, z_, w_ = (int(v) for v in ops[q, ln])
-            rhs = bool(y_ & 2)
-            c = (cdvals if (rhs and rhs_dt) else cvals)[x_ & 0xFFFF]
-            v = c * ((y_ >> 8) & 0xFF)
-            facs = [(z_ >> (8 * m)) & 0xFF for m in range(4)] + [(w_ >> (8 * m)) & 0xFF for m in range(4)]
-            for m in range(int(nfac[q])):
-                v *= xs[facs[m]]
-            acc += v
-            if y_ & 1:
-                d = x_ >> 16
-                M[d // (N + 1), d % (N + 1)] = acc
+            x, y = int(ops[q, ln, 0]), int(ops[q, ln, 1])
+            fl = y >> 16
+            rs.append(dict(slot=x & 0xFFFF, mono=x >> 16, dest=y & 0xFFFF, last=bool(fl & 1), rhs=bool(fl & 2)))
+        lanes.append(rs)
+    return lanes
+
+
+def eval_tables(ops, prog, smap, emap, N, cvals, x):
+    """Direct interpretation of the compiled tables (independent of the CUDA kernel):
+    returns [A | b] with b = H, coefficient slot value = scale * c_j."""
+    mono = list(x) + [1.0 + 0j]
+    for e in prog:
+        mono.append(mono[int(e) & 0xFFFF] * mono[int(e) >> 16])
+    slotv = [smap[s, 1] * cvals[smap[s, 0]] for s in range(smap.shape[0])]
+    compact = {}
+    for rs in decode_ops(ops, N):
+        acc = 0j
+        for r in rs:
+            acc += slotv[r["slot"]] * mono[r["mono"]]
+            if r["last"]:
+                compact[r["dest"]] = acc
                 acc = 0j
+    M = np.zeros((N, N + 1), complex)
+    for i in range(N):
+        for j in range(N + 1):
+            if emap[i, j] >= 0:
+                M[i, j] = compact[int(emap[i, j])]
+    assert sorted(compact) == list(range(len(compact)))   # every compact entry written exactly once
     return M
 
 
@@ -92,40 +102,35 @@ def test_paper_index_format_example(hc):
     F1 = a[0] * x1 * x1 + 2 * a[1] * x1 * x1 * x2 + 8 * a[2] * x1 * x2 * x2
     F2 = 2.5 * a[3] * x1 * x1 * x2 + 7 * a[4] * x1 * x2 * x2
     d = systems.from_polys([F1, F2], "paper-example")
-    ops, nfac, info = hc.hc_system_compile_ops(d)
+    ops, prog, smap, emap, info = hc.hc_system_compile_tables(d)
+    dense = {int(emap[i, j]): i * (n + 1) + j for i in range(n) for j in range(n + 1) if emap[i, j] >= 0}
     assert info["lanes_per_track"] == 2 and info["max_factors"] == 3
-    recs = _decode(ops, nfac, n)
+    facs = mono_factors(prog, n)
     # coefficient expression j -> (weight, parameter index)
     cw = {j: (complex(d.coef_w[d.coef_ptr[j]]), int(np.argmax(d.coef_pexp[d.coef_ptr[j]]))) for j in range(d.n_coefs)}
 
     def entry_terms(row, col):
-        """(s_k, a index (1-based), sorted 1-based factor indices padded to 2 with the constant slot)."""
-        terms, lanes = [], {}
-        for r in recs:
-            lanes.setdefault(r["lane"], []).append(r)
-        for ln, rs in lanes.items():
+        """(s_k * weight, a index (1-based), sorted 1-based factors padded to 2 with the constant slot N+1)."""
+        terms = []
+        for rs in decode_ops(ops, n):
             cur = []
             for r in rs:
-                if r["scale"] == 0:
-                    continue
                 cur.append(r)
                 if r["last"]:
-                    if r["dest"] == row * (n + 1) + col:
+                    if dense[r["dest"]] == row * (n + 1) + col:
                         for t in cur:
-                            w, q = cw[t["coef"]]
-                            f = sorted(i + 1 for i in t["fac"] if i != n)
+                            j, sc = int(smap[t["slot"], 0]), int(smap[t["slot"], 1])
+                            w, q = cw[j]
+                            f = sorted(i + 1 for i in facs[t["mono"]])
                             f = f + [n + 1] * (2 - len(f))
-                            terms.append((round((t["scale"] * w).real, 12), q + 1, tuple(f)))
+                            terms.append((round((sc * w).real, 12), q + 1, tuple(f)))
                     cur = []
         return sorted(terms)
 
     assert entry_terms(0, 0) == sorted([(2.0, 1, (1, 3)), (4.0, 2, (1, 2)), (8.0, 3, (2, 2))])
     assert entry_terms(1, 0) == sorted([(5.0, 4, (1, 2)), (7.0, 5, (2, 2))])
-    # every factor slot is a variable or the constant-one slot index N (P:430); padding ops have scale 0
-    for r in recs:
-        assert all(0 <= f <= n for f in r["allfac"])
-        if r["dest"] == 0xFFFF and not r["last"] and r["scale"] == 0:
-            assert all(f == n for f in r["allfac"])
+    # the constant-one slot is monomial index N (P:430): a degree-1 term's partner is x3 = 1
+    assert facs[n] == []
 
 
 @pytest.mark.parametrize("name", ["katsura-6", "cyclic-7", "4-view", "trifocal"])
@@ -134,7 +139,7 @@ def test_compiled_table_matches_oracle_evaluation(hc, orc, name):
     (PH: coefficients at p) -- pins the host compiler (differentiation, folding, lane packing)."""
     d = {"katsura-6": lambda: systems.katsura(6), "cyclic-7": lambda: systems.cyclic(7),
          "4-view": lambda: systems.nview_triangulation(4), "trifocal": systems.trifocal_unknown_f}[name]()
-    ops, nfac, info = hc.hc_system_compile_ops(d)
+    ops, prog, smap, emap, info = hc.hc_system_compile_tables(d)
     N = d.n_vars
     assert info["n_ops_rhs"] == d.n_terms
     g = rng.gen(3)
@@ -142,13 +147,17 @@ def test_compiled_table_matches_oracle_evaluation(hc, orc, name):
         p = (g.standard_normal(d.n_params) + 1j * g.standard_normal(d.n_params))
         x = g.standard_normal(N) + 1j * g.standard_normal(N)
         c = orc.eval_coefs(d, p)
-        M = eval_ops(ops, nfac, N, c, np.zeros_like(c), x)
+        M = eval_tables(ops, prog, smap, emap, N, c, x)
         J = orc.eval_JF(d, p, x)
         F = orc.eval_F(d, p, x)
         assert np.max(np.abs(M[:, :N] - J)) <= 1e-12 * (1 + np.max(np.abs(J)))
         assert np.max(np.abs(M[:, N] - F)) <= 1e-12 * (1 + np.max(np.abs(F)))
-    # lane balance: no lane carries more than the ideal share + the largest entry
-    assert info["op_steps"] * info["lanes_per_track"] >= info["n_ops_J"] + info["n_ops_rhs"]
+    # lane balance: every op placed; at most one entry's worth above the ideal share per lane
+    nops = info["n_ops_J"] + info["n_ops_rhs"]
+    assert info["op_steps"] * info["lanes_per_track"] >= nops
+    assert info["op_steps"] <= nops / info["lanes_per_track"] + N + 2
+    # monomial sharing: each table entry is one complex product
+    assert info["n_monos"] - N - 1 == len(prog)
 
 
 def test_flop_model(hc):
