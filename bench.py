@@ -225,6 +225,7 @@ def run_ours(args):
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     elapsed_max = float(t.item())
+    launch = results[0].launch()
     per_launch = [r.elapsed_ms() for r in results]   # (total, prologue, tracker) events on the launch stream
     tracker_ms = statistics.mean(p[2] for p in per_launch)
     prologue_ms = statistics.mean(p[1] for p in per_launch)
@@ -294,7 +295,8 @@ def run_ours(args):
             "scaling": "weak", "vs_baseline": None, "dtype": "c128 (fp64)", "data": "synthetic",
             "instances_per_sec": world * B * args.steps / (elapsed_max / 1e3),
             "config": {"workload": meta["workload"], "instances_per_gpu": B, "tracks_per_instance": S,
-                       "N": N, "l2": "256 MB buffer written between steps (flush)", "parallelism": f"dp{world}"},
+                       "N": N, "l2": "256 MB buffer written between steps (flush)", "parallelism": f"dp{world}",
+                       "launch": launch},
             "roofline": {"bound": "alu", "achieved": achieved, "peak": peak_max, "unit": "TFLOP/s",
                          "frac": achieved / peak_max, "traffic": None,
                          "kernel": "hcb::hc_track_kernel<%d>" % N,

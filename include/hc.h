@@ -191,6 +191,10 @@ hc_status hc_result_wait(hc_result res);
  * kernel, measured with CUDA events on the batch stream; also each kernel alone. */
 hc_status hc_result_elapsed_ms(hc_result res, float *total_ms, float *prologue_ms, float *tracker_ms);
 
+/* Launch configuration the tracker kernel used (lanes per track, warps per CTA, persistent CTAs,
+ * dynamic shared memory per CTA). */
+hc_status hc_result_launch(hc_result res, int32_t *lanes, int32_t *warps_per_cta, int32_t *ctas, int64_t *smem_bytes);
+
 typedef struct {
   int32_t status;       /* hc_track_status */
   int32_t steps, rejections, newton_iters, solves;

@@ -21,7 +21,7 @@ EXPORTED = [
     "hc_system_create", "hc_system_create_total_degree", "hc_total_degree_params", "hc_total_degree_count",
     "hc_total_degree_start", "hc_system_info_get", "hc_system_destroy", "hc_system_compile_info",
     "hc_system_compile_tables", "hc_tracker_settings_default", "hc_track_batch", "hc_result_wait",
-    "hc_result_elapsed_ms", "hc_result_get", "hc_result_destroy", "hc_batched_zgesv", "hc_fp64_peak_probe",
+    "hc_result_elapsed_ms", "hc_result_launch", "hc_result_get", "hc_result_destroy", "hc_batched_zgesv", "hc_fp64_peak_probe",
     "hc_last_error", "hc_version",
 ]
 
@@ -105,6 +105,7 @@ def lib() -> C.CDLL:
     L.hc_track_batch.argtypes = [C.c_void_p, P(hc_tracker_settings), P(hc_batch), P(C.c_void_p)]
     L.hc_result_wait.argtypes = [C.c_void_p]
     L.hc_result_elapsed_ms.argtypes = [C.c_void_p, P(C.c_float), P(C.c_float), P(C.c_float)]
+    L.hc_result_launch.argtypes = [C.c_void_p, P(C.c_int32), P(C.c_int32), P(C.c_int32), P(C.c_int64)]
     L.hc_result_get.argtypes = [C.c_void_p, C.c_int64, C.c_int64, C.c_void_p, P(hc_track_info)]
     L.hc_result_destroy.argtypes = [C.c_void_p]
     L.hc_batched_zgesv.argtypes = [C.c_int32, C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,

@@ -96,6 +96,7 @@ struct hc_result_s {
   double *resid = nullptr;
   bool outputs_on_host = false;
   bool waited = false;
+  TrackerPlan plan{};
 };
 
 static void destroy_result(hc_result r) {
@@ -151,8 +152,12 @@ static hc_status upload_system(hc_system sys) {
   CK(cudaSetDevice(sys->device));
   CK(cudaMalloc(&sys->d_ops, sizeof(uint2) * std::max<size_t>(1, cs.ops.size())));
   CK(cudaMalloc(&sys->d_mono_prog, sizeof(uint32_t) * std::max<size_t>(1, cs.mono_prog.size())));
-  CK(cudaMalloc(&sys->d_mpos, sizeof(int16_t) * cs.mpos.size()));
-  CK(cudaMemcpy(sys->d_mpos, cs.mpos.data(), sizeof(int16_t) * cs.mpos.size(), cudaMemcpyHostToDevice));
+  // device copy of the entry map: structural zeros point at the extra always-zero entry n_entries
+  std::vector<int16_t> mp(cs.mpos);
+  for (auto &v : mp)
+    if (v < 0) v = (int16_t)cs.n_entries;
+  CK(cudaMalloc(&sys->d_mpos, sizeof(int16_t) * mp.size()));
+  CK(cudaMemcpy(sys->d_mpos, mp.data(), sizeof(int16_t) * mp.size(), cudaMemcpyHostToDevice));
   CK(cudaMalloc(&sys->d_mono, sizeof(CoefMono) * std::max<size_t>(1, cs.mono.size())));
   CK(cudaMalloc(&sys->d_mono_ptr, sizeof(int32_t) * cs.mono_ptr.size()));
   if (!cs.ops.empty()) CK(cudaMemcpy(sys->d_ops, cs.ops.data(), sizeof(uint2) * cs.ops.size(), cudaMemcpyHostToDevice));
@@ -292,7 +297,7 @@ static void fill_info(const CompiledSystem &cs, hc_system_info *o) {
   o->mono_levels = cs.n_levels;
   o->flops_eval_kernel = cs.flops_eval_kernel;
   o->flops_solve_kernel = cs.flops_solve_kernel;
-  o->smem_per_track = (int64_t)slot_bytes(cs.N, cs.ncoef, cs.ncoef_src, cs.n_mono, cs.n_entries);
+  o->smem_per_track = (int64_t)slot_bytes(cs.N, cs.ncoef, cs.ncoef_src, cs.n_mono, cs.n_entries + 1);
 }
 
 hc_status hc_system_info_get(hc_system sys, hc_system_info *o) {
@@ -484,8 +489,7 @@ hc_status hc_track_batch(hc_system sys, const hc_tracker_settings *settings, con
   ta.st.max_newton = st.max_newton;
   ta.st.max_steps = st.max_steps;
   ta.st.end_newton = st.end_newton;
-  TrackerPlan plan{};
-  e = tracker_launcher(N)(ta, sys->device, r->stream, &plan);
+  e = tracker_launcher(N)(ta, sys->device, r->stream, &r->plan);
   if (e != cudaSuccess) return bail(cuda_fail(e, "tracker launch"));
   cudaEventRecord(r->ev[2], r->stream);
 
@@ -538,6 +542,15 @@ hc_status hc_result_elapsed_ms(hc_result r, float *total, float *prologue, float
   if (total) *total = a;
   if (prologue) *prologue = b;
   if (tracker) *tracker = c;
+  return HC_OK;
+}
+
+hc_status hc_result_launch(hc_result r, int32_t *lanes, int32_t *warps_per_cta, int32_t *ctas, int64_t *smem_bytes) {
+  if (!r) return fail(HC_E_INVALID_ARG, "null result");
+  if (lanes) *lanes = r->plan.lanes;
+  if (warps_per_cta) *warps_per_cta = r->plan.warps_per_cta;
+  if (ctas) *ctas = r->plan.ctas;
+  if (smem_bytes) *smem_bytes = (int64_t)r->plan.smem_bytes;
   return HC_OK;
 }
 

@@ -21,6 +21,7 @@
 #pragma once
 
 #include <cstdint>
+#include <cstdlib>
 #include <cuda_runtime.h>
 
 #include "../hc_internal.h"
@@ -29,7 +30,15 @@
 namespace hcb {
 
 constexpr unsigned FULL = 0xffffffffu;
-constexpr int TRACKER_WARPS = 4;
+// Warps per CTA and minimum resident CTAs per SM, by N (register budget 65536 / (32 * warps * ctas)):
+//   N <= 14: 4 warps x 4 CTAs (128 regs);  15..20: one 16-warp CTA per SM (128 regs; the trifocal
+//   slot needs ~13.5 KB of shared memory, so 16 slots + one copy of the tables just fit 227 KB);
+//   N > 20: 4 warps x 2 CTAs.  The launcher shrinks the CTA when the shared memory does not fit.
+template <int N>
+struct TrackerShape {
+  static constexpr int MAXW = (N >= 15 && N <= 20) ? 16 : 4;
+  static constexpr int MINB = (N <= 14) ? 4 : (N <= 20) ? 1 : 2;
+};
 
 __device__ __forceinline__ double2 cmul(double2 a, double2 b) {
   return make_double2(fma(a.x, b.x, -a.y * b.y), fma(a.x, b.y, a.y * b.x));
@@ -43,8 +52,19 @@ __device__ __forceinline__ double2 cfms(double2 c, double2 a, double2 b) {
   return make_double2(fma(-a.x, b.x, fma(a.y, b.y, c.x)), fma(-a.x, b.y, fma(-a.y, b.x, c.y)));
 }
 __device__ __forceinline__ double abs2(double2 a) { return fma(a.x, a.x, a.y * a.y); }
+// 1/x for x > 0: MUFU reciprocal estimate + two Newton steps (full FP64 accuracy, no slow-path
+// call; non-finite or zero x gives a non-finite or huge result, and such pivots fail the
+// singularity test anyway).
+__device__ __forceinline__ double frcp(double x) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  double e = fma(-x, r, 1.0);
+  r = fma(r, e, r);
+  e = fma(-x, r, 1.0);
+  return fma(r, e, r);
+}
 __device__ __forceinline__ double2 crecip(double2 a) {
-  double d = 1.0 / abs2(a);
+  const double d = frcp(abs2(a));
   return make_double2(a.x * d, -a.y * d);
 }
 __device__ __forceinline__ bool cfinite(double2 a) { return isfinite(a.x) && isfinite(a.y); }
@@ -73,28 +93,23 @@ __device__ __forceinline__ bool seg_all(bool p, int seg) {
 enum SlotState : int { ST_RK = 0, ST_NEWTON = 1, ST_POLISH = 2, ST_RESID = 3, ST_DONE = 4 };
 
 // ------------------------------------------------------------------------------------------
-// Fused LU with partial pivoting + back-substitution on [A | b] held one row per lane
-// (a[0..N-1] = row r of A, a[N] = b_r).  Pivot = max |a|^2 over the not-yet-pivoted
-// rows (ties -> lower row, reading R13); the pivot row is broadcast through `prow` (shared);
-// singular when |pivot| <= pivot_rel * max|A_ij| (R9) or anything is non-finite.  Returns the
-// solution component y_r in lane r and a slot-uniform success flag.
+// Arg-max of v over the L lanes of a segment; ties -> lowest lane.  v < 0 marks a non-candidate.
+// L == 32: two REDUX (max of the high, then low words of the IEEE bit pattern, which orders
+// non-negative doubles like their values) + one ballot; L < 32: shuffle butterfly.
+// Returns the winning lane (segment-relative) and the maximum value (-1 when no candidate).
 // ------------------------------------------------------------------------------------------
-template <int N, int L>
-__device__ __forceinline__ bool lu_rows(double2 (&a)[N + 1], int r, int seg, double2 *prow, double pivot_rel,
-                                        double2 &y) {
-  bool used = (r >= N);
-  int mystep = used ? N : -1;
-  double2 myinv = make_double2(0.0, 0.0);
-  double am = 0.0;
-#pragma unroll
-  for (int j = 0; j < N; ++j) am = fmax(am, abs2(a[j]));
-  am = seg_max<L>(am);
-  const double thr = pivot_rel * pivot_rel * am;
-  bool sing = !(am < INFINITY);
-#pragma unroll
-  for (int k = 0; k < N; ++k) {
-    double v = used ? -1.0 : abs2(a[k]);
-    if (!(v >= 0.0)) v = -1.0;  // NaN is never a pivot
+template <int L>
+__device__ __forceinline__ int seg_argmax(double v, int r, double &vmax) {
+  if constexpr (L == 32) {
+    const unsigned long long bits = (unsigned long long)__double_as_longlong(v);
+    const unsigned hi = (v >= 0.0) ? (unsigned)(bits >> 32) + 1u : 0u;
+    const unsigned mhi = __reduce_max_sync(FULL, hi);
+    const unsigned lo = (hi == mhi) ? (unsigned)bits : 0u;
+    const unsigned mlo = __reduce_max_sync(FULL, lo);
+    const unsigned ball = __ballot_sync(FULL, hi == mhi && lo == mlo);
+    vmax = (mhi == 0u) ? -1.0 : __longlong_as_double((long long)(((unsigned long long)(mhi - 1u) << 32) | mlo));
+    return __ffs(ball) - 1;
+  } else {
     int idx = r;
 #pragma unroll
     for (int off = L / 2; off >= 1; off >>= 1) {
@@ -105,35 +120,84 @@ __device__ __forceinline__ bool lu_rows(double2 (&a)[N + 1], int r, int seg, dou
         idx = oi;
       }
     }
-    sing |= !(v > thr);
-    if (r == idx) {
+    vmax = v;
+    return idx;
+  }
+}
+
+// ------------------------------------------------------------------------------------------
+// Fused LU with partial pivoting + back-substitution on [A | b] held one row per lane
+// (a[0..N-1] = row r of A, a[N] = b_r) (one kernel, augmented matrix, back-substitution
+// on the cached U).  Pivot = max |a|^2 over the not-yet-pivoted rows (ties -> lowest row, reading
+// R13); singular when |pivot| <= pivot_rel * max|A_ij| (R9) or anything is non-finite.
+// Latency schedule (one warp owns the whole factorisation, so the per-column dependency chain is
+// the cost): the pivot lane publishes 1/pivot and its row in a double-buffered shared row (one
+// __syncwarp per column); every other row updates column k+1 first, the arg-max for step k+1
+// starts on it while the remaining columns are updated.  The pivot order is recorded so
+// back-substitution, which runs on the U rows still held by their lanes, never searches for the
+// source lane; solution components are collected through shared memory.
+// Returns the solution component y_r in lane r and a slot-uniform success flag.
+// prow: 2 * (N + 1) double2; pl: N bytes (per slot shared memory).
+// ------------------------------------------------------------------------------------------
+template <int N, int L>
+__device__ __forceinline__ bool lu_rows(double2 (&a)[N + 1], int r, int seg, double2 *prow, uint8_t *pl,
+                                        double pivot_rel, double2 &y) {
+  bool used = (r >= N);
+  int mystep = used ? N : -1;
+  double2 myinv = make_double2(0.0, 0.0);
+  double am = 0.0;
 #pragma unroll
-      for (int j = k; j <= N; ++j) prow[j] = a[j];
+  for (int j = 0; j < N; ++j) am = fmax(am, abs2(a[j]));
+  am = seg_max<L>(am);
+  const double thr = pivot_rel * pivot_rel * am;
+  bool sing = !(am < INFINITY);
+  // pivot of step 0
+  double vmax;
+  double v0 = used ? -1.0 : abs2(a[0]);
+  if (!(v0 >= 0.0)) v0 = -1.0;   // NaN is never a pivot
+  int p = seg_argmax<L>(v0, r, vmax);
+  sing |= !(vmax > thr);
+#pragma unroll
+  for (int k = 0; k < N; ++k) {
+    double2 *pr = prow + (k & 1) * (N + 1);
+    if (r == p) {   // the pivot lane publishes 1/pivot (at slot k) and its row right of k
+      const double2 spec = crecip(a[k]);
+      pr[k] = spec;
+#pragma unroll
+      for (int j = k + 1; j <= N; ++j) pr[j] = a[j];
+      pl[k] = (uint8_t)r;
       used = true;
       mystep = k;
+      myinv = spec;
     }
     __syncwarp();
-    const double2 inv = crecip(prow[k]);
-    if (r == idx) myinv = inv;
-    if (!used) {
-      const double2 l = cmul(a[k], inv);
+    if (k + 1 < N) {
+      // multiplier; rows already pivoted (and padding lanes) use l = 0, which leaves them unchanged
+      // (a - 0 * u = a for finite u; a non-finite u fails the solve anyway) without a branch
+      const double2 lc = cmul(a[k], pr[k]);
+      const double2 l = used ? make_double2(0.0, 0.0) : lc;
+      a[k + 1] = cfms(a[k + 1], l, pr[k + 1]);
+      double v = used ? -1.0 : abs2(a[k + 1]);
+      if (!(v >= 0.0)) v = -1.0;
+      p = seg_argmax<L>(v, r, vmax);
 #pragma unroll
-      for (int j = k + 1; j <= N; ++j) a[j] = cfms(a[j], l, prow[j]);
+      for (int j = k + 2; j <= N; ++j) a[j] = cfms(a[j], l, pr[j]);
+      sing |= !(vmax > thr);
     }
-    __syncwarp();
   }
-  // ---- back-substitution on the cached U: lane with mystep == k holds U row k ----
-  double2 sol = make_double2(0.0, 0.0);
+  __syncwarp();
+  // ---- back-substitution on the cached U: lane pl[k] holds U row k (a[k..N]) and 1/U_kk ----
+  double2 *xsol = prow + 2 * (N + 1) - N;   // second pivot-row buffer: free after the elimination
 #pragma unroll
   for (int k = N - 1; k >= 0; --k) {
-    const unsigned bal = __ballot_sync(FULL, mystep == k);
-    const unsigned segbits = (L == 32) ? bal : ((bal >> (seg * L)) & seg_mask<L>());
-    const int src = __ffs(segbits) - 1;
-    const double2 cand = (mystep == k) ? cmul(a[N], myinv) : make_double2(0.0, 0.0);
-    const double2 xk = shfl2(cand, src < 0 ? 0 : src, L);
-    if (mystep < k) a[N] = cfms(a[N], a[k], xk);
-    if (r == k) sol = xk;
+    const int src = pl[k];
+    const double2 xk = shfl2(cmul(a[N], myinv), src, L);
+    const double2 u = (mystep < k) ? a[k] : make_double2(0.0, 0.0);   // U_{mystep,k}, or 0
+    a[N] = cfms(a[N], u, xk);
+    if (r == 0) xsol[k] = xk;
   }
+  __syncwarp();
+  const double2 sol = (r < N) ? xsol[r] : make_double2(0.0, 0.0);
   y = sol;
   return seg_all<L>(!sing && cfinite(sol), seg);
 }
@@ -150,6 +214,7 @@ __device__ __forceinline__ void run_ops(const uint2 *__restrict__ ops_s, int Q, 
                                         int r) {
   double2 acc = make_double2(0.0, 0.0);
   double acc_abs = 0.0;
+#pragma unroll(ABS ? 1 : 4)
   for (int q = 0; q < Q; ++q) {
     const uint2 op = ops_s[q * L + r];
     const uint32_t fl = op.y >> 16;
@@ -174,6 +239,40 @@ __device__ __forceinline__ void run_ops(const uint2 *__restrict__ ops_s, int Q, 
 }
 
 // ------------------------------------------------------------------------------------------
+// Coefficient values at t: c_j(t) for every slot and c_j'(t) for the rhs slots (j < nsrc), by
+// Horner on the prologue's polynomials coef_t[d][j] (d <= D); two slots per lane per iteration,
+// all loads issued before the FMA chains.
+// ------------------------------------------------------------------------------------------
+template <int D, int L>
+__device__ __forceinline__ void horner(const double2 *__restrict__ ct, double t, int ncoef, int nsrc,
+                                       double2 *__restrict__ cval, int r) {
+  for (int j0 = r; j0 < ncoef; j0 += 2 * L) {
+    const int j1 = j0 + L;
+    const bool has1 = j1 < ncoef;
+    double2 c0[D + 1], c1[D + 1];
+#pragma unroll
+    for (int d = 0; d <= D; ++d) {
+      c0[d] = __ldg(&ct[(size_t)d * ncoef + j0]);
+      c1[d] = has1 ? __ldg(&ct[(size_t)d * ncoef + j1]) : make_double2(0.0, 0.0);
+    }
+    double2 p0 = c0[D], p1 = c1[D], q0 = make_double2(0.0, 0.0), q1 = q0;
+#pragma unroll
+    for (int d = D - 1; d >= 0; --d) {
+      q0 = make_double2(fma(q0.x, t, p0.x), fma(q0.y, t, p0.y));
+      q1 = make_double2(fma(q1.x, t, p1.x), fma(q1.y, t, p1.y));
+      p0 = make_double2(fma(p0.x, t, c0[d].x), fma(p0.y, t, c0[d].y));
+      p1 = make_double2(fma(p1.x, t, c1[d].x), fma(p1.y, t, c1[d].y));
+    }
+    cval[j0] = p0;
+    if (j0 < nsrc) cval[ncoef + j0] = q0;
+    if (has1) {
+      cval[j1] = p1;
+      if (j1 < nsrc) cval[ncoef + j1] = q1;
+    }
+  }
+}
+
+// ------------------------------------------------------------------------------------------
 // Evaluate [dH/dx | rhs] into the slot's M (shared), then fused LU + solve.  Returns the solution
 // component y_r in lane r (r < N) and whether the solve succeeded (uniform over the slot).
 // rhs_off = 0 -> rhs = H (coefficients c(t)); rhs_off = ncoef -> rhs = dH/dt (coefficients c'(t)).
@@ -183,22 +282,29 @@ __device__ __forceinline__ bool eval_solve(const TrackArgs &A, const uint2 *__re
                                            const uint32_t *__restrict__ prog_s, const int16_t *__restrict__ mpos_s,
                                            const int16_t *__restrict__ row_of, const double2 *__restrict__ ct,
                                            double t, int rhs_off, bool want_abs, double2 *cval, double2 *mono,
-                                           double2 *M, double2 *prow, double *rabs, int r, int seg, double2 xr,
+                                           double2 *M, double2 *prow, double *rabs, uint8_t *pl, int r, int seg,
+                                           double2 xr,
                                            double2 &y, double2 &fr, double &fabs_r) {
   const int ncoef = A.ncoef, D = A.D;
   // ---- stage x (monomial slots 0..N-1) and coefficient values c(t) (all slots), c'(t) (rhs
   //      slots) by Horner on the prologue's polynomials in t ----
   if (r < N) mono[r] = xr;
-  for (int j = r; j < ncoef; j += L) {
-    double2 p = __ldg(&ct[(size_t)D * ncoef + j]);
-    double2 dp = make_double2(0.0, 0.0);
-    for (int d = D - 1; d >= 0; --d) {
-      const double2 a = __ldg(&ct[(size_t)d * ncoef + j]);
-      dp = make_double2(fma(dp.x, t, p.x), fma(dp.y, t, p.y));
-      p = make_double2(fma(p.x, t, a.x), fma(p.y, t, a.y));
-    }
-    cval[j] = p;
-    if (j < A.ncoef_src) cval[ncoef + j] = dp;
+  switch (D) {   // D is uniform: the common degrees keep all loads of a coefficient in flight together
+    case 1: horner<1, L>(ct, t, ncoef, A.ncoef_src, cval, r); break;
+    case 2: horner<2, L>(ct, t, ncoef, A.ncoef_src, cval, r); break;
+    case 3: horner<3, L>(ct, t, ncoef, A.ncoef_src, cval, r); break;
+    default:
+      for (int j = r; j < ncoef; j += L) {
+        double2 p = __ldg(&ct[(size_t)D * ncoef + j]), q = make_double2(0.0, 0.0);
+#pragma unroll 1
+        for (int d = D - 1; d >= 0; --d) {
+          const double2 c = __ldg(&ct[(size_t)d * ncoef + j]);
+          q = make_double2(fma(q.x, t, p.x), fma(q.y, t, p.y));
+          p = make_double2(fma(p.x, t, c.x), fma(p.y, t, c.y));
+        }
+        cval[j] = p;
+        if (j < A.ncoef_src) cval[ncoef + j] = q;
+      }
   }
   __syncwarp();
   // ---- monomial program: degree d products from degree d-1 (shared by all entries) ----
@@ -216,23 +322,25 @@ __device__ __forceinline__ bool eval_solve(const TrackArgs &A, const uint2 *__re
   if (want_abs) run_ops<N, L, true>(ops_s, A.Q, rhs_off, cval, mono, M, rabs, row_of, r);
   else run_ops<N, L, false>(ops_s, A.Q, rhs_off, cval, mono, M, rabs, row_of, r);
   __syncwarp();
-  // ---- load row r of [A | b] into registers (structural zeros from the compact map) ----
+  // ---- load row r of [A | b] into registers (structural zeros read the always-zero entry) ----
   double2 a[N + 1];
+  const int rr = (r < N) ? r : 0;
 #pragma unroll
-  for (int j = 0; j <= N; ++j) {
-    const int mp = (r < N) ? mpos_s[r * (N + 1) + j] : -1;
-    a[j] = (mp >= 0) ? M[mp] : make_double2(0.0, 0.0);
+  for (int j = 0; j <= N; ++j) a[j] = M[mpos_s[rr * (N + 1) + j]];
+  if (r >= N) {
+#pragma unroll
+    for (int j = 0; j <= N; ++j) a[j] = make_double2(0.0, 0.0);
   }
   fr = a[N];
   fabs_r = (r < N && want_abs) ? rabs[r] : 0.0;
-  return lu_rows<N, L>(a, r, seg, prow, A.st.pivot_rel, y);
+  return lu_rows<N, L>(a, r, seg, prow, pl, A.st.pivot_rel, y);
 }
 
 // ------------------------------------------------------------------------------------------
 // The persistent tracker kernel.
 // ------------------------------------------------------------------------------------------
 template <int N>
-__global__ void __launch_bounds__(TRACKER_WARPS * 32) hc_track_kernel(const TrackArgs A) {
+__global__ void __launch_bounds__(TrackerShape<N>::MAXW * 32, TrackerShape<N>::MINB) hc_track_kernel(const TrackArgs A) {
   constexpr int L = (N <= 1) ? 1 : (N <= 2) ? 2 : (N <= 4) ? 4 : (N <= 8) ? 8 : (N <= 16) ? 16 : 32;
   constexpr int TPW = 32 / L;
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -250,19 +358,23 @@ __global__ void __launch_bounds__(TRACKER_WARPS * 32) hc_track_kernel(const Trac
   // compact entry -> row (for the relative residual of rhs entries)
   int16_t *row_of = reinterpret_cast<int16_t *>(smem_raw + table_bytes(A.Q, L, nprog, N));
   for (int i = threadIdx.x; i < N * (N + 1); i += blockDim.x)
-    if (A.mpos[i] >= 0) row_of[A.mpos[i]] = (int16_t)(i / (N + 1));
+    if (A.mpos[i] < A.n_entries) row_of[A.mpos[i]] = (int16_t)(i / (N + 1));
 
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int seg = lane / L, r = lane % L;
   const int slot = warp * TPW + seg;
   const int ncoef = A.ncoef, D = A.D;
-  unsigned char *sb = slots_base + (size_t)slot * slot_bytes(N, ncoef, A.ncoef_src, A.n_mono, A.n_entries);
+  unsigned char *sb = slots_base + (size_t)slot * slot_bytes(N, ncoef, A.ncoef_src, A.n_mono, A.n_entries + 1);
   double2 *cval = reinterpret_cast<double2 *>(sb);
   double2 *mono = cval + ncoef + A.ncoef_src;
   double2 *M = mono + A.n_mono;
-  double2 *prow = M + A.n_entries;
-  double *rabs = reinterpret_cast<double *>(prow + (N + 1));
-  if (r == 0) mono[N] = make_double2(1.0, 0.0);   // constant-one slot
+  double2 *prow = M + A.n_entries + 1;
+  double *rabs = reinterpret_cast<double *>(prow + 2 * (N + 1));
+  uint8_t *pl = reinterpret_cast<uint8_t *>(rabs + N);
+  if (r == 0) {
+    mono[N] = make_double2(1.0, 0.0);            // constant-one slot
+    M[A.n_entries] = make_double2(0.0, 0.0);     // the entry every structural zero reads
+  }
   __syncthreads();
 
   const DevSettings &st = A.st;
@@ -355,7 +467,7 @@ __global__ void __launch_bounds__(TRACKER_WARPS * 32) hc_track_kernel(const Trac
     double2 yv, fr;
     double fa;
     const bool ok = eval_solve<N, L>(A, ops_s, prog_s, mpos_s, row_of, ct, te, rhs_off, want_abs, cval, mono, M, prow, rabs,
-                                     r, seg, xe, yv, fr, fa);
+                                     pl, r, seg, xe, yv, fr, fa);
 
     // ---- slot-uniform reductions, computed on all lanes before any slot-divergent branch ----
     const double2 base = (state == ST_POLISH) ? x : xc;
@@ -445,28 +557,38 @@ template <int N>
 cudaError_t launch_tracker_n(const TrackArgs &A, int device, cudaStream_t stream, TrackerPlan *plan) {
   constexpr int L = (N <= 1) ? 1 : (N <= 2) ? 2 : (N <= 4) ? 4 : (N <= 8) ? 8 : (N <= 16) ? 16 : 32;
   constexpr int TPW = 32 / L;
-  const size_t smem = table_bytes(A.Q, L, A.n_mono - (N + 1), N) + align16((size_t)2 * A.n_entries) +
-                      (size_t)TRACKER_WARPS * TPW * slot_bytes(N, A.ncoef, A.ncoef_src, A.n_mono, A.n_entries);
+  const size_t tables = table_bytes(A.Q, L, A.n_mono - (N + 1), N) + align16((size_t)2 * A.n_entries);
+  const size_t per_warp = (size_t)TPW * slot_bytes(N, A.ncoef, A.ncoef_src, A.n_mono, A.n_entries + 1);
+  int smem_max = 0;
+  cudaDeviceGetAttribute(&smem_max, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
+  int warps = TrackerShape<N>::MAXW;
+  if (const char *ev = getenv("HC_TRACKER_WARPS")) {   // experiment override (<= compile-time max)
+    const int w = atoi(ev);
+    if (w >= 1 && w < warps) warps = w;
+  }
+  while (warps > 1 && tables + warps * per_warp > (size_t)smem_max) --warps;
+  const size_t smem = tables + warps * per_warp;
+  if (smem > (size_t)smem_max) return cudaErrorInvalidConfiguration;
   cudaError_t e = cudaFuncSetAttribute(hc_track_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   int per_sm = 0;
-  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, hc_track_kernel<N>, TRACKER_WARPS * 32, smem);
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, hc_track_kernel<N>, warps * 32, smem);
   if (e != cudaSuccess) return e;
   if (per_sm < 1) return cudaErrorInvalidConfiguration;
   int sms = 0;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
-  long long slots_needed = (A.total + TPW - 1) / TPW;
+  const long long slots_needed = (A.total + TPW - 1) / TPW;
   long long ctas = (long long)per_sm * sms;
-  long long ctas_needed = (slots_needed + TRACKER_WARPS - 1) / TRACKER_WARPS;
+  const long long ctas_needed = (slots_needed + warps - 1) / warps;
   if (ctas_needed < ctas) ctas = ctas_needed;
   if (ctas < 1) ctas = 1;
   if (plan) {
     plan->lanes = L;
-    plan->warps_per_cta = TRACKER_WARPS;
+    plan->warps_per_cta = warps;
     plan->ctas = (int)ctas;
     plan->smem_bytes = smem;
   }
-  hc_track_kernel<N><<<(unsigned)ctas, TRACKER_WARPS * 32, smem, stream>>>(A);
+  hc_track_kernel<N><<<(unsigned)ctas, warps * 32, smem, stream>>>(A);
   return cudaGetLastError();
 }
 

@@ -151,6 +151,12 @@ class BatchResult:
     def wait(self):
         check(L.lib().hc_result_wait(self.handle), "hc_result_wait")
 
+    def launch(self) -> dict:
+        """Tracker launch configuration (hc_result_launch)."""
+        a, b, c, d = C.c_int32(), C.c_int32(), C.c_int32(), C.c_int64()
+        check(L.lib().hc_result_launch(self.handle, C.byref(a), C.byref(b), C.byref(c), C.byref(d)), "hc_result_launch")
+        return {"lanes_per_track": a.value, "warps_per_cta": b.value, "ctas": c.value, "smem_per_cta": d.value}
+
     def close(self):
         if self.handle:
             L.lib().hc_result_destroy(self.handle)
