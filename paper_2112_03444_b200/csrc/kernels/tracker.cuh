@@ -131,9 +131,11 @@ __device__ __forceinline__ int seg_argmax(double v, int r, double &vmax) {
 // on the cached U).  Pivot = max |a|^2 over the not-yet-pivoted rows (ties -> lowest row, reading
 // R13); singular when |pivot| <= pivot_rel * max|A_ij| (R9) or anything is non-finite.
 // Latency schedule (one warp owns the whole factorisation, so the per-column dependency chain is
-// the cost): the pivot lane publishes 1/pivot and its row in a double-buffered shared row (one
-// __syncwarp per column); every other row updates column k+1 first, the arg-max for step k+1
-// starts on it while the remaining columns are updated.  The pivot order is recorded so
+// the cost): every lane computes 1/a_rk of its candidate speculatively; once the arg-max names the
+// pivot lane, 1/pivot and the pivot row's column k+1 are shuffled from it while the rest of its row
+// goes through a double-buffered shared row (one __syncwarp per column); every other row updates
+// column k+1 first, and the arg-max for step k+1 starts on it while the remaining columns are
+// updated.  The pivot order is recorded so
 // back-substitution, which runs on the U rows still held by their lanes, never searches for the
 // source lane; solution components are collected through shared memory.
 // Returns the solution component y_r in lane r and a slot-uniform success flag.
@@ -157,29 +159,32 @@ __device__ __forceinline__ bool lu_rows(double2 (&a)[N + 1], int r, int seg, dou
   if (!(v0 >= 0.0)) v0 = -1.0;   // NaN is never a pivot
   int p = seg_argmax<L>(v0, r, vmax);
   sing |= !(vmax > thr);
+  double2 spec = crecip(a[0]);   // speculative 1/a_rk of this lane's candidate (overlaps the search)
 #pragma unroll
   for (int k = 0; k < N; ++k) {
     double2 *pr = prow + (k & 1) * (N + 1);
-    if (r == p) {   // the pivot lane publishes 1/pivot (at slot k) and its row right of k
-      const double2 spec = crecip(a[k]);
-      pr[k] = spec;
+    // early broadcast from the pivot lane by shuffles: 1/pivot and the pivot row's column k+1
+    const double2 inv = shfl2(spec, p, L);
+    const double2 u1 = shfl2(a[k + 1], p, L);
+    if (r == p) {   // the pivot lane publishes the rest of its row (columns k+2..N) through shared memory
 #pragma unroll
-      for (int j = k + 1; j <= N; ++j) pr[j] = a[j];
+      for (int j = k + 2; j <= N; ++j) pr[j] = a[j];
       pl[k] = (uint8_t)r;
       used = true;
       mystep = k;
       myinv = spec;
     }
-    __syncwarp();
     if (k + 1 < N) {
       // multiplier; rows already pivoted (and padding lanes) use l = 0, which leaves them unchanged
       // (a - 0 * u = a for finite u; a non-finite u fails the solve anyway) without a branch
-      const double2 lc = cmul(a[k], pr[k]);
+      const double2 lc = cmul(a[k], inv);
       const double2 l = used ? make_double2(0.0, 0.0) : lc;
-      a[k + 1] = cfms(a[k + 1], l, pr[k + 1]);
+      a[k + 1] = cfms(a[k + 1], l, u1);
       double v = used ? -1.0 : abs2(a[k + 1]);
       if (!(v >= 0.0)) v = -1.0;
+      spec = crecip(a[k + 1]);
       p = seg_argmax<L>(v, r, vmax);
+      __syncwarp();   // the published row is visible
 #pragma unroll
       for (int j = k + 2; j <= N; ++j) a[j] = cfms(a[j], l, pr[j]);
       sing |= !(vmax > thr);
@@ -212,7 +217,9 @@ __device__ __forceinline__ void run_ops(const uint2 *__restrict__ ops_s, int Q, 
                                         const double2 *__restrict__ cval, const double2 *__restrict__ mono,
                                         double2 *__restrict__ M, double *__restrict__ rabs, const int16_t *row_of,
                                         int r) {
-  double2 acc = make_double2(0.0, 0.0);
+  // the complex product is split over two accumulators (c.x*m and -c.y*conj-swap(m)) so the
+  // four DFMAs of an op depend only on the previous op's same-part accumulator (chain of 1)
+  double2 acc = make_double2(0.0, 0.0), acc2 = make_double2(0.0, 0.0);
   double acc_abs = 0.0;
 #pragma unroll(ABS ? 1 : 4)
   for (int q = 0; q < Q; ++q) {
@@ -220,19 +227,17 @@ __device__ __forceinline__ void run_ops(const uint2 *__restrict__ ops_s, int Q, 
     const uint32_t fl = op.y >> 16;
     const double2 c = cval[(int)(op.x & 0xFFFFu) + ((fl & OP_RHS) ? rhs_off : 0)];
     const double2 m = mono[op.x >> 16];
-    if (ABS) {
-      const double2 v = cmul(c, m);
-      acc.x += v.x;
-      acc.y += v.y;
-      acc_abs += sqrt(abs2(v));
-    } else {
-      acc = cfma(c, m, acc);
-    }
+    if (ABS) acc_abs += sqrt(abs2(cmul(c, m)));
+    acc.x = fma(c.x, m.x, acc.x);
+    acc.y = fma(c.x, m.y, acc.y);
+    acc2.x = fma(-c.y, m.y, acc2.x);
+    acc2.y = fma(c.y, m.x, acc2.y);
     if (fl & OP_LAST) {
       const uint32_t dest = op.y & 0xFFFFu;
-      M[dest] = acc;
+      M[dest] = make_double2(acc.x + acc2.x, acc.y + acc2.y);
       if (ABS && (fl & OP_RHS)) rabs[row_of[dest]] = acc_abs;
       acc = make_double2(0.0, 0.0);
+      acc2 = make_double2(0.0, 0.0);
       acc_abs = 0.0;
     }
   }

@@ -208,3 +208,130 @@ def test_trifocal_ph_parity_sampled(hc, orc):
     assert both.mean() > 0.8
     close = np.all(np.abs(Xg[both] - ref.x[0][both]) <= TOL * np.maximum(1, np.abs(ref.x[0][both])), axis=1)
     assert close.mean() >= 0.97
+
+
+# ------------------------------------------------------------------ edge cases
+
+def _linear_plus_quadratic(n, nq, seed):
+    """n-unknown system: nq quadratic equations + (n - nq) linear ones, random complex coefficients
+    (2^nq finite roots generically) -- exercises large-N instantiations with few tracks."""
+    from hc_inputs.poly import const, var_x
+    g = rng.gen(seed)
+    X = [var_x(n, 0, i) for i in range(n)]
+    c = lambda: complex(g.standard_normal(), g.standard_normal())   # noqa: E731
+    eqs = []
+    for i in range(n):
+        f = const(n, 0, c())
+        for v in range(n):
+            f = f + c() * X[v]
+        if i < nq:
+            f = f + c() * X[i] * X[(i + 1) % n] + c() * X[i] * X[i]
+        eqs.append(f)
+    return systems.from_polys(eqs, f"lin{n}q{nq}")
+
+
+@pytest.mark.parametrize("n,nq", [(1, 1), (17, 3), (24, 2), (32, 3)])
+def test_large_n_instantiations(hc, orc, n, nq):
+    """N = 17..32 kernels (32-lane tracks, large register rows) match the oracle set."""
+    d = _linear_plus_quadratic(n, nq, 1000 + n)
+    gam = rng.gamma(n)
+    res, _ = run_td(hc, d, gam)
+    ref = orc.track(orc.td_homotopy(d, gam), orc.td_start(d.degrees()))
+    A = orc.dedup(orc.finite_solutions(ref))[0]
+    B = gpu_set(orc, res)
+    assert len(A) == 2 ** nq
+    assert_same_set(orc, A, B, f"lin{n}q{nq}")
+
+
+def test_single_track_and_ragged_batches(hc, orc):
+    """S = 1, B = 1 and a batch size that does not fill a warp of 2-track slots."""
+    d = systems.nview_triangulation(4)
+    start = fixtures.read_solutions(fixtures.fixture_path("fourview_start.sols"))
+    p0 = fixtures.read_params(fixtures.fixture_path("fourview_p0.params"))
+    p1s, xs = rng.fourview_batch(3)
+    one = run_ph(hc, d, start[:1], p0, p1s[:1])
+    ref = orc.track(orc.ph_homotopy(d, p0), start[:1], p1s=p1s[:1])
+    assert one.status.cpu().numpy()[0, 0] == ref.status[0, 0]
+    if ref.status[0, 0] == 0:
+        assert np.allclose(one.x.cpu().numpy()[0, 0], ref.x[0, 0], rtol=TOL, atol=TOL)
+    odd = run_ph(hc, d, start[:7], p0, p1s)
+    ref = orc.track(orc.ph_homotopy(d, p0), start[:7], p1s=p1s)
+    st = odd.status.cpu().numpy()
+    X = odd.x.cpu().numpy()
+    both = (st == 0) & (ref.status == 0)
+    assert both.sum() >= 0.8 * both.size
+    assert np.all(np.abs(X[both] - ref.x[both]) <= TOL * np.maximum(1, np.abs(ref.x[both])))
+
+
+def test_invalid_batches_rejected(hc):
+    from paper_2112_03444_b200._lib import HC_E_INVALID_ARG
+    d = systems.katsura(3)
+    s = hc.System.total_degree_homotopy(d, device=0)
+    p0, p1 = s.td_params(rng.gamma(0))
+    X0 = s.td_start()
+    with pytest.raises(hc.HCError) as e:
+        hc.track_batch(s, _cuda(X0), _cuda(p0), _cuda(p1)[None], st=hc.settings(dt_min=1.0))
+    assert e.value.code == HC_E_INVALID_ARG
+    with pytest.raises(hc.HCError) as e:
+        hc.track_batch(s, _cuda(X0), _cuda(p0), _cuda(np.zeros((0, p1.shape[0]), complex)))
+    assert e.value.code == HC_E_INVALID_ARG
+    with pytest.raises(hc.HCError):
+        s.td_params(0.0)
+
+
+def test_euler_predictor_setting(hc, orc):
+    """Euler (Eq. 4) as a setting: same solution set as the oracle with the same setting."""
+    d = systems.katsura(4)
+    gam = rng.gamma(5)
+    res, _ = run_td(hc, d, gam, st=hc.settings(predictor=hc.HC_EULER))
+    ost = orc.default_settings()
+    ost.predictor = 1
+    ref = orc.track(orc.td_homotopy(d, gam), orc.td_start(d.degrees()), settings=ost)
+    assert_same_set(orc, orc.dedup(orc.finite_solutions(ref))[0], gpu_set(orc, res), "katsura-4 Euler")
+
+
+# ------------------------------------------------------------------ full configuration sizes
+
+def test_fourview_config3_full_batch_sampled(hc, orc):
+    """Config 3 at full size (1024 instances x 296 tracks, bench launch configuration); sampled
+    instances compared with the oracle as sets; every instance recovers its planted x*."""
+    d = systems.nview_triangulation(4)
+    start = fixtures.read_solutions(fixtures.fixture_path("fourview_start.sols"))
+    p0 = fixtures.read_params(fixtures.fixture_path("fourview_p0.params"))
+    p1s, xs = rng.fourview_batch(1024)
+    res = run_ph(hc, d, start, p0, p1s)
+    st = res.status.cpu().numpy()
+    X = res.x.cpu().numpy()
+    for b in range(1024):
+        G = X[b][st[b] == 0]
+        assert np.min(np.max(np.abs(G - xs[b]), axis=1)) < 1e-8, b
+    for b in (0, 511, 1023):
+        ref = orc.track(orc.ph_homotopy(d, p0), start, p1s=p1s[b:b + 1])
+        assert_same_set(orc, orc.dedup(ref.x[0][ref.status[0] == 0])[0], orc.dedup(X[b][st[b] == 0])[0],
+                        f"4-view instance {b}")
+
+
+def test_trifocal_config4_full_batch_sampled(hc, orc):
+    """Config 4 at full size (1024 instances x 5328 tracks, the bench workload): sampled tracks
+    from spread-out instances agree with the oracle one by one; planted ground truth recovered."""
+    d = systems.trifocal_unknown_f()
+    start, p0 = fixtures.trifocal_start()
+    p1s, xg = rng.trifocal_batch(1024)
+    res = run_ph(hc, d, start, p0, p1s)
+    st = res.status.cpu().numpy()
+    X = res.x.cpu().numpy()
+    assert (st == 0).mean() > 0.9
+    for b in range(0, 1024, 64):
+        imgs = np.array(systems.trifocal_symmetry(xg[b]))
+        G = X[b][st[b] == 0]
+        assert min(np.min(np.max(np.abs(G - y), axis=1)) for y in imgs) < 1e-8, b
+    g = rng.gen(77)
+    agree = tot = 0
+    for b in (0, 300, 777, 1023):
+        idx = g.choice(start.shape[0], 12, replace=False)
+        ref = orc.track(orc.ph_homotopy(d, p0), start[idx], p1s=p1s[b:b + 1])
+        for k, s in enumerate(idx):
+            if ref.status[0, k] == 0 and st[b, s] == 0:
+                tot += 1
+                agree += np.all(np.abs(X[b, s] - ref.x[0, k]) <= TOL * np.maximum(1, np.abs(ref.x[0, k])))
+    assert tot >= 30 and agree >= 0.95 * tot
