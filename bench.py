@@ -171,11 +171,13 @@ def run_ours(args):
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+    distributed = world > 1 or "TORCHELASTIC_RUN_ID" in os.environ or args.gather
+    if distributed:
+        dist.init_process_group("nccl", device_id=dev, init_method=None if "MASTER_ADDR" in os.environ
+                                else "tcp://127.0.0.1:29533", world_size=world, rank=rank)
 
     def barrier():
-        if world > 1:
+        if distributed:
             dist.barrier(device_ids=[local_rank])
 
     B = args.instances
@@ -227,7 +229,7 @@ def run_ours(args):
     ck = clocks.stop()
     elapsed = e0.elapsed_time(e1)
     t = torch.tensor([elapsed], dtype=torch.float64, device=dev)
-    if world > 1:
+    if distributed:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     elapsed_max = float(t.item())
     launch = results[0].launch()
@@ -250,7 +252,7 @@ def run_ours(args):
 
     # ---- gather solutions to rank 0 (NCCL), timed separately ----
     gather_ms = None
-    if world > 1:
+    if distributed:
         barrier()
         torch.cuda.synchronize()
         g0 = time.perf_counter()
@@ -279,7 +281,7 @@ def run_ours(args):
             hc.track_batch_host(sysh, hstart, hp0, hp1, st=st, out=(hx, hs, hcn, hr)).close()
         w = time.perf_counter() - w0
         tw = torch.tensor([w], dtype=torch.float64, device=dev)
-        if world > 1:
+        if distributed:
             dist.all_reduce(tw, op=dist.ReduceOp.MAX)
         h2d = hstart.nbytes + hp0.nbytes + hp1.nbytes
         d2h = hx.nbytes + hs.nbytes + hcn.nbytes + hr.nbytes
@@ -315,7 +317,7 @@ def run_ours(args):
             "solves_per_track": solves / (B * S),
         }
         print(json.dumps(line), flush=True)
-    if world > 1:
+    if distributed:
         dist.destroy_process_group()
 
 
@@ -330,6 +332,7 @@ def main():
     ap.add_argument("--warmup-instances", type=int, default=16)
     ap.add_argument("--e2e-steps", type=int, default=1)
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--gather", action="store_true", help="init NCCL and run the final gather even on 1 GPU")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget-s", type=float, default=15.0)
     ap.add_argument("--ref-step-s", type=float, default=10.0)

@@ -143,14 +143,13 @@ __device__ __forceinline__ int seg_argmax(double v, int r, double &vmax) {
 // ------------------------------------------------------------------------------------------
 template <int N, int L>
 __device__ __forceinline__ bool lu_rows(double2 (&a)[N + 1], int r, int seg, double2 *prow, uint8_t *pl,
-                                        double pivot_rel, double2 &y) {
+                                        double pivot_rel, double lane_max, double2 &y) {
   bool used = (r >= N);
   int mystep = used ? N : -1;
   double2 myinv = make_double2(0.0, 0.0);
-  double am = 0.0;
-#pragma unroll
-  for (int j = 0; j < N; ++j) am = fmax(am, abs2(a[j]));
-  am = seg_max<L>(am);
+  // lane_max: max |A_ij|^2 over the entries this lane holds or produced (NaN entries are ignored by
+  // fmax; they make the solve fail through the non-finite solution check)
+  const double am = seg_max<L>(lane_max);
   const double thr = pivot_rel * pivot_rel * am;
   bool sing = !(am < INFINITY);
   // pivot of step 0
@@ -213,14 +212,14 @@ __device__ __forceinline__ bool lu_rows(double2 (&a)[N + 1], int r, int seg, dou
 // relative residual of the rhs rows (reading R10).
 // ------------------------------------------------------------------------------------------
 template <int N, int L, bool ABS>
-__device__ __forceinline__ void run_ops(const uint2 *__restrict__ ops_s, int Q, int rhs_off,
+__device__ __forceinline__ double run_ops(const uint2 *__restrict__ ops_s, int Q, int rhs_off,
                                         const double2 *__restrict__ cval, const double2 *__restrict__ mono,
                                         double2 *__restrict__ M, double *__restrict__ rabs, const int16_t *row_of,
                                         int r) {
   // the complex product is split over two accumulators (c.x*m and -c.y*conj-swap(m)) so the
   // four DFMAs of an op depend only on the previous op's same-part accumulator (chain of 1)
   double2 acc = make_double2(0.0, 0.0), acc2 = make_double2(0.0, 0.0);
-  double acc_abs = 0.0;
+  double acc_abs = 0.0, jmax = 0.0;
 #pragma unroll(ABS ? 1 : 4)
   for (int q = 0; q < Q; ++q) {
     const uint2 op = ops_s[q * L + r];
@@ -234,13 +233,16 @@ __device__ __forceinline__ void run_ops(const uint2 *__restrict__ ops_s, int Q, 
     acc2.y = fma(c.y, m.x, acc2.y);
     if (fl & OP_LAST) {
       const uint32_t dest = op.y & 0xFFFFu;
-      M[dest] = make_double2(acc.x + acc2.x, acc.y + acc2.y);
+      const double2 e = make_double2(acc.x + acc2.x, acc.y + acc2.y);
+      M[dest] = e;
+      if (!(fl & OP_RHS)) jmax = fmax(jmax, abs2(e));   // for the singularity threshold (R9)
       if (ABS && (fl & OP_RHS)) rabs[row_of[dest]] = acc_abs;
       acc = make_double2(0.0, 0.0);
       acc2 = make_double2(0.0, 0.0);
       acc_abs = 0.0;
     }
   }
+  return jmax;
 }
 
 // ------------------------------------------------------------------------------------------
@@ -286,7 +288,8 @@ template <int N, int L>
 __device__ __forceinline__ bool eval_solve(const TrackArgs &A, const uint2 *__restrict__ ops_s,
                                            const uint32_t *__restrict__ prog_s, const int16_t *__restrict__ mpos_s,
                                            const int16_t *__restrict__ row_of, const double2 *__restrict__ ct,
-                                           double t, int rhs_off, bool want_abs, double2 *cval, double2 *mono,
+                                           double t, bool need_coef, int rhs_off, bool want_abs, double2 *cval,
+                                           double2 *mono,
                                            double2 *M, double2 *prow, double *rabs, uint8_t *pl, int r, int seg,
                                            double2 xr,
                                            double2 &y, double2 &fr, double &fabs_r) {
@@ -294,7 +297,7 @@ __device__ __forceinline__ bool eval_solve(const TrackArgs &A, const uint2 *__re
   // ---- stage x (monomial slots 0..N-1) and coefficient values c(t) (all slots), c'(t) (rhs
   //      slots) by Horner on the prologue's polynomials in t ----
   if (r < N) mono[r] = xr;
-  switch (D) {   // D is uniform: the common degrees keep all loads of a coefficient in flight together
+  if (need_coef) switch (D) {   // D is uniform: the common degrees keep all loads of a coefficient in flight together
     case 1: horner<1, L>(ct, t, ncoef, A.ncoef_src, cval, r); break;
     case 2: horner<2, L>(ct, t, ncoef, A.ncoef_src, cval, r); break;
     case 3: horner<3, L>(ct, t, ncoef, A.ncoef_src, cval, r); break;
@@ -324,8 +327,8 @@ __device__ __forceinline__ bool eval_solve(const TrackArgs &A, const uint2 *__re
     __syncwarp();
   }
   // ---- homogenised term evaluation, lane-balanced op list ----
-  if (want_abs) run_ops<N, L, true>(ops_s, A.Q, rhs_off, cval, mono, M, rabs, row_of, r);
-  else run_ops<N, L, false>(ops_s, A.Q, rhs_off, cval, mono, M, rabs, row_of, r);
+  const double jmax = want_abs ? run_ops<N, L, true>(ops_s, A.Q, rhs_off, cval, mono, M, rabs, row_of, r)
+                               : run_ops<N, L, false>(ops_s, A.Q, rhs_off, cval, mono, M, rabs, row_of, r);
   __syncwarp();
   // ---- load row r of [A | b] into registers (structural zeros read the always-zero entry) ----
   double2 a[N + 1];
@@ -338,7 +341,7 @@ __device__ __forceinline__ bool eval_solve(const TrackArgs &A, const uint2 *__re
   }
   fr = a[N];
   fabs_r = (r < N && want_abs) ? rabs[r] : 0.0;
-  return lu_rows<N, L>(a, r, seg, prow, pl, A.st.pivot_rel, y);
+  return lu_rows<N, L>(a, r, seg, prow, pl, A.st.pivot_rel, jmax, y);
 }
 
 // ------------------------------------------------------------------------------------------
@@ -393,6 +396,7 @@ __global__ void __launch_bounds__(TrackerShape<N>::MAXW * 32, TrackerShape<N>::M
   int stage = 0, it = 0, acc = 0, steps = 0, rej = 0, newt = 0, solves = 0;
   double2 x = make_double2(0.0, 0.0), kacc = x, kprev = x, xc = x;
   bool need_track = true;
+  double cval_t = -1.0;   // t at which the slot's coefficient values were last evaluated (-1: none)
 
   // begin a step attempt from (x, t) with dt; returns false when max_steps is exhausted
   auto begin_step = [&]() -> bool {
@@ -435,6 +439,7 @@ __global__ void __launch_bounds__(TrackerShape<N>::MAXW * 32, TrackerShape<N>::M
           g = (long long)got;
           const long long b = g / A.S, s = g % A.S;
           ct = A.coef_t + (size_t)b * (D + 1) * ncoef;
+          cval_t = -1.0;   // new instance: coefficient values are stale
           x = (r < N) ? A.start_x[s * N + r] : make_double2(0.0, 0.0);
           t = 0.0;
           dt = st.dt_init;
@@ -471,7 +476,12 @@ __global__ void __launch_bounds__(TrackerShape<N>::MAXW * 32, TrackerShape<N>::M
     const bool want_abs = __any_sync(FULL, state == ST_RESID);
     double2 yv, fr;
     double fa;
-    const bool ok = eval_solve<N, L>(A, ops_s, prog_s, mpos_s, row_of, ct, te, rhs_off, want_abs, cval, mono, M, prow, rabs,
+    // coefficient values depend only on (instance, t): RK stages 2/3 share t + h/2, and stage 4,
+    // the Newton iterations and the next step's stage 1 share t + h, so Horner is skipped then
+    const bool need_coef = (te != cval_t);
+    cval_t = te;
+    const bool ok = eval_solve<N, L>(A, ops_s, prog_s, mpos_s, row_of, ct, te, need_coef, rhs_off, want_abs, cval, mono,
+                                     M, prow, rabs,
                                      pl, r, seg, xe, yv, fr, fa);
 
     // ---- slot-uniform reductions, computed on all lanes before any slot-divergent branch ----
@@ -480,9 +490,13 @@ __global__ void __launch_bounds__(TrackerShape<N>::MAXW * 32, TrackerShape<N>::M
     const bool cand_fin = seg_all<L>(cfinite(cand), seg);
     const double d2 = seg_max<L>(abs2(yv));
     const double c2 = seg_max<L>(abs2(cand));
-    const double fm = (r < N) ? sqrt(abs2(fr)) : 0.0;
-    const double fq = (r < N) ? (fa > 0.0 ? fm / fa : (fm == 0.0 ? 0.0 : INFINITY)) : 0.0;
-    const double res_abs = seg_max<L>(fm), res_rel = seg_max<L>(fq);
+    double res_abs = 0.0, res_rel = 0.0;
+    if (want_abs) {   // warp-uniform: only when some slot classifies its endpoint
+      const double fm = (r < N) ? sqrt(abs2(fr)) : 0.0;
+      const double fq = (r < N) ? (fa > 0.0 ? fm / fa : (fm == 0.0 ? 0.0 : INFINITY)) : 0.0;
+      res_abs = seg_max<L>(fm);
+      res_rel = seg_max<L>(fq);
+    }
 
     // ---- advance the slot's state machine ----
     if (state == ST_DONE) continue;

@@ -30,7 +30,10 @@ __global__ void __launch_bounds__(128) batched_zgesv_kernel(const double2 *__res
     for (int j = 0; j < N; ++j) a[j] = (r < N) ? A[((size_t)kk * N + r) * N + j] : make_double2(0.0, 0.0);
     a[N] = (r < N) ? b[(size_t)kk * N + r] : make_double2(0.0, 0.0);
     double2 y;
-    const bool ok = lu_rows<N, L>(a, r, seg, prow, pl, pivot_rel, y);
+    double amax = 0.0;
+#pragma unroll
+    for (int j = 0; j < N; ++j) amax = fmax(amax, abs2(a[j]));
+    const bool ok = lu_rows<N, L>(a, r, seg, prow, pl, pivot_rel, amax, y);
     if (k < batch) {
       if (r < N) x[(size_t)k * N + r] = y;
       if (r == 0) info[k] = ok ? 0 : 1;

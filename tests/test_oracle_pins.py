@@ -312,3 +312,41 @@ def test_trifocal_planted_is_exact(orc):
             assert np.max(np.abs(orc.eval_F(d, p, y))) < 1e-12
     p0, x0 = rng.trifocal_complex_start()
     assert np.max(np.abs(orc.eval_F(d, p0, x0))) < 1e-12
+
+
+# ---------------------------------------------------------------- more Table 2 / §4 counts
+
+def _frozen(desc, p):
+    """F(x; p) with coefficients frozen at p (a constant-coefficient TD target)."""
+    import oracle
+    from hc_inputs.descriptor import SystemDesc
+    c = oracle.eval_coefs(desc, p)
+    return SystemDesc(desc.n_vars, 0, desc.term_eq, desc.term_xexp, desc.term_coef,
+                      np.arange(desc.n_coefs + 1, dtype=np.int32), c,
+                      np.zeros((desc.n_coefs, 0), np.int32)).contiguous()
+
+
+def test_three_view_triangulation_94(orc):
+    """Paper count: 3-view triangulation (9 unknowns) has 94 solutions (Table 2); TD at a
+    generic complex parameter point, 2^9 = 512 tracks."""
+    d = systems.nview_triangulation(3)
+    assert (d.n_vars, d.n_params) == (9, 33)
+    td = _frozen(d, rng.complex_normal(rng.gen(103), d.n_params))
+    res = orc.track(orc.td_homotopy(td, rng.gamma(0)), orc.td_start(td.degrees()))
+    U, mult = orc.dedup(orc.finite_solutions(res))
+    assert len(U) == 94 and mult.max() == 1
+
+
+def test_two_view_triangulation_six(orc):
+    """Paper: 2-view optimal triangulation reduces to a single 6th-order polynomial, i.e. 6
+    stationary points when E is an essential (rank-2) matrix; generic full-rank E gives 8."""
+    d = systems.nview_triangulation(2)
+    g = rng.gen(5)
+    gam = rng.complex_normal(g, 4)
+    E = rng.complex_normal(g, (3, 2)) @ rng.complex_normal(g, (2, 3))
+    td = _frozen(d, np.concatenate([gam, E.reshape(-1)]))
+    res = orc.track(orc.td_homotopy(td, rng.gamma(0)), orc.td_start(td.degrees()))
+    assert len(orc.dedup(orc.finite_solutions(res))[0]) == 6
+    td8 = _frozen(d, rng.complex_normal(rng.gen(102), d.n_params))
+    res8 = orc.track(orc.td_homotopy(td8, rng.gamma(0)), orc.td_start(td8.degrees()))
+    assert len(orc.dedup(orc.finite_solutions(res8))[0]) == 8
