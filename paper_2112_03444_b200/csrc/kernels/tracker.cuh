@@ -72,11 +72,21 @@ __device__ __forceinline__ double2 shfl2(double2 v, int src, int width) {
   return make_double2(__shfl_sync(FULL, v.x, src, width), __shfl_sync(FULL, v.y, src, width));
 }
 
+// Maximum over the L lanes of a segment of a value that is >= 0 or NaN.  L == 32: exact max by two
+// REDUX on the IEEE bit pattern (non-negative doubles order like their bits; a NaN lane yields a
+// NaN result, which every caller treats like a failure); L < 32: butterfly of fmax (NaN ignored).
 template <int L>
 __device__ __forceinline__ double seg_max(double v) {
+  if constexpr (L == 32) {
+    const unsigned long long bits = (unsigned long long)__double_as_longlong(v);
+    const unsigned mhi = __reduce_max_sync(FULL, (unsigned)(bits >> 32));
+    const unsigned mlo = __reduce_max_sync(FULL, ((unsigned)(bits >> 32) == mhi) ? (unsigned)bits : 0u);
+    return __longlong_as_double((long long)(((unsigned long long)mhi << 32) | mlo));
+  } else {
 #pragma unroll
-  for (int off = L / 2; off >= 1; off >>= 1) v = fmax(v, __shfl_xor_sync(FULL, v, off));
-  return v;
+    for (int off = L / 2; off >= 1; off >>= 1) v = fmax(v, __shfl_xor_sync(FULL, v, off));
+    return v;
+  }
 }
 template <int L>
 __host__ __device__ constexpr unsigned seg_mask() {
@@ -180,7 +190,7 @@ __device__ __forceinline__ bool lu_rows(double2 (&a)[N + 1], int r, int seg, dou
       const double2 l = used ? make_double2(0.0, 0.0) : lc;
       a[k + 1] = cfms(a[k + 1], l, u1);
       double v = used ? -1.0 : abs2(a[k + 1]);
-      if (!(v >= 0.0)) v = -1.0;
+      if (L < 32 && !(v >= 0.0)) v = -1.0;   // NaN is never a pivot (the REDUX path excludes it itself)
       spec = crecip(a[k + 1]);
       p = seg_argmax<L>(v, r, vmax);
       __syncwarp();   // the published row is visible
