@@ -222,3 +222,21 @@ def trifocal_complex_start(seed: int = SEED_TRIFOCAL_MONODROMY):
         x[base:base + 4] /= np.sqrt(qq)
     view1 = complex_normal(g, (4, 2))
     return trifocal_project(x, view1), x
+
+
+def fourview_complex_start(seed: int = 23, nv: int = 4):
+    """Planted generic complex (x0, p0) for 4-view monodromy: complex random x0 and image points,
+    E chosen as the min-norm complex solution of the (affine in E) system F(x0; gamma, E) = 0
+    plus a random complex component in its null space."""
+    g = gen(seed)
+    pairs = systems.nview_pairs(nv)
+    n = 2 * nv + len(pairs)
+    x0 = complex_normal(g, n)
+    gam = complex_normal(g, (nv, 2))
+    A, b = fourview_linear_in_E(x0, gam, nv)
+    E0, *_ = np.linalg.lstsq(A, -b, rcond=None)
+    # add a generic null-space component so p0 is not the minimum-norm (special) point
+    _, _, Vh = np.linalg.svd(A)
+    null = Vh[A.shape[0]:].conj().T
+    E = E0 + null @ complex_normal(g, null.shape[1])
+    return np.concatenate([gam.reshape(-1), E]).astype(np.complex128), x0

@@ -53,6 +53,23 @@ def gpu_set(orc, res, b=0):
     return orc.dedup(X[st == 0])[0]
 
 
+def assert_same_set_r21(orc, desc, p, A, B, what, tol=TOL):
+    """Matching rule R21: equal counts; every well-conditioned solution (cond_inf(J_F) <= 1e8 and
+    ||x||_inf <= 1e6) has a partner within tol relative per coordinate; ill-conditioned ones within
+    1e-5 (their endpoints are only determined to ~cond * eps)."""
+    assert len(A) == len(B), (what, len(A), len(B))
+
+    def near(P, Q):
+        return np.array([np.min(np.max(np.abs(Q - a) / np.maximum(1, np.abs(a)), axis=1)) for a in P])
+    for P, Q in ((A, B), (B, A)):
+        dist = near(P, Q)
+        for a, dd in zip(P, dist):
+            if dd <= tol:
+                continue
+            cond = np.linalg.cond(orc.eval_JF(desc, p, a), np.inf)
+            assert (cond > 1e8 or np.max(np.abs(a)) > 1e6) and dd <= 1e-5, (what, dd, cond)
+
+
 def assert_same_set(orc, A, B, what):
     ok, ua, ub = orc.match_sets(A, B, tol=TOL)
     assert ok, f"{what}: oracle {len(A)} vs gpu {len(B)} solutions, unmatched {ua}/{ub}"
@@ -378,3 +395,33 @@ def test_two_view_td_six(hc, orc):
     td = _frozen(d, np.concatenate([gam4, E.reshape(-1)]))
     res, _ = run_td(hc, td, rng.gamma(0))
     assert len(gpu_set(orc, res)) == 6
+
+
+# ------------------------------------------------------------------ monodromy on the GPU tracker
+
+def test_monodromy_fourview_296(hc, orc):
+    """GPU monodromy from a planted complex (x0, p0) reaches the paper's 296 4-view solutions
+    (Table 2); every one is a root (oracle residual) and distinct."""
+    from paper_2112_03444_b200.monodromy import monodromy_solve
+    d = systems.nview_triangulation(4)
+    p0, x0 = rng.fourview_complex_start()
+    s = hc.System(d, device=0)
+    res = monodromy_solve(s, x0, p0, seed=1, stall_loops=5)
+    assert res.solutions.shape[0] == 296, res.history
+    for y in res.solutions[::7]:
+        assert np.max(np.abs(orc.eval_F(d, p0, y))) < 1e-9 * max(1, np.max(np.abs(y))) ** 2
+    assert orc.dedup(res.solutions)[0].shape[0] == 296
+
+
+def test_monodromy_trifocal_matches_oracle_fixture(hc, orc):
+    """GPU monodromy (with the Z2^3 symmetry) from the fixture's planted (x0, p0) reproduces the
+    oracle's monodromy set exactly (666 orbits = 5328 solutions), as a set within 1e-8."""
+    from paper_2112_03444_b200.monodromy import monodromy_solve
+    d = systems.trifocal_unknown_f()
+    p0, x0 = rng.trifocal_complex_start()
+    fix, fp0 = fixtures.trifocal_start()
+    assert np.array_equal(fp0, p0)
+    s = hc.System(d, device=0)
+    res = monodromy_solve(s, x0, p0, symmetry=systems.trifocal_symmetry, seed=3, stall_loops=4)
+    assert res.solutions.shape[0] == fix.shape[0], res.history
+    assert_same_set_r21(orc, d, p0, fix, res.solutions, "trifocal monodromy")
