@@ -141,6 +141,73 @@ static hc_status validate(const hc_system_desc &d, std::string &err) {
   return HC_OK;
 }
 
+
+// ------------------------------------------------------------------------------------------
+// Shared-memory bank relabelling.  The op loop reads coef[slot] and mono[k] with LDS.128: a warp
+// request is served in phases of 8 lanes, and two lanes of a phase that read different 16-byte
+// entries with the same index mod 8 conflict.  Slot and monomial ids are free up to permutations
+// within groups (rhs slots / other slots; monomials of one degree level), so a greedy swap search
+// (deterministic seed) minimises sum over (step, phase) of the worst bank multiplicity.
+// Returns perm: old label -> new label.
+// ------------------------------------------------------------------------------------------
+static std::vector<int> bank_relabel(const std::vector<int> &lab, int Q, int L, int nlabels,
+                                     const std::vector<std::vector<int>> &groups, uint64_t seed, int iters) {
+  const int W = std::min(8, L), P = std::max(1, L / 8), C = Q * P;
+  std::vector<int> perm(nlabels);
+  std::iota(perm.begin(), perm.end(), 0);
+  std::vector<std::vector<int>> cell_labels(C), lab_cells(nlabels);
+  for (int q = 0; q < Q; ++q)
+    for (int p = 0; p < P; ++p) {
+      std::vector<int> v;
+      for (int l = p * W; l < p * W + W && l < L; ++l) v.push_back(lab[(size_t)q * L + l]);
+      std::sort(v.begin(), v.end());
+      v.erase(std::unique(v.begin(), v.end()), v.end());
+      const int c = q * P + p;
+      cell_labels[c] = v;
+      for (int x : v) lab_cells[x].push_back(c);
+    }
+  auto cell_cost = [&](int c) {
+    int b[8] = {0, 0, 0, 0, 0, 0, 0, 0}, m = 0;
+    for (int x : cell_labels[c]) m = std::max(m, ++b[perm[x] & 7]);
+    return m;
+  };
+  std::vector<int> cost(C);
+  for (int c = 0; c < C; ++c) cost[c] = cell_cost(c);
+  std::vector<const std::vector<int> *> gl;
+  for (const auto &g : groups)
+    if (g.size() > 1) gl.push_back(&g);
+  if (gl.empty()) return perm;
+  uint64_t st = seed * 0x9E3779B97F4A7C15ull + 1;
+  auto rnd = [&]() {
+    st ^= st << 13;
+    st ^= st >> 7;
+    st ^= st << 17;
+    return st;
+  };
+  std::vector<int> stamp(C, -1), cells;
+  for (int it = 0; it < iters; ++it) {
+    const std::vector<int> &g = *gl[rnd() % gl.size()];
+    const int a = g[rnd() % g.size()], b = g[rnd() % g.size()];
+    if (a == b) continue;
+    cells.clear();
+    for (int c : lab_cells[a])
+      if (stamp[c] != it) stamp[c] = it, cells.push_back(c);
+    for (int c : lab_cells[b])
+      if (stamp[c] != it) stamp[c] = it, cells.push_back(c);
+    int old = 0, nw = 0;
+    for (int c : cells) old += cost[c];
+    std::swap(perm[a], perm[b]);
+    std::vector<int> nc(cells.size());
+    for (size_t i = 0; i < cells.size(); ++i) nw += (nc[i] = cell_cost(cells[i]));
+    if (nw <= old) {
+      for (size_t i = 0; i < cells.size(); ++i) cost[cells[i]] = nc[i];
+    } else {
+      std::swap(perm[a], perm[b]);
+    }
+  }
+  return perm;
+}
+
 hc_status compile_system(const hc_system_desc &d, CompiledSystem &cs, std::string &err) {
   hc_status s = validate(d, err);
   if (s != HC_OK) return s;
@@ -351,6 +418,60 @@ hc_status compile_system(const hc_system_desc &d, CompiledSystem &cs, std::strin
       }
     // padding ops after the lane's last entry: slot 0 times the constant monomial, never stored
     for (; q < Q; ++q) cs.ops[(size_t)q * L + l] = uint2{(uint32_t)N << 16, OP_NO_DEST};
+  }
+
+  // ---- bank relabelling of coefficient slots and monomials (see bank_relabel) ----
+  {
+    const int nsrc = d.n_coefs;
+    std::vector<int> sl((size_t)Q * L), mo((size_t)Q * L);
+    for (size_t i = 0; i < cs.ops.size(); ++i) {
+      sl[i] = (int)(cs.ops[i].x & 0xFFFFu);
+      mo[i] = (int)(cs.ops[i].x >> 16);
+    }
+    std::vector<std::vector<int>> sg(2);
+    for (int j = 0; j < cs.ncoef; ++j) sg[j < nsrc ? 0 : 1].push_back(j);
+    const std::vector<int> ps = bank_relabel(sl, Q, L, cs.ncoef, sg, 2112, 40000);
+    std::vector<std::vector<int>> mg(std::max(0, maxdeg - 1));
+    for (int k = N + 1, lvl = 0; k < cs.n_mono; ++k) {
+      while (k >= cs.level_end[lvl]) ++lvl;
+      mg[lvl].push_back(k);
+    }
+    const std::vector<int> pm = bank_relabel(mo, Q, L, cs.n_mono, mg, 3444, 40000);
+    for (auto &w : cs.ops) w.x = (uint32_t)ps[w.x & 0xFFFFu] | ((uint32_t)pm[w.x >> 16] << 16);
+    // monomial program in the new numbering (permutations stay within a degree level)
+    std::vector<uint32_t> prog(cs.mono_prog.size());
+    for (int k = N + 1; k < cs.n_mono; ++k) {
+      const uint32_t e = cs.mono_prog[k - N - 1];
+      const int parent = (int)(e & 0xFFFFu), var = (int)(e >> 16);
+      prog[pm[k] - N - 1] = (uint32_t)pm[parent] | ((uint32_t)var << 16);
+    }
+    cs.mono_prog = prog;
+    // coefficient slots in the new numbering; pad the slot count to a multiple of 8 so that the
+    // c'(t) copy (slot + ncoef) falls in the same bank group as c(t)
+    const int ncoef_pad = (cs.ncoef + 7) & ~7;
+    std::vector<int32_t> smap(2 * ncoef_pad, 0);
+    std::vector<std::vector<CoefMono>> per(ncoef_pad);
+    for (int j = 0; j < cs.ncoef; ++j) {
+      smap[2 * ps[j]] = cs.slot_map[2 * j];
+      smap[2 * ps[j] + 1] = cs.slot_map[2 * j + 1];
+      for (int m = cs.mono_ptr[j]; m < cs.mono_ptr[j + 1]; ++m) {
+        CoefMono c = cs.mono[m];
+        c.coef = ps[j];
+        per[ps[j]].push_back(c);
+      }
+    }
+    for (int j = cs.ncoef; j < ncoef_pad; ++j) {   // padding slots: zero coefficient, weight-0 monomial
+      smap[2 * j] = 0;
+      smap[2 * j + 1] = 0;
+    }
+    cs.mono.clear();
+    cs.mono_ptr.assign(ncoef_pad + 1, 0);
+    for (int j = 0; j < ncoef_pad; ++j) {
+      for (const CoefMono &c : per[j]) cs.mono.push_back(c);
+      cs.mono_ptr[j + 1] = (int32_t)cs.mono.size();
+    }
+    cs.slot_map = smap;
+    cs.ncoef = ncoef_pad;
   }
   return HC_OK;
 }
