@@ -473,6 +473,27 @@ hc_status compile_system(const hc_system_desc &d, CompiledSystem &cs, std::strin
     cs.slot_map = smap;
     cs.ncoef = ncoef_pad;
   }
+  // ---- bank relabelling of the compact entries for the row loads (lane r reads row r's column
+  //      j at step j; structural zeros all read the single zero entry, a broadcast) ----
+  {
+    const int NE = cs.n_entries;
+    const int Lr = lanes_for(N);
+    std::vector<int> lab((size_t)(N + 1) * Lr, NE);
+    for (int j = 0; j <= N; ++j)
+      for (int r = 0; r < Lr && r < N; ++r) {
+        const int e = cs.mpos[(size_t)r * (N + 1) + j];
+        lab[(size_t)j * Lr + r] = e < 0 ? NE : e;
+      }
+    std::vector<std::vector<int>> eg(1);
+    for (int e = 0; e < NE; ++e) eg[0].push_back(e);
+    const std::vector<int> pe = bank_relabel(lab, N + 1, Lr, NE + 1, eg, 2021, 20000);
+    for (auto &v : cs.mpos)
+      if (v >= 0) v = (int16_t)pe[v];
+    for (auto &w : cs.ops) {
+      const uint32_t dest = w.y & 0xFFFFu;
+      if (dest != OP_NO_DEST) w.y = (w.y & 0xFFFF0000u) | (uint32_t)pe[dest];
+    }
+  }
   return HC_OK;
 }
 
