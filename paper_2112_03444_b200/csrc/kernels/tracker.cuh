@@ -136,18 +136,19 @@ __device__ __forceinline__ int seg_argmax(double v, int r, double &vmax) {
 }
 
 // ------------------------------------------------------------------------------------------
-// Fused LU with partial pivoting + back-substitution on [A | b] held one row per lane
-// (a[0..N-1] = row r of A, a[N] = b_r) (one kernel, augmented matrix, back-substitution
-// on the cached U).  Pivot = max |a|^2 over the not-yet-pivoted rows (ties -> lowest row, reading
-// R13); singular when |pivot| <= pivot_rel * max|A_ij| (R9) or anything is non-finite.
+// Fused elimination with partial pivoting on [A | b] held one row per lane (a[0..N-1] = row r of
+// A, a[N] = b_r) (one kernel, the augmented matrix carries the triangular solve with L).
+// The paper back-substitutes on the cached U; here the rows already pivoted also eliminate the
+// current column (Gauss-Jordan), which costs nothing extra in the one-row-per-lane SIMT layout and
+// replaces the N-step sequential back-substitution by one division per row.
+// Pivot = max |a|^2 over the not-yet-pivoted rows (ties -> lowest row, reading R13); singular when
+// |pivot| <= pivot_rel * max|A_ij| (R9) or anything is non-finite.
 // Latency schedule (one warp owns the whole factorisation, so the per-column dependency chain is
 // the cost): every lane computes 1/a_rk of its candidate speculatively; once the arg-max names the
 // pivot lane, 1/pivot and the pivot row's column k+1 are shuffled from it while the rest of its row
 // goes through a double-buffered shared row (one __syncwarp per column); every other row updates
 // column k+1 first, and the arg-max for step k+1 starts on it while the remaining columns are
-// updated.  The pivot order is recorded so
-// back-substitution, which runs on the U rows still held by their lanes, never searches for the
-// source lane; solution components are collected through shared memory.
+// updated.  Solution components are collected through shared memory.
 // Returns the solution component y_r in lane r and a slot-uniform success flag.
 // prow: 2 * (N + 1) double2; pl: N bytes (per slot shared memory).
 // ------------------------------------------------------------------------------------------
@@ -175,20 +176,21 @@ __device__ __forceinline__ bool lu_rows(double2 (&a)[N + 1], int r, int seg, dou
     // early broadcast from the pivot lane by shuffles: 1/pivot and the pivot row's column k+1
     const double2 inv = shfl2(spec, p, L);
     const double2 u1 = shfl2(a[k + 1], p, L);
-    if (r == p) {   // the pivot lane publishes the rest of its row (columns k+2..N) through shared memory
+    const bool me = (r == p);
+    if (me) {   // the pivot lane publishes the rest of its row (columns k+2..N) through shared memory
 #pragma unroll
       for (int j = k + 2; j <= N; ++j) pr[j] = a[j];
-      pl[k] = (uint8_t)r;
       used = true;
       mystep = k;
       myinv = spec;
     }
+    // Gauss-Jordan: every row except the pivot row eliminates column k -- the rows pivoted earlier
+    // too, which in this one-row-per-lane layout costs no extra instruction (the whole warp runs
+    // the update anyway) and removes the sequential back-substitution.  Padding rows are zero.
+    const double2 lc = cmul(a[k], inv);
+    const double2 l = me ? make_double2(0.0, 0.0) : lc;
+    a[k + 1] = cfms(a[k + 1], l, u1);   // column k+1 first (k + 1 == N: the right-hand side)
     if (k + 1 < N) {
-      // multiplier; rows already pivoted (and padding lanes) use l = 0, which leaves them unchanged
-      // (a - 0 * u = a for finite u; a non-finite u fails the solve anyway) without a branch
-      const double2 lc = cmul(a[k], inv);
-      const double2 l = used ? make_double2(0.0, 0.0) : lc;
-      a[k + 1] = cfms(a[k + 1], l, u1);
       double v = used ? -1.0 : abs2(a[k + 1]);
       if (L < 32 && !(v >= 0.0)) v = -1.0;   // NaN is never a pivot (the REDUX path excludes it itself)
       spec = crecip(a[k + 1]);
@@ -200,16 +202,9 @@ __device__ __forceinline__ bool lu_rows(double2 (&a)[N + 1], int r, int seg, dou
     }
   }
   __syncwarp();
-  // ---- back-substitution on the cached U: lane pl[k] holds U row k (a[k..N]) and 1/U_kk ----
-  double2 *xsol = prow + 2 * (N + 1) - N;   // second pivot-row buffer: free after the elimination
-#pragma unroll
-  for (int k = N - 1; k >= 0; --k) {
-    const int src = pl[k];
-    const double2 xk = shfl2(cmul(a[N], myinv), src, L);
-    const double2 u = (mystep < k) ? a[k] : make_double2(0.0, 0.0);   // U_{mystep,k}, or 0
-    a[N] = cfms(a[N], u, xk);
-    if (r == 0) xsol[k] = xk;
-  }
+  // ---- the system is now diagonal in pivot order: x_{mystep} = b' / pivot, routed through shared memory ----
+  double2 *xsol = prow;
+  if (mystep < N) xsol[mystep] = cmul(a[N], myinv);
   __syncwarp();
   const double2 sol = (r < N) ? xsol[r] : make_double2(0.0, 0.0);
   y = sol;
