@@ -191,13 +191,23 @@ __device__ __forceinline__ bool lu_rows(double2 (&a)[N + 1], int r, int seg, dou
     const double2 l = me ? make_double2(0.0, 0.0) : lc;
     a[k + 1] = cfms(a[k + 1], l, u1);   // column k+1 first (k + 1 == N: the right-hand side)
     if (k + 1 < N) {
-      double v = used ? -1.0 : abs2(a[k + 1]);
-      if (L < 32 && !(v >= 0.0)) v = -1.0;   // NaN is never a pivot (the REDUX path excludes it itself)
+      double v = abs2(a[k + 1]);
+      if (used || (L < 32 && !(v >= 0.0))) v = -1.0;   // NaN is never a pivot (the REDUX path excludes it itself)
       spec = crecip(a[k + 1]);
       p = seg_argmax<L>(v, r, vmax);
       __syncwarp();   // the published row is visible
+      // trailing update in chunks of 4 columns: the 4 shared loads are issued before their FMAs so
+      // the load latency overlaps (the compiler otherwise keeps only ~2 loads in flight)
 #pragma unroll
-      for (int j = k + 2; j <= N; ++j) a[j] = cfms(a[j], l, pr[j]);
+      for (int j0 = k + 2; j0 <= N; j0 += 4) {
+        double2 u[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+          if (j0 + i <= N) u[i] = pr[j0 + i];
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+          if (j0 + i <= N) a[j0 + i] = cfms(a[j0 + i], l, u[i]);
+      }
       sing |= !(vmax > thr);
     }
   }
@@ -217,14 +227,14 @@ __device__ __forceinline__ bool lu_rows(double2 (&a)[N + 1], int r, int seg, dou
 // relative residual of the rhs rows (reading R10).
 // ------------------------------------------------------------------------------------------
 template <int N, int L, bool ABS>
-__device__ __forceinline__ double run_ops(const uint2 *__restrict__ ops_s, int Q, int rhs_off,
+__device__ __forceinline__ void run_ops(const uint2 *__restrict__ ops_s, int Q, int rhs_off,
                                         const double2 *__restrict__ cval, const double2 *__restrict__ mono,
                                         double2 *__restrict__ M, double *__restrict__ rabs, const int16_t *row_of,
                                         int r) {
   // the complex product is split over two accumulators (c.x*m and -c.y*conj-swap(m)) so the
   // four DFMAs of an op depend only on the previous op's same-part accumulator (chain of 1)
   double2 acc = make_double2(0.0, 0.0), acc2 = make_double2(0.0, 0.0);
-  double acc_abs = 0.0, jmax = 0.0;
+  double acc_abs = 0.0;
 #pragma unroll(ABS ? 1 : 4)
   for (int q = 0; q < Q; ++q) {
     const uint2 op = ops_s[q * L + r];
@@ -238,16 +248,13 @@ __device__ __forceinline__ double run_ops(const uint2 *__restrict__ ops_s, int Q
     acc2.y = fma(c.y, m.x, acc2.y);
     if (fl & OP_LAST) {
       const uint32_t dest = op.y & 0xFFFFu;
-      const double2 e = make_double2(acc.x + acc2.x, acc.y + acc2.y);
-      M[dest] = e;
-      if (!(fl & OP_RHS)) jmax = fmax(jmax, abs2(e));   // for the singularity threshold (R9)
+      M[dest] = make_double2(acc.x + acc2.x, acc.y + acc2.y);
       if (ABS && (fl & OP_RHS)) rabs[row_of[dest]] = acc_abs;
       acc = make_double2(0.0, 0.0);
       acc2 = make_double2(0.0, 0.0);
       acc_abs = 0.0;
     }
   }
-  return jmax;
 }
 
 // ------------------------------------------------------------------------------------------
@@ -332,15 +339,20 @@ __device__ __forceinline__ bool eval_solve(const TrackArgs &A, const uint2 *__re
     __syncwarp();
   }
   // ---- homogenised term evaluation, lane-balanced op list ----
-  const double jmax = want_abs ? run_ops<N, L, true>(ops_s, A.Q, rhs_off, cval, mono, M, rabs, row_of, r)
-                               : run_ops<N, L, false>(ops_s, A.Q, rhs_off, cval, mono, M, rabs, row_of, r);
+  if (want_abs) run_ops<N, L, true>(ops_s, A.Q, rhs_off, cval, mono, M, rabs, row_of, r);
+  else run_ops<N, L, false>(ops_s, A.Q, rhs_off, cval, mono, M, rabs, row_of, r);
   __syncwarp();
   // ---- load row r of [A | b] into registers (structural zeros read the always-zero entry) ----
   double2 a[N + 1];
   const int rr = (r < N) ? r : 0;
+  double jmax = 0.0;   // max |A_rj|^2 of this row, for the singularity threshold (R9)
 #pragma unroll
-  for (int j = 0; j <= N; ++j) a[j] = M[mpos_s[rr * (N + 1) + j]];
+  for (int j = 0; j <= N; ++j) {
+    a[j] = M[mpos_s[rr * (N + 1) + j]];
+    if (j < N) jmax = fmax(jmax, abs2(a[j]));
+  }
   if (r >= N) {
+    jmax = 0.0;
 #pragma unroll
     for (int j = 0; j <= N; ++j) a[j] = make_double2(0.0, 0.0);
   }
