@@ -36,7 +36,7 @@ constexpr unsigned FULL = 0xffffffffu;
 //   N > 20: 4 warps x 2 CTAs.  The launcher shrinks the CTA when the shared memory does not fit.
 template <int N>
 struct TrackerShape {
-  static constexpr int MAXW = (N >= 15 && N <= 20) ? 16 : 4;
+  static constexpr int MAXW = (N >= 15 && N <= 20) ? 12 : 4;
   static constexpr int MINB = (N <= 14) ? 4 : (N <= 20) ? 1 : 2;
 };
 
