@@ -31,9 +31,9 @@ namespace hcb {
 
 constexpr unsigned FULL = 0xffffffffu;
 // Warps per CTA and minimum resident CTAs per SM, by N (register budget 65536 / (32 * warps * ctas)):
-//   N <= 14: 4 warps x 4 CTAs (128 regs);  15..20: one 16-warp CTA per SM (128 regs; the trifocal
-//   slot needs ~13.5 KB of shared memory, so 16 slots + one copy of the tables just fit 227 KB);
-//   N > 20: 4 warps x 2 CTAs.  The launcher shrinks the CTA when the shared memory does not fit.
+//   N <= 14: 4 warps x 4 CTAs (128 regs);  15..20: one 12-warp CTA per SM (168 regs; measured on the
+//   trifocal system: 12 warps at 168 regs beat 16 at 128 (spills) and 8 at 218);  N > 20: 4 warps x
+//   2 CTAs.  The launcher shrinks the CTA when the shared memory does not fit.
 template <int N>
 struct TrackerShape {
   static constexpr int MAXW = (N >= 15 && N <= 20) ? 12 : 4;
