@@ -217,6 +217,11 @@ hc_status hc_batched_zgesv(int32_t n, int64_t batch, const hc_complex *A, const 
  * independent DFMA chains on every SM of `device`; *tflops receives the achieved FLOP/s / 1e12. */
 hc_status hc_fp64_peak_probe(int device, double *tflops);
 
+/* Experiment hook: per-phase cycle sums of the tracker kernel (coefficients, monomials, ops, row
+ * load, elimination, state machine, eval+solve, iterations) -- only in libraries built with
+ * -DHCB_PHASE_TIMING (HCB_VARIANT=timing); HC_E_INVALID_ARG otherwise. out8: host [8]. */
+hc_status hc_debug_phase_cycles(hc_result res, unsigned long long *out8);
+
 /* Thread-local message of the last failing call (never NULL). */
 const char *hc_last_error(void);
 /* Library version string. */

@@ -9,7 +9,7 @@ import ctypes as C
 import os
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "lib", "libhc.so")
+LIB_PATH = os.environ.get("HC_LIB_PATH") or os.path.join(_PKG, "lib", "libhc.so")
 
 HC_OK, HC_E_INVALID_ARG, HC_E_TOO_LARGE, HC_E_CUDA, HC_E_OOM, HC_E_INTERNAL = range(6)
 HC_CONVERGED, HC_DIVERGED, HC_STEP_UNDERFLOW, HC_MAX_STEPS, HC_SINGULAR, HC_NONFINITE = range(6)
@@ -22,7 +22,7 @@ EXPORTED = [
     "hc_total_degree_start", "hc_system_info_get", "hc_system_destroy", "hc_system_compile_info",
     "hc_system_compile_tables", "hc_tracker_settings_default", "hc_track_batch", "hc_result_wait",
     "hc_result_elapsed_ms", "hc_result_launch", "hc_result_get", "hc_result_destroy", "hc_batched_zgesv", "hc_fp64_peak_probe",
-    "hc_last_error", "hc_version",
+    "hc_last_error", "hc_version", "hc_debug_phase_cycles",
 ]
 
 
@@ -111,6 +111,7 @@ def lib() -> C.CDLL:
     L.hc_batched_zgesv.argtypes = [C.c_int32, C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
                                    C.c_double, C.c_void_p]
     L.hc_fp64_peak_probe.argtypes = [C.c_int, P(C.c_double)]
+    L.hc_debug_phase_cycles.argtypes = [C.c_void_p, C.c_void_p]
     L.hc_last_error.restype = C.c_char_p
     L.hc_version.restype = C.c_char_p
     for name in EXPORTED:

@@ -17,12 +17,17 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 INCLUDE = os.path.join(ROOT, "include")
-BUILD = os.path.join(PKG, "build")
-LIBDIR = os.path.join(PKG, "lib")
+# HCB_VARIANT=timing builds an experiment library with per-phase cycle counters (-DHCB_PHASE_TIMING)
+# into lib_timing/ (load it with HC_LIB_PATH); the product library is the default variant.
+VARIANT = os.environ.get("HCB_VARIANT", "")
+BUILD = os.path.join(PKG, "build" + ("_" + VARIANT if VARIANT else ""))
+LIBDIR = os.path.join(PKG, "lib" + ("_" + VARIANT if VARIANT else ""))
 LIB = os.path.join(LIBDIR, "libhc.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-I" + INCLUDE, "-I" + CSRC]
+if VARIANT == "timing":
+    FLAGS = FLAGS + ["-DHCB_PHASE_TIMING"]
 
 
 def sources():

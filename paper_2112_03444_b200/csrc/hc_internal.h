@@ -70,6 +70,7 @@ struct TrackArgs {
   int32_t *counters_out;     // [total][4]
   double *resid_out;         // [total][2]
   DevSettings st;
+  unsigned long long *phase_cycles;  // [8] per-phase clock sums (only in HCB_PHASE_TIMING builds), or null
 };
 
 struct PrologueArgs {

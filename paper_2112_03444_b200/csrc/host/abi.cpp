@@ -97,6 +97,7 @@ struct hc_result_s {
   bool outputs_on_host = false;
   bool waited = false;
   TrackerPlan plan{};
+  unsigned long long *phase_cycles = nullptr;
 };
 
 static void destroy_result(hc_result r) {
@@ -489,6 +490,16 @@ hc_status hc_track_batch(hc_system sys, const hc_tracker_settings *settings, con
   ta.st.max_newton = st.max_newton;
   ta.st.max_steps = st.max_steps;
   ta.st.end_newton = st.end_newton;
+  ta.phase_cycles = nullptr;
+#ifdef HCB_PHASE_TIMING
+  {
+    unsigned long long *pc = nullptr;
+    if ((s = dev_alloc(r, &pc, 8)) != HC_OK) return bail(s);
+    cudaMemsetAsync(pc, 0, 64, r->stream);
+    ta.phase_cycles = pc;
+    r->phase_cycles = pc;
+  }
+#endif
   e = tracker_launcher(N)(ta, sys->device, r->stream, &r->plan);
   if (e != cudaSuccess) return bail(cuda_fail(e, "tracker launch"));
   cudaEventRecord(r->ev[2], r->stream);
@@ -551,6 +562,16 @@ hc_status hc_result_launch(hc_result r, int32_t *lanes, int32_t *warps_per_cta, 
   if (warps_per_cta) *warps_per_cta = r->plan.warps_per_cta;
   if (ctas) *ctas = r->plan.ctas;
   if (smem_bytes) *smem_bytes = (int64_t)r->plan.smem_bytes;
+  return HC_OK;
+}
+
+// Experiment builds (-DHCB_PHASE_TIMING) only: per-phase cycle sums of the tracker kernel.
+hc_status hc_debug_phase_cycles(hc_result r, unsigned long long *out8) {
+  if (!r || !out8) return fail(HC_E_INVALID_ARG, "null");
+  if (!r->phase_cycles) return fail(HC_E_INVALID_ARG, "not a phase-timing build");
+  hc_status s = hc_result_wait(r);
+  if (s != HC_OK) return s;
+  CK(cudaMemcpy(out8, r->phase_cycles, 64, cudaMemcpyDeviceToHost));
   return HC_OK;
 }
 

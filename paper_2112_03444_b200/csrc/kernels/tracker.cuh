@@ -30,6 +30,15 @@
 namespace hcb {
 
 constexpr unsigned FULL = 0xffffffffu;
+
+// Optional per-phase cycle accounting (experiments only: -DHCB_PHASE_TIMING).
+#ifdef HCB_PHASE_TIMING
+#define HCB_T(var) const long long var = clock64()
+#define HCB_ACC(i, a, b) (hcb_phase[i] += (unsigned long long)((b) - (a)))
+#else
+#define HCB_T(var)
+#define HCB_ACC(i, a, b)
+#endif
 // Warps per CTA and minimum resident CTAs per SM, by N (register budget 65536 / (32 * warps * ctas)):
 //   N <= 14: 4 warps x 4 CTAs (128 regs);  15..20: one 12-warp CTA per SM (168 regs; measured on the
 //   trifocal system: 12 warps at 168 regs beat 16 at 128 (spills) and 8 at 218);  N > 20: 4 warps x
@@ -226,34 +235,58 @@ __device__ __forceinline__ bool lu_rows(double2 (&a)[N + 1], int r, int seg, dou
 // products shared through the monomial program).  ABS also accumulates sum |c m| for the
 // relative residual of the rhs rows (reading R10).
 // ------------------------------------------------------------------------------------------
+// One op: accumulate c*m; at the entry's last op store the entry and reset.  The complex product is
+// split over two accumulators (c.x*m and the c.y part) so the four DFMAs of an op depend only on
+// the previous op's same-part accumulator (chain of 1).
+template <int N, bool ABS>
+__device__ __forceinline__ void op_accumulate(uint2 op, double2 c, double2 m, double2 &acc, double2 &acc2,
+                                              double &acc_abs, double2 *__restrict__ M, double *__restrict__ rabs,
+                                              const int16_t *row_of) {
+  const uint32_t fl = op.y >> 16;
+  if (ABS) acc_abs += sqrt(abs2(cmul(c, m)));
+  acc.x = fma(c.x, m.x, acc.x);
+  acc.y = fma(c.x, m.y, acc.y);
+  acc2.x = fma(-c.y, m.y, acc2.x);
+  acc2.y = fma(c.y, m.x, acc2.y);
+  if (fl & OP_LAST) {
+    const uint32_t dest = op.y & 0xFFFFu;
+    M[dest] = make_double2(acc.x + acc2.x, acc.y + acc2.y);
+    if (ABS && (fl & OP_RHS)) rabs[row_of[dest]] = acc_abs;
+    acc = make_double2(0.0, 0.0);
+    acc2 = make_double2(0.0, 0.0);
+    acc_abs = 0.0;
+  }
+}
+
+// Op list: M[dest] = sum over the entry's ops of coef[slot] * mono[k].  Ops are processed in blocks
+// of 4 whose op records and operands are all loaded before any store of the block (the stores into
+// M would otherwise serialise every op behind the previous op's store: the compiler cannot prove
+// that M does not alias the op table, both being shared memory).
 template <int N, int L, bool ABS>
 __device__ __forceinline__ void run_ops(const uint2 *__restrict__ ops_s, int Q, int rhs_off,
                                         const double2 *__restrict__ cval, const double2 *__restrict__ mono,
                                         double2 *__restrict__ M, double *__restrict__ rabs, const int16_t *row_of,
                                         int r) {
-  // the complex product is split over two accumulators (c.x*m and -c.y*conj-swap(m)) so the
-  // four DFMAs of an op depend only on the previous op's same-part accumulator (chain of 1)
   double2 acc = make_double2(0.0, 0.0), acc2 = make_double2(0.0, 0.0);
   double acc_abs = 0.0;
-#pragma unroll(ABS ? 1 : 4)
-  for (int q = 0; q < Q; ++q) {
-    const uint2 op = ops_s[q * L + r];
-    const uint32_t fl = op.y >> 16;
-    const double2 c = cval[(int)(op.x & 0xFFFFu) + ((fl & OP_RHS) ? rhs_off : 0)];
-    const double2 m = mono[op.x >> 16];
-    if (ABS) acc_abs += sqrt(abs2(cmul(c, m)));
-    acc.x = fma(c.x, m.x, acc.x);
-    acc.y = fma(c.x, m.y, acc.y);
-    acc2.x = fma(-c.y, m.y, acc2.x);
-    acc2.y = fma(c.y, m.x, acc2.y);
-    if (fl & OP_LAST) {
-      const uint32_t dest = op.y & 0xFFFFu;
-      M[dest] = make_double2(acc.x + acc2.x, acc.y + acc2.y);
-      if (ABS && (fl & OP_RHS)) rabs[row_of[dest]] = acc_abs;
-      acc = make_double2(0.0, 0.0);
-      acc2 = make_double2(0.0, 0.0);
-      acc_abs = 0.0;
+  int q = 0;
+  for (; q + 4 <= Q; q += 4) {
+    uint2 op[4];
+    double2 c[4], m[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) op[i] = ops_s[(q + i) * L + r];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      c[i] = cval[(int)(op[i].x & 0xFFFFu) + (((op[i].y >> 16) & OP_RHS) ? rhs_off : 0)];
+      m[i] = mono[op[i].x >> 16];
     }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) op_accumulate<N, ABS>(op[i], c[i], m[i], acc, acc2, acc_abs, M, rabs, row_of);
+  }
+  for (; q < Q; ++q) {
+    const uint2 o = ops_s[q * L + r];
+    const double2 c = cval[(int)(o.x & 0xFFFFu) + (((o.y >> 16) & OP_RHS) ? rhs_off : 0)];
+    op_accumulate<N, ABS>(o, c, mono[o.x >> 16], acc, acc2, acc_abs, M, rabs, row_of);
   }
 }
 
@@ -304,10 +337,15 @@ __device__ __forceinline__ bool eval_solve(const TrackArgs &A, const uint2 *__re
                                            double2 *mono,
                                            double2 *M, double2 *prow, double *rabs, uint8_t *pl, int r, int seg,
                                            double2 xr,
-                                           double2 &y, double2 &fr, double &fabs_r) {
+                                           double2 &y, double2 &fr, double &fabs_r
+#ifdef HCB_PHASE_TIMING
+                                           , unsigned long long (&hcb_phase)[8]
+#endif
+                                           ) {
   const int ncoef = A.ncoef, D = A.D;
   // ---- stage x (monomial slots 0..N-1) and coefficient values c(t) (all slots), c'(t) (rhs
   //      slots) by Horner on the prologue's polynomials in t ----
+  HCB_T(c0);
   if (r < N) mono[r] = xr;
   if (need_coef) switch (D) {   // D is uniform: the common degrees keep all loads of a coefficient in flight together
     case 1: horner<1, L>(ct, t, ncoef, A.ncoef_src, cval, r); break;
@@ -327,6 +365,8 @@ __device__ __forceinline__ bool eval_solve(const TrackArgs &A, const uint2 *__re
       }
   }
   __syncwarp();
+  HCB_T(c1);
+  HCB_ACC(0, c0, c1);
   // ---- monomial program: degree d products from degree d-1 (shared by all entries) ----
   int lo = N + 1;
   for (int l = 0; l < A.n_levels; ++l) {
@@ -338,10 +378,14 @@ __device__ __forceinline__ bool eval_solve(const TrackArgs &A, const uint2 *__re
     lo = hi;
     __syncwarp();
   }
+  HCB_T(c2);
+  HCB_ACC(1, c1, c2);
   // ---- homogenised term evaluation, lane-balanced op list ----
   if (want_abs) run_ops<N, L, true>(ops_s, A.Q, rhs_off, cval, mono, M, rabs, row_of, r);
   else run_ops<N, L, false>(ops_s, A.Q, rhs_off, cval, mono, M, rabs, row_of, r);
   __syncwarp();
+  HCB_T(c3);
+  HCB_ACC(2, c2, c3);
   // ---- load row r of [A | b] into registers (structural zeros read the always-zero entry) ----
   double2 a[N + 1];
   const int rr = (r < N) ? r : 0;
@@ -358,7 +402,12 @@ __device__ __forceinline__ bool eval_solve(const TrackArgs &A, const uint2 *__re
   }
   fr = a[N];
   fabs_r = (r < N && want_abs) ? rabs[r] : 0.0;
-  return lu_rows<N, L>(a, r, seg, prow, pl, A.st.pivot_rel, jmax, y);
+  HCB_T(c4);
+  HCB_ACC(3, c3, c4);
+  const bool ok = lu_rows<N, L>(a, r, seg, prow, pl, A.st.pivot_rel, jmax, y);
+  HCB_T(c5);
+  HCB_ACC(4, c4, c5);
+  return ok;
 }
 
 // ------------------------------------------------------------------------------------------
@@ -414,6 +463,11 @@ __global__ void __launch_bounds__(TrackerShape<N>::MAXW * 32, TrackerShape<N>::M
   double2 x = make_double2(0.0, 0.0), kacc = x, kprev = x, xc = x;
   bool need_track = true;
   double cval_t = -1.0;   // t at which the slot's coefficient values were last evaluated (-1: none)
+#ifdef HCB_PHASE_TIMING
+  unsigned long long hcb_phase[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  long long hcb_iter0 = clock64();
+  long long hcb_k0 = hcb_iter0;
+#endif
 
   // begin a step attempt from (x, t) with dt; returns false when max_steps is exhausted
   auto begin_step = [&]() -> bool {
@@ -470,6 +524,10 @@ __global__ void __launch_bounds__(TrackerShape<N>::MAXW * 32, TrackerShape<N>::M
       }
     }
     if (__all_sync(FULL, state == ST_DONE)) break;
+#ifdef HCB_PHASE_TIMING
+    hcb_iter0 = clock64();
+    hcb_phase[7] += 1;   // iterations
+#endif
 
     // ---- what this slot evaluates in this iteration ----
     double te;
@@ -499,8 +557,15 @@ __global__ void __launch_bounds__(TrackerShape<N>::MAXW * 32, TrackerShape<N>::M
     cval_t = te;
     const bool ok = eval_solve<N, L>(A, ops_s, prog_s, mpos_s, row_of, ct, te, need_coef, rhs_off, want_abs, cval, mono,
                                      M, prow, rabs,
-                                     pl, r, seg, xe, yv, fr, fa);
+                                     pl, r, seg, xe, yv, fr, fa
+#ifdef HCB_PHASE_TIMING
+                                     , hcb_phase
+#endif
+                                     );
 
+#ifdef HCB_PHASE_TIMING
+    const long long hcb_e = clock64();
+#endif
     // ---- slot-uniform reductions, computed on all lanes before any slot-divergent branch ----
     const double2 base = (state == ST_POLISH) ? x : xc;
     const double2 cand = make_double2(base.x - yv.x, base.y - yv.y);   // Newton update x - dx
@@ -586,7 +651,17 @@ __global__ void __launch_bounds__(TrackerShape<N>::MAXW * 32, TrackerShape<N>::M
       if (dt < st.dt_min) finish(HC_STEP_UNDERFLOW, INFINITY, INFINITY);
       else if (!begin_step()) finish(HC_MAX_STEPS, INFINITY, INFINITY);
     }
+#ifdef HCB_PHASE_TIMING
+    hcb_phase[5] += (unsigned long long)(clock64() - hcb_e);          // reductions + state machine
+    hcb_phase[6] += (unsigned long long)(hcb_e - hcb_iter0);          // whole eval + solve
+#endif
   }
+#ifdef HCB_PHASE_TIMING
+  if ((threadIdx.x & 31) == 0 && A.phase_cycles) {
+    for (int i = 0; i < 8; ++i) atomicAdd(&A.phase_cycles[i], hcb_phase[i]);
+  }
+  (void)hcb_k0;
+#endif
 }
 
 template <int N>
