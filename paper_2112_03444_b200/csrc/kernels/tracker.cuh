@@ -371,7 +371,16 @@ __device__ __forceinline__ bool eval_solve(const TrackArgs &A, const uint2 *__re
   int lo = N + 1;
   for (int l = 0; l < A.n_levels; ++l) {
     const int hi = A.level_end[l];
-    for (int k = lo + r; k < hi; k += L) {
+    int k = lo + r;
+    // batches of 2 items per lane: both items' operands are loaded before either product is stored
+    // (the parents come from earlier levels, but the compiler cannot move loads above a store)
+    for (; k + L < hi; k += 2 * L) {
+      const uint32_t e0 = prog_s[k - (N + 1)], e1 = prog_s[k + L - (N + 1)];
+      const double2 a0 = mono[e0 & 0xFFFFu], b0 = mono[e0 >> 16], a1 = mono[e1 & 0xFFFFu], b1 = mono[e1 >> 16];
+      mono[k] = cmul(a0, b0);
+      mono[k + L] = cmul(a1, b1);
+    }
+    if (k < hi) {
       const uint32_t e = prog_s[k - (N + 1)];
       mono[k] = cmul(mono[e & 0xFFFFu], mono[e >> 16]);
     }
