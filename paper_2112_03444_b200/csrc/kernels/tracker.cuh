@@ -117,6 +117,36 @@ enum SlotState : int { ST_RK = 0, ST_NEWTON = 1, ST_POLISH = 2, ST_RESID = 3, ST
 // non-negative doubles like their values) + one ballot; L < 32: shuffle butterfly.
 // Returns the winning lane (segment-relative) and the maximum value (-1 when no candidate).
 // ------------------------------------------------------------------------------------------
+// Arg-max with the singularity test folded in: returns the pivot lane and sets sing when the maximum
+// is <= thr (or there is no candidate).  L == 32: the common case -- a unique maximum in the high
+// words that differs from thr's high word -- needs a single REDUX; ties or a high word equal to
+// thr's take the exact two-REDUX path of seg_argmax.
+template <int L>
+__device__ __forceinline__ int seg_argmax(double v, int r, double &vmax);
+template <int L>
+__device__ __forceinline__ int seg_argmax_thr(double v, int r, double thr, bool &sing) {
+  if constexpr (L == 32) {
+    const unsigned long long bits = (unsigned long long)__double_as_longlong(v);
+    const unsigned hi = (v >= 0.0) ? (unsigned)(bits >> 32) + 1u : 0u;
+    const unsigned mhi = __reduce_max_sync(FULL, hi);
+    const unsigned b1 = __ballot_sync(FULL, hi == mhi);
+    const unsigned thr_hi1 = (unsigned)((unsigned long long)__double_as_longlong(thr) >> 32) + 1u;
+    if (__popc(b1) == 1 && mhi != thr_hi1 && mhi != 0u) {   // warp-uniform branch
+      sing |= (mhi < thr_hi1);
+      return __ffs(b1) - 1;
+    }
+    double vmax;
+    const int idx = seg_argmax<L>(v, r, vmax);
+    sing |= !(vmax > thr);
+    return idx;
+  } else {
+    double vmax;
+    const int idx = seg_argmax<L>(v, r, vmax);
+    sing |= !(vmax > thr);
+    return idx;
+  }
+}
+
 template <int L>
 __device__ __forceinline__ int seg_argmax(double v, int r, double &vmax) {
   if constexpr (L == 32) {
@@ -173,11 +203,9 @@ __device__ __forceinline__ bool lu_rows(double2 (&a)[N + 1], int r, int seg, dou
   const double thr = pivot_rel * pivot_rel * am;
   bool sing = !(am < INFINITY);
   // pivot of step 0
-  double vmax;
   double v0 = used ? -1.0 : abs2(a[0]);
   if (!(v0 >= 0.0)) v0 = -1.0;   // NaN is never a pivot
-  int p = seg_argmax<L>(v0, r, vmax);
-  sing |= !(vmax > thr);
+  int p = seg_argmax_thr<L>(v0, r, thr, sing);
   double2 spec = crecip(a[0]);   // speculative 1/a_rk of this lane's candidate (overlaps the search)
 #pragma unroll
   for (int k = 0; k < N; ++k) {
@@ -203,7 +231,7 @@ __device__ __forceinline__ bool lu_rows(double2 (&a)[N + 1], int r, int seg, dou
       double v = abs2(a[k + 1]);
       if (used || (L < 32 && !(v >= 0.0))) v = -1.0;   // NaN is never a pivot (the REDUX path excludes it itself)
       spec = crecip(a[k + 1]);
-      p = seg_argmax<L>(v, r, vmax);
+      p = seg_argmax_thr<L>(v, r, thr, sing);
       __syncwarp();   // the published row is visible
       // trailing update in chunks of 4 columns: the 4 shared loads are issued before their FMAs so
       // the load latency overlaps (the compiler otherwise keeps only ~2 loads in flight)
@@ -217,7 +245,6 @@ __device__ __forceinline__ bool lu_rows(double2 (&a)[N + 1], int r, int seg, dou
         for (int i = 0; i < 4; ++i)
           if (j0 + i <= N) a[j0 + i] = cfms(a[j0 + i], l, u[i]);
       }
-      sing |= !(vmax > thr);
     }
   }
   __syncwarp();
