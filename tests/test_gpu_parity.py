@@ -425,3 +425,21 @@ def test_monodromy_trifocal_matches_oracle_fixture(hc, orc):
     res = monodromy_solve(s, x0, p0, symmetry=systems.trifocal_symmetry, seed=3, stall_loops=4)
     assert res.solutions.shape[0] == fix.shape[0], res.history
     assert_same_set_r21(orc, d, p0, fix, res.solutions, "trifocal monodromy")
+
+
+def test_bits_independent_of_launch_shape(hc, monkeypatch):
+    """S:277 determinism: a track's arithmetic does not depend on scheduling -- identical bits for a
+    different CTA shape (HC_TRACKER_WARPS) and for a batch that contains the instance at another
+    position."""
+    d = systems.nview_triangulation(4)
+    start = fixtures.read_solutions(fixtures.fixture_path("fourview_start.sols"))
+    p0 = fixtures.read_params(fixtures.fixture_path("fourview_p0.params"))
+    p1s, _ = rng.fourview_batch(6)
+    a = run_ph(hc, d, start, p0, p1s)
+    monkeypatch.setenv("HC_TRACKER_WARPS", "1")
+    b = run_ph(hc, d, start, p0, p1s[::-1].copy())
+    monkeypatch.delenv("HC_TRACKER_WARPS")
+    xa, xb = a.x.cpu().numpy(), b.x.cpu().numpy()[::-1]
+    assert a.launch()["warps_per_cta"] != b.launch()["warps_per_cta"]
+    assert np.array_equal(xa.view(np.float64), xb.view(np.float64))
+    assert np.array_equal(a.counters.cpu().numpy(), b.counters.cpu().numpy()[::-1])
