@@ -18,7 +18,8 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 INCLUDE = os.path.join(ROOT, "include")
 # HCB_VARIANT=timing builds an experiment library with per-phase cycle counters (-DHCB_PHASE_TIMING)
-# into lib_timing/ (load it with HC_LIB_PATH); the product library is the default variant.
+# into lib_timing/, HCB_VARIANT=hybrid one with the hybrid 16-lane layout for N = 17, 18 into
+# lib_hybrid/ (load either with HC_LIB_PATH); the product library is the default variant.
 VARIANT = os.environ.get("HCB_VARIANT", "")
 BUILD = os.path.join(PKG, "build" + ("_" + VARIANT if VARIANT else ""))
 LIBDIR = os.path.join(PKG, "lib" + ("_" + VARIANT if VARIANT else ""))
@@ -28,6 +29,8 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-I" + INCLUDE, "-I" + CSRC]
 if VARIANT == "timing":
     FLAGS = FLAGS + ["-DHCB_PHASE_TIMING"]
+elif VARIANT == "hybrid":   # experiment: 16-lane hybrid layout for N = 17, 18 (csrc/hc_internal.h)
+    FLAGS = FLAGS + ["-DHCB_HYBRID_LAYOUT=1"]
 
 
 def sources():

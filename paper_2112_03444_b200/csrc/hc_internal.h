@@ -100,10 +100,16 @@ cudaError_t launch_batched_zgesv(int n, int64_t batch, const double2 *A, const d
                                  int32_t *info, double pivot_rel, cudaStream_t);
 cudaError_t run_fp64_probe(int device, double *tflops);
 
-inline int lanes_for(int N) {
-  int L = 1;
-  while (L < N) L <<= 1;
-  return L;
+// Track layouts.  Default: a sub-warp of L = next_pow2(N) lanes, lane r owns row r.  Hybrid
+// layout for 17 <= N <= 18: L = 16 lanes (two tracks per warp); lane r owns row r, and the
+// E = N - 16 "extra" rows 16..N-1 are held column-distributed (lane r holds their columns r and
+// r + 16), see tracker.cuh lu_rows_hy.  Host (op balancing over L lanes) and device agree here.
+#ifndef HCB_HYBRID_LAYOUT
+#define HCB_HYBRID_LAYOUT 0   // experiment switch: measured slower on trifocal
+#endif
+__host__ __device__ constexpr bool hy_layout(int N) { return HCB_HYBRID_LAYOUT && (N == 17 || N == 18); }
+__host__ __device__ constexpr int lanes_for(int N) {
+  return hy_layout(N) ? 16 : (N <= 1) ? 1 : (N <= 2) ? 2 : (N <= 4) ? 4 : (N <= 8) ? 8 : (N <= 16) ? 16 : 32;
 }
 
 }  // namespace hcb

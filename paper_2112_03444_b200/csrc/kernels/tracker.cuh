@@ -43,9 +43,15 @@ constexpr unsigned FULL = 0xffffffffu;
 //   N <= 14: 4 warps x 4 CTAs (128 regs);  15..20: one 12-warp CTA per SM (168 regs; measured on the
 //   trifocal system: 12 warps at 168 regs beat 16 at 128 (spills) and 8 at 218);  N > 20: 4 warps x
 //   2 CTAs.  The launcher shrinks the CTA when the shared memory does not fit.
+//   Hybrid layout (hy_layout(N), 16-lane tracks with column-distributed extra rows): one 8-warp CTA
+//   (16 tracks; shared memory bound).
 template <int N>
 struct TrackerShape {
-  static constexpr int MAXW = (N >= 15 && N <= 20) ? 12 : 4;
+  static constexpr bool HY = hy_layout(N);
+  static constexpr int L = lanes_for(N);
+  static constexpr int E = HY ? N - 16 : 0;   // extra rows (hybrid layout)
+  static constexpr int NC = HY ? 2 : 1;       // unknown components per lane
+  static constexpr int MAXW = HY ? 8 : (N >= 15 && N <= 20) ? 12 : 4;
   static constexpr int MINB = (N <= 14) ? 4 : (N <= 20) ? 1 : 2;
 };
 
@@ -77,6 +83,8 @@ __device__ __forceinline__ double2 crecip(double2 a) {
   return make_double2(a.x * d, -a.y * d);
 }
 __device__ __forceinline__ bool cfinite(double2 a) { return isfinite(a.x) && isfinite(a.y); }
+// max that propagates NaN from b (a is >= 0 or NaN already)
+__device__ __forceinline__ double nmax(double a, double b) { return (b > a || b != b) ? b : a; }
 __device__ __forceinline__ double2 shfl2(double2 v, int src, int width) {
   return make_double2(__shfl_sync(FULL, v.x, src, width), __shfl_sync(FULL, v.y, src, width));
 }
@@ -258,6 +266,176 @@ __device__ __forceinline__ bool lu_rows(double2 (&a)[N + 1], int r, int seg, dou
 }
 
 // ------------------------------------------------------------------------------------------
+// The same elimination in the hybrid layout (hy_layout(N), 17 <= N <= 18): 16 lanes per track,
+// two tracks per warp.  Lane r holds row r of [A | b] in a[0..N] and, for each extra row
+// 16 + q (q < E = N - 16), the entries of columns r and r + 16 in e[q][0], e[q][1] (the second
+// exists when r + 16 <= N).  A 32-lane track would leave 14 of 32 lanes idle for N = 18; here the
+// idle work is 2 extra rows spread over 16 lanes, and the per-column pivot overhead is shared by
+// two tracks.  Same pivots (max |a|^2, ties -> lowest row, R13), same Gauss-Jordan update order.
+// Per column k: arg-max over own rows and the extras' column k (held by lane k & 15) by a
+// 16-lane (value, row) butterfly; 1/pivot and the pivot row's column k+1 are shuffled from the
+// lane(s) holding them; the extras' column-k entries are shuffled to every lane for their
+// multipliers; column k+1 is updated first; the pivot row's columns k+2..N go through shared
+// memory (an own row by its lane, an extra row by all lanes); then the trailing update.
+// Returns x_r in y[0] and x_{16+r} (r < E) in y[1].
+// ------------------------------------------------------------------------------------------
+template <int N, int E>
+__device__ __forceinline__ bool lu_rows_hy(double2 (&a)[N + 1], double2 (&e)[E][2], int r, int seg, double2 *prow,
+                                           double pivot_rel, double lane_max, double2 (&y)[2]) {
+  constexpr int L = 16;
+  const double2 zero = make_double2(0.0, 0.0);
+  bool used = false;
+  int mystep = N;
+  double2 myinv = zero;
+  bool eused[E];
+  int estep[E];
+  double2 einv[E];
+#pragma unroll
+  for (int q = 0; q < E; ++q) {
+    eused[q] = false;
+    estep[q] = N;
+    einv[q] = zero;
+  }
+  const double am = seg_max<L>(lane_max);
+  const double thr = pivot_rel * pivot_rel * am;
+  bool sing = !(am < INFINITY);
+#pragma unroll
+  for (int k = 0; k < N; ++k) {
+    const int kc = k & 15, ks = k >> 4;               // lane and slot of the extras' column k
+    const int kc1 = (k + 1) & 15, ks1 = (k + 1) >> 4;  // ... and of column k+1
+    double2 *pr = prow + (k & 1) * (N + 1);
+    // ---- pivot: (value, row) arg-max over the own rows and the extras' column k ----
+    double v = used ? -1.0 : abs2(a[k]);
+    if (!(v >= 0.0)) v = -1.0;   // NaN is never a pivot
+    int row = r;
+#pragma unroll
+    for (int q = 0; q < E; ++q) {
+      double ve = abs2(e[q][ks]);
+      if (eused[q] || r != kc || !(ve >= 0.0)) ve = -1.0;
+      if (ve > v) {
+        v = ve;
+        row = 16 + q;
+      }
+    }
+#pragma unroll
+    for (int off = L / 2; off >= 1; off >>= 1) {
+      const double ov = __shfl_xor_sync(FULL, v, off);
+      const int orow = __shfl_xor_sync(FULL, row, off);
+      if (ov > v || (ov == v && orow < row)) {
+        v = ov;
+        row = orow;
+      }
+    }
+    const int pid = row;   // uniform over the segment
+    sing |= !(v > thr);
+    // ---- 1/pivot and the pivot row's column k+1 ----
+    double2 pv = a[k], pu = a[k + 1];
+    int src = pid, src1 = pid;
+    if (pid >= 16) {
+#pragma unroll
+      for (int q = 0; q < E; ++q)
+        if (pid == 16 + q) {
+          pv = e[q][ks];
+          pu = e[q][ks1];
+        }
+      src = kc;
+      src1 = kc1;
+    }
+    const double2 inv = crecip(shfl2(pv, src, L));
+    const double2 u1 = shfl2(pu, src1, L);
+    // ---- multipliers (the pivot row keeps its entries; every other row is eliminated) ----
+    const bool me = (r == pid);
+    const double2 l = me ? zero : cmul(a[k], inv);
+    double2 le[E];
+#pragma unroll
+    for (int q = 0; q < E; ++q) {
+      const double2 ek = shfl2(e[q][ks], kc, L);
+      le[q] = (pid == 16 + q) ? zero : cmul(ek, inv);
+    }
+    // ---- column k+1 first (k + 1 == N: the right-hand side) ----
+    a[k + 1] = cfms(a[k + 1], l, u1);
+#pragma unroll
+    for (int q = 0; q < E; ++q) {
+      const double2 t1 = cfms(e[q][ks1], le[q], u1);
+      if (r == kc1) e[q][ks1] = t1;
+    }
+    if (me) {
+      used = true;
+      mystep = k;
+      myinv = inv;
+    }
+#pragma unroll
+    for (int q = 0; q < E; ++q)
+      if (pid == 16 + q) {
+        eused[q] = true;
+        estep[q] = k;
+        einv[q] = inv;
+      }
+    if (k + 1 < N) {
+      // ---- publish columns k+2..N of the pivot row ----
+      if (me) {
+#pragma unroll
+        for (int j = k + 2; j <= N; ++j) pr[j] = a[j];
+      }
+      if (pid >= 16) {
+        double2 s0 = zero, s1 = zero;
+#pragma unroll
+        for (int q = 0; q < E; ++q)
+          if (pid == 16 + q) {
+            s0 = e[q][0];
+            s1 = e[q][1];
+          }
+        pr[r] = s0;
+        if (r + 16 <= N) pr[r + 16] = s1;
+      }
+      __syncwarp();
+      // ---- trailing update: own row, columns k+2..N (4 loads in flight per chunk) ----
+#pragma unroll
+      for (int j0 = k + 2; j0 <= N; j0 += 4) {
+        double2 u[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+          if (j0 + i <= N) u[i] = pr[j0 + i];
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+          if (j0 + i <= N) a[j0 + i] = cfms(a[j0 + i], l, u[i]);
+      }
+      // ---- trailing update of the extras: lane r's columns r and r + 16 when >= k+2 ----
+      if (k + 2 <= 15) {
+        const double2 u = pr[r];
+#pragma unroll
+        for (int q = 0; q < E; ++q) {
+          const double2 t0 = cfms(e[q][0], le[q], u);
+          if (r >= k + 2) e[q][0] = t0;
+        }
+      }
+      {
+        const int c1 = (r + 16 <= N) ? r + 16 : N;
+        const double2 u = pr[c1];
+#pragma unroll
+        for (int q = 0; q < E; ++q) {
+          const double2 t0 = cfms(e[q][1], le[q], u);
+          if (r + 16 >= k + 2 && r + 16 <= N) e[q][1] = t0;
+        }
+      }
+    }
+  }
+  __syncwarp();
+  // ---- the system is diagonal in pivot order: x_step = b' / pivot ----
+  double2 *xsol = prow;
+  if (mystep < N) xsol[mystep] = cmul(a[N], myinv);
+  if (r == (N & 15)) {
+#pragma unroll
+    for (int q = 0; q < E; ++q)
+      if (estep[q] < N) xsol[estep[q]] = cmul(e[q][N >> 4], einv[q]);
+  }
+  __syncwarp();
+  y[0] = xsol[r];
+  y[1] = (r < E) ? xsol[16 + r] : zero;
+  return seg_all<L>(!sing && cfinite(y[0]) && cfinite(y[1]), seg);
+}
+
+// ------------------------------------------------------------------------------------------
 // Op list: M[dest] = sum over the entry's ops of coef[slot] * mono[k] (P:432-434 terms with the
 // products shared through the monomial program).  ABS also accumulates sum |c m| for the
 // relative residual of the rhs rows (reading R10).
@@ -356,15 +534,15 @@ __device__ __forceinline__ void horner(const double2 *__restrict__ ct, double t,
 // component y_r in lane r (r < N) and whether the solve succeeded (uniform over the slot).
 // rhs_off = 0 -> rhs = H (coefficients c(t)); rhs_off = ncoef -> rhs = dH/dt (coefficients c'(t)).
 // ------------------------------------------------------------------------------------------
-template <int N, int L>
+template <int N, int L, int NC>
 __device__ __forceinline__ bool eval_solve(const TrackArgs &A, const uint2 *__restrict__ ops_s,
                                            const uint32_t *__restrict__ prog_s, const int16_t *__restrict__ mpos_s,
                                            const int16_t *__restrict__ row_of, const double2 *__restrict__ ct,
                                            double t, bool need_coef, int rhs_off, bool want_abs, double2 *cval,
                                            double2 *mono,
                                            double2 *M, double2 *prow, double *rabs, uint8_t *pl, int r, int seg,
-                                           double2 xr,
-                                           double2 &y, double2 &fr, double &fabs_r
+                                           const double2 (&xr)[NC],
+                                           double2 (&y)[NC], double2 (&fr)[NC], double (&fabs_r)[NC]
 #ifdef HCB_PHASE_TIMING
                                            , unsigned long long (&hcb_phase)[8]
 #endif
@@ -373,7 +551,11 @@ __device__ __forceinline__ bool eval_solve(const TrackArgs &A, const uint2 *__re
   // ---- stage x (monomial slots 0..N-1) and coefficient values c(t) (all slots), c'(t) (rhs
   //      slots) by Horner on the prologue's polynomials in t ----
   HCB_T(c0);
-  if (r < N) mono[r] = xr;
+  constexpr int E = TrackerShape<N>::E;
+  if (r < N) mono[r] = xr[0];
+  if constexpr (NC == 2) {
+    if (r < E) mono[16 + r] = xr[NC - 1];
+  }
   if (need_coef) switch (D) {   // D is uniform: the common degrees keep all loads of a coefficient in flight together
     case 1: horner<1, L>(ct, t, ncoef, A.ncoef_src, cval, r); break;
     case 2: horner<2, L>(ct, t, ncoef, A.ncoef_src, cval, r); break;
@@ -423,6 +605,34 @@ __device__ __forceinline__ bool eval_solve(const TrackArgs &A, const uint2 *__re
   HCB_T(c3);
   HCB_ACC(2, c2, c3);
   // ---- load row r of [A | b] into registers (structural zeros read the always-zero entry) ----
+  if constexpr (NC == 2) {
+    // hybrid layout: row r plus the extra rows' columns r and r + 16
+    double2 a[N + 1], e[E][2];
+    double jmax = 0.0;
+#pragma unroll
+    for (int j = 0; j <= N; ++j) {
+      a[j] = M[mpos_s[r * (N + 1) + j]];
+      if (j < N) jmax = fmax(jmax, abs2(a[j]));
+    }
+#pragma unroll
+    for (int q = 0; q < E; ++q)
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        const int col = r + 16 * c;
+        e[q][c] = (col <= N) ? M[mpos_s[(16 + q) * (N + 1) + col]] : make_double2(0.0, 0.0);
+        if (col < N) jmax = fmax(jmax, abs2(e[q][c]));
+      }
+    fr[0] = a[N];
+    fr[NC - 1] = (r < E) ? M[mpos_s[(16 + (r < E ? r : 0)) * (N + 1) + N]] : make_double2(0.0, 0.0);
+    fabs_r[0] = want_abs ? rabs[r] : 0.0;
+    fabs_r[NC - 1] = (r < E && want_abs) ? rabs[16 + r] : 0.0;
+    HCB_T(c4h);
+    HCB_ACC(3, c3, c4h);
+    const bool okh = lu_rows_hy<N, E>(a, e, r, seg, prow, A.st.pivot_rel, jmax, y);
+    HCB_T(c5h);
+    HCB_ACC(4, c4h, c5h);
+    return okh;
+  }
   double2 a[N + 1];
   const int rr = (r < N) ? r : 0;
   double jmax = 0.0;   // max |A_rj|^2 of this row, for the singularity threshold (R9)
@@ -436,11 +646,11 @@ __device__ __forceinline__ bool eval_solve(const TrackArgs &A, const uint2 *__re
 #pragma unroll
     for (int j = 0; j <= N; ++j) a[j] = make_double2(0.0, 0.0);
   }
-  fr = a[N];
-  fabs_r = (r < N && want_abs) ? rabs[r] : 0.0;
+  fr[0] = a[N];
+  fabs_r[0] = (r < N && want_abs) ? rabs[r] : 0.0;
   HCB_T(c4);
   HCB_ACC(3, c3, c4);
-  const bool ok = lu_rows<N, L>(a, r, seg, prow, pl, A.st.pivot_rel, jmax, y);
+  const bool ok = lu_rows<N, L>(a, r, seg, prow, pl, A.st.pivot_rel, jmax, y[0]);
   HCB_T(c5);
   HCB_ACC(4, c4, c5);
   return ok;
@@ -451,7 +661,9 @@ __device__ __forceinline__ bool eval_solve(const TrackArgs &A, const uint2 *__re
 // ------------------------------------------------------------------------------------------
 template <int N>
 __global__ void __launch_bounds__(TrackerShape<N>::MAXW * 32, TrackerShape<N>::MINB) hc_track_kernel(const TrackArgs A) {
-  constexpr int L = (N <= 1) ? 1 : (N <= 2) ? 2 : (N <= 4) ? 4 : (N <= 8) ? 8 : (N <= 16) ? 16 : 32;
+  constexpr int L = TrackerShape<N>::L;
+  constexpr int NC = TrackerShape<N>::NC;   // unknown components per lane (2: hybrid layout)
+  constexpr int E = TrackerShape<N>::E;
   constexpr int TPW = 32 / L;
   extern __shared__ __align__(16) unsigned char smem_raw[];
 
@@ -496,7 +708,12 @@ __global__ void __launch_bounds__(TrackerShape<N>::MAXW * 32, TrackerShape<N>::M
   const double2 *ct = A.coef_t;   // instance coefficient table
   double t = 0.0, dt = 0.0, h = 0.0, t1 = 0.0;
   int stage = 0, it = 0, acc = 0, steps = 0, rej = 0, newt = 0, solves = 0;
-  double2 x = make_double2(0.0, 0.0), kacc = x, kprev = x, xc = x;
+  // component c of lane r is unknown r (c = 0) or 16 + r (c = 1, hybrid layout, r < E)
+  double2 x[NC], kacc[NC], kprev[NC], xc[NC];
+#pragma unroll
+  for (int c = 0; c < NC; ++c) x[c] = kacc[c] = kprev[c] = xc[c] = make_double2(0.0, 0.0);
+  auto comp_valid = [&](int c) -> bool { return c == 0 ? (r < N) : (r < E); };
+  auto comp_row = [&](int c) -> int { return c == 0 ? r : 16 + r; };
   bool need_track = true;
   double cval_t = -1.0;   // t at which the slot's coefficient values were last evaluated (-1: none)
 #ifdef HCB_PHASE_TIMING
@@ -516,13 +733,15 @@ __global__ void __launch_bounds__(TrackerShape<N>::MAXW * 32, TrackerShape<N>::M
       h = 1.0 - t;
     }
     stage = 0;
-    kacc = make_double2(0.0, 0.0);
-    kprev = make_double2(0.0, 0.0);
+#pragma unroll
+    for (int c = 0; c < NC; ++c) kacc[c] = kprev[c] = make_double2(0.0, 0.0);
     state = ST_RK;
     return true;
   };
   auto finish = [&](int status, double ra, double rr) {
-    if (r < N) A.x_out[(size_t)g * N + r] = x;
+#pragma unroll
+    for (int c = 0; c < NC; ++c)
+      if (comp_valid(c)) A.x_out[(size_t)g * N + comp_row(c)] = x[c];
     if (r == 0) {
       A.status_out[g] = status;
       int4 c = make_int4(steps, rej, newt, solves);
@@ -547,7 +766,8 @@ __global__ void __launch_bounds__(TrackerShape<N>::MAXW * 32, TrackerShape<N>::M
           const long long b = g / A.S, s = g % A.S;
           ct = A.coef_t + (size_t)b * (D + 1) * ncoef;
           cval_t = -1.0;   // new instance: coefficient values are stale
-          x = (r < N) ? A.start_x[s * N + r] : make_double2(0.0, 0.0);
+#pragma unroll
+          for (int c = 0; c < NC; ++c) x[c] = comp_valid(c) ? A.start_x[s * N + comp_row(c)] : make_double2(0.0, 0.0);
           t = 0.0;
           dt = st.dt_init;
           acc = steps = rej = newt = solves = 0;
@@ -567,31 +787,36 @@ __global__ void __launch_bounds__(TrackerShape<N>::MAXW * 32, TrackerShape<N>::M
 
     // ---- what this slot evaluates in this iteration ----
     double te;
-    double2 xe;
+    double2 xe[NC];
     int rhs_off = 0;
     if (state == ST_RK) {
-      const double c = (stage == 0) ? 0.0 : (stage == 3 ? 1.0 : 0.5);
-      te = t + c * h;
-      xe = make_double2(fma(c * h, kprev.x, x.x), fma(c * h, kprev.y, x.y));
+      const double cs = (stage == 0) ? 0.0 : (stage == 3 ? 1.0 : 0.5);
+      te = t + cs * h;
+#pragma unroll
+      for (int c = 0; c < NC; ++c)
+        xe[c] = make_double2(fma(cs * h, kprev[c].x, x[c].x), fma(cs * h, kprev[c].y, x[c].y));
       rhs_off = ncoef;  // rhs = dH/dt
     } else if (state == ST_NEWTON) {
       te = t1;
-      xe = xc;
+#pragma unroll
+      for (int c = 0; c < NC; ++c) xe[c] = xc[c];
     } else if (state == ST_POLISH || state == ST_RESID) {
       te = 1.0;
-      xe = x;
+#pragma unroll
+      for (int c = 0; c < NC; ++c) xe[c] = x[c];
     } else {
       te = 0.0;
-      xe = make_double2(0.0, 0.0);
+#pragma unroll
+      for (int c = 0; c < NC; ++c) xe[c] = make_double2(0.0, 0.0);
     }
     const bool want_abs = __any_sync(FULL, state == ST_RESID);
-    double2 yv, fr;
-    double fa;
+    double2 yv[NC], fr[NC];
+    double fa[NC];
     // coefficient values depend only on (instance, t): RK stages 2/3 share t + h/2, and stage 4,
     // the Newton iterations and the next step's stage 1 share t + h, so Horner is skipped then
     const bool need_coef = (te != cval_t);
     cval_t = te;
-    const bool ok = eval_solve<N, L>(A, ops_s, prog_s, mpos_s, row_of, ct, te, need_coef, rhs_off, want_abs, cval, mono,
+    const bool ok = eval_solve<N, L, NC>(A, ops_s, prog_s, mpos_s, row_of, ct, te, need_coef, rhs_off, want_abs, cval, mono,
                                      M, prow, rabs,
                                      pl, r, seg, xe, yv, fr, fa
 #ifdef HCB_PHASE_TIMING
@@ -603,15 +828,30 @@ __global__ void __launch_bounds__(TrackerShape<N>::MAXW * 32, TrackerShape<N>::M
     const long long hcb_e = clock64();
 #endif
     // ---- slot-uniform reductions, computed on all lanes before any slot-divergent branch ----
-    const double2 base = (state == ST_POLISH) ? x : xc;
-    const double2 cand = make_double2(base.x - yv.x, base.y - yv.y);   // Newton update x - dx
-    const bool cand_fin = seg_all<L>(cfinite(cand), seg);
-    const double d2 = seg_max<L>(abs2(yv));
-    const double c2 = seg_max<L>(abs2(cand));
+    double2 cand[NC];
+    bool fin = true;
+    double yd2 = 0.0, cd2 = 0.0;
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+      const double2 base = (state == ST_POLISH) ? x[c] : xc[c];
+      cand[c] = make_double2(base.x - yv[c].x, base.y - yv[c].y);   // Newton update x - dx
+      fin = fin && cfinite(cand[c]);
+      yd2 = nmax(yd2, abs2(yv[c]));
+      cd2 = nmax(cd2, abs2(cand[c]));
+    }
+    const bool cand_fin = seg_all<L>(fin, seg);
+    const double d2 = seg_max<L>(NC == 1 ? abs2(yv[0]) : yd2);
+    const double c2 = seg_max<L>(NC == 1 ? abs2(cand[0]) : cd2);
     double res_abs = 0.0, res_rel = 0.0;
     if (want_abs) {   // warp-uniform: only when some slot classifies its endpoint
-      const double fm = (r < N) ? sqrt(abs2(fr)) : 0.0;
-      const double fq = (r < N) ? (fa > 0.0 ? fm / fa : (fm == 0.0 ? 0.0 : INFINITY)) : 0.0;
+      double fm = 0.0, fq = 0.0;
+#pragma unroll
+      for (int c = 0; c < NC; ++c) {
+        if (!comp_valid(c)) continue;
+        const double m = sqrt(abs2(fr[c]));
+        fm = nmax(fm, m);
+        fq = nmax(fq, fa[c] > 0.0 ? m / fa[c] : (m == 0.0 ? 0.0 : INFINITY));
+      }
       res_abs = seg_max<L>(fm);
       res_rel = seg_max<L>(fq);
     }
@@ -624,18 +864,24 @@ __global__ void __launch_bounds__(TrackerShape<N>::MAXW * 32, TrackerShape<N>::M
       if (!ok) {
         reject = true;
       } else {
-        const double2 k = make_double2(-yv.x, -yv.y);
         const double w = (stage == 0 || stage == 3) ? 1.0 : 2.0;
-        kacc = make_double2(fma(w, k.x, kacc.x), fma(w, k.y, kacc.y));
-        kprev = k;
+#pragma unroll
+        for (int c = 0; c < NC; ++c) {
+          const double2 k = make_double2(-yv[c].x, -yv[c].y);
+          kacc[c] = make_double2(fma(w, k.x, kacc[c].x), fma(w, k.y, kacc[c].y));
+          kprev[c] = k;
+        }
         if (stage + 1 < n_rk) {
           ++stage;
         } else {
-          if (n_rk == 1) {
-            xc = make_double2(fma(h, k.x, x.x), fma(h, k.y, x.y));
-          } else {
-            const double h6 = h / 6.0;
-            xc = make_double2(fma(h6, kacc.x, x.x), fma(h6, kacc.y, x.y));
+#pragma unroll
+          for (int c = 0; c < NC; ++c) {
+            if (n_rk == 1) {
+              xc[c] = make_double2(fma(h, kprev[c].x, x[c].x), fma(h, kprev[c].y, x[c].y));
+            } else {
+              const double h6 = h / 6.0;
+              xc[c] = make_double2(fma(h6, kacc[c].x, x[c].x), fma(h6, kacc[c].y, x[c].y));
+            }
           }
           state = ST_NEWTON;
           it = 0;
@@ -646,7 +892,8 @@ __global__ void __launch_bounds__(TrackerShape<N>::MAXW * 32, TrackerShape<N>::M
       if (!ok || !cand_fin) {
         reject = true;
       } else {
-        xc = cand;
+#pragma unroll
+        for (int c = 0; c < NC; ++c) xc[c] = cand[c];
         if (d2 <= st.newton_tol * st.newton_tol * fmax(1.0, c2)) accept = true;
         else if (++it >= st.max_newton) reject = true;
       }
@@ -654,7 +901,8 @@ __global__ void __launch_bounds__(TrackerShape<N>::MAXW * 32, TrackerShape<N>::M
       if (!ok) {
         state = ST_RESID;
       } else {
-        x = cand;
+#pragma unroll
+        for (int c = 0; c < NC; ++c) x[c] = cand[c];
         if (!cand_fin) {
           finish(HC_NONFINITE, INFINITY, INFINITY);
         } else if (d2 <= st.end_tol * st.end_tol * fmax(1.0, c2) || ++it >= st.end_newton) {
@@ -666,7 +914,8 @@ __global__ void __launch_bounds__(TrackerShape<N>::MAXW * 32, TrackerShape<N>::M
       finish(status, res_abs, res_rel);
     }
     if (accept) {
-      x = xc;
+#pragma unroll
+      for (int c = 0; c < NC; ++c) x[c] = xc[c];
       t = t1;
       if (++acc >= st.grow_after) {
         dt = fmin(dt * st.grow, st.dt_max);
@@ -702,7 +951,7 @@ __global__ void __launch_bounds__(TrackerShape<N>::MAXW * 32, TrackerShape<N>::M
 
 template <int N>
 cudaError_t launch_tracker_n(const TrackArgs &A, int device, cudaStream_t stream, TrackerPlan *plan) {
-  constexpr int L = (N <= 1) ? 1 : (N <= 2) ? 2 : (N <= 4) ? 4 : (N <= 8) ? 8 : (N <= 16) ? 16 : 32;
+  constexpr int L = TrackerShape<N>::L;
   constexpr int TPW = 32 / L;
   const size_t tables = table_bytes(A.Q, L, A.n_mono - (N + 1), N) + align16((size_t)2 * A.n_entries);
   const size_t per_warp = (size_t)TPW * slot_bytes(N, A.ncoef, A.ncoef_src, A.n_mono, A.n_entries + 1);
