@@ -1,6 +1,6 @@
 """Benchmark: device-timed tracks/s and instances/s of the fused B200 HC tracker.
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--config trifocal|fourview|cyclic7|katsura6]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config trifocal|fourview|fivepoint|cyclic7|katsura6]
                   [--instances B] [--impl ours|reference] [--no-e2e] [--no-cpu-baseline]
 
 One "step" = one pass of the whole hot path (coefficient prologue + fused tracker: every
@@ -55,6 +55,14 @@ def make_workload(name: str, B: int, rank: int):
         p1s = np.stack([rng.fourview_instance(rng.SEED_FOURVIEW_INSTANCE + rank * B + b)[0] for b in range(B)])
         meta = {"workload": f"4-view triangulation (14x14, Table 2 P:490) PH, S=296 x {B} planted instances "
                             f"per GPU (configs[2])"}
+        return d, start, p0, p1s, {}, meta
+    if name == "fivepoint":
+        d = systems.fivepoint_relpose_depth()
+        start = fixtures.read_solutions(fixtures.fixture_path("fivepoint_start.sols"))
+        p0 = fixtures.read_params(fixtures.fixture_path("fivepoint_p0.params"))
+        p1s = np.stack([rng.fivepoint_instance(rng.SEED_FIVEPOINT_INSTANCE + rank * B + b)[0] for b in range(B)])
+        meta = {"workload": f"5-point rel. pose + depth (16x16, Table 2 P:492; reading R24) PH, S=40 x {B} "
+                            f"planted instances per GPU (SURVEY N2)"}
         return d, start, p0, p1s, {}, meta
     if name in ("cyclic7", "katsura6"):
         d = systems.cyclic(7) if name == "cyclic7" else systems.katsura(6)
@@ -326,7 +334,7 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=1)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", default="trifocal", choices=["trifocal", "fourview", "cyclic7", "katsura6"])
+    ap.add_argument("--config", default="trifocal", choices=["trifocal", "fourview", "fivepoint", "cyclic7", "katsura6"])
     ap.add_argument("--instances", type=int, default=1024)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--warmup-instances", type=int, default=16)

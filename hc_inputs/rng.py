@@ -240,3 +240,61 @@ def fourview_complex_start(seed: int = 23, nv: int = 4):
     null = Vh[A.shape[0]:].conj().T
     E = E0 + null @ complex_normal(g, null.shape[1])
     return np.concatenate([gam.reshape(-1), E]).astype(np.complex128), x0
+
+
+# ---------------------------------------------------------------------------
+# Five-point relative pose + depth (N2 workload, reading R24)
+# ---------------------------------------------------------------------------
+
+SEED_FIVEPOINT_INSTANCE = 6_000_000
+SEED_FIVEPOINT_MONODROMY = 13
+
+
+def fivepoint_project(x: np.ndarray, gam: np.ndarray) -> np.ndarray:
+    """Second-view coordinates that make x an exact solution, given the first view gam [5, 2]:
+    W = rho_i R(q) gamma_i + T, rhob_i = W_z, gammab_i = W / W_z.  Returns (p [20], x with rhob set)."""
+    x = np.array(x, dtype=np.result_type(x, gam, np.complex128))
+    R = np.array(systems.quat_rot(*x[10:14]))
+    T = np.array([x[14], x[15], 1.0])
+    p = np.zeros(20, dtype=x.dtype)
+    for i in range(5):
+        g = np.array([gam[i, 0], gam[i, 1], 1.0])
+        W = x[i] * (R @ g) + T
+        x[5 + i] = W[2]
+        p[systems.fivepoint_param_index(0, i, 0)] = gam[i, 0]
+        p[systems.fivepoint_param_index(0, i, 1)] = gam[i, 1]
+        p[systems.fivepoint_param_index(1, i, 0)] = W[0] / W[2]
+        p[systems.fivepoint_param_index(1, i, 1)] = W[1] / W[2]
+    return p, x
+
+
+def fivepoint_instance(seed: int):
+    """Planted real 5-point instance: rotation 0.1-0.5 rad, T = (tx, ty, 1) with tx, ty ~ N(0, 0.5),
+    five points at depth 3-6 in front of both cameras, normalised image coordinates |u|, |v| <= 0.4.
+    Returns (p [20] complex, x_gt [16] complex)."""
+    g = gen(seed)
+    while True:
+        _, q = random_rotation(g)
+        t = g.normal(0, 0.5, 2)
+        rho = g.uniform(3, 6, 5)
+        gam = g.uniform(-0.4, 0.4, (5, 2))
+        x = np.concatenate([rho, np.zeros(5), q, t]).astype(np.complex128)
+        p, x = fivepoint_project(x, gam.astype(np.complex128))
+        if np.all(x[5:10].real > 1.0):
+            return p, x
+
+
+def fivepoint_batch(n_instances: int, base: int = SEED_FIVEPOINT_INSTANCE):
+    ps, xs = zip(*(fivepoint_instance(base + b) for b in range(n_instances)))
+    return np.stack(ps), np.stack(xs)
+
+
+def fivepoint_complex_start(seed: int = SEED_FIVEPOINT_MONODROMY):
+    """Planted generic complex (x0, p0) for monodromy: complex depths, T, first-view points and q
+    normalised by the complex square root of q.q; the second view from the closed form."""
+    g = gen(seed)
+    x = complex_normal(g, 16)
+    x[10:14] /= np.sqrt(np.sum(x[10:14] ** 2))
+    gam = complex_normal(g, (5, 2))
+    p, x = fivepoint_project(x, gam)
+    return p, x

@@ -215,3 +215,54 @@ def trifocal_symmetry(x):
             y[14] = -y[14]
         out.append(y)
     return out
+
+
+# ---------------------------------------------------------------------------
+# Five-point relative pose with depth reconstruction (Table 2 P:492;
+# reading R24)
+# ---------------------------------------------------------------------------
+
+FIVEPOINT_VARS = ([f"rho{i + 1}" for i in range(5)] + [f"rhob{i + 1}" for i in range(5)]
+                  + ["a", "b", "c", "d", "tx", "ty"])
+
+
+def fivepoint_param_index(view: int, point: int, coord: int) -> int:
+    """p index of image coordinate `coord` (0: u, 1: v) of `point` (0..4) in `view` (0: gamma, 1: gamma-bar)."""
+    return 10 * view + 2 * point + coord
+
+
+def fivepoint_relpose_depth() -> SystemDesc:
+    """16x16 relative pose + depth reconstruction (reading R24).
+
+    rhob_i gammab_i = R(q) rho_i gamma_i + T for five correspondences gamma_i = (u_i, v_i, 1),
+    gammab_i = (ub_i, vb_i, 1) (the 15 equations of, row by row), plus q.q = 1 (P:207:
+    "quaternions which involves 4 unknowns with one equation").  The scale is fixed by T_z = 1,
+    T = (tx, ty, 1) (the 2-parameter T-hat of P:207).  Unknowns FIVEPOINT_VARS (16);
+    parameters: 20 image coordinates in fivepoint_param_index order.
+    """
+    n, P = 16, 20
+    X = [var_x(n, P, i) for i in range(n)]
+    Pv = [var_p(n, P, q) for q in range(P)]
+    one = const(n, P, 1)
+    rho, rhob = X[0:5], X[5:10]
+    a, b, c, d = X[10:14]
+    T = [X[14], X[15], one]
+    R = quat_rot(a, b, c, d)
+    eqs = []
+    for i in range(5):
+        g = [Pv[fivepoint_param_index(0, i, 0)], Pv[fivepoint_param_index(0, i, 1)], one]
+        gb = [Pv[fivepoint_param_index(1, i, 0)], Pv[fivepoint_param_index(1, i, 1)], one]
+        for row in range(3):
+            Rg = R[row][0] * g[0] + R[row][1] * g[1] + R[row][2] * g[2]
+            eqs.append(rhob[i] * gb[row] - rho[i] * Rg - T[row])
+    eqs.append(a * a + b * b + c * c + d * d - 1)
+    return desc_from_equations(eqs, name="5pt-relpose-depth", var_names=FIVEPOINT_VARS)
+
+
+def fivepoint_symmetry(x):
+    """q -> -q leaves R(q) and hence every equation unchanged: the two images of a solution."""
+    import numpy as np
+    x = np.asarray(x, dtype=np.complex128)
+    y = x.copy()
+    y[10:14] = -y[10:14]
+    return [x, y]

@@ -2,6 +2,7 @@
 
   python scripts/make_fixtures.py fourview   # 4-view TD solve at generic complex p0 -> 296 starts
   python scripts/make_fixtures.py trifocal   # trifocal monodromy from a planted (x0, p0)
+  python scripts/make_fixtures.py fivepoint  # 5-point relpose + depth monodromy (reading R24)
 
 This script imports only `oracle` and `hc_inputs`; the CUDA path never writes fixtures
 (prompt rule ③: no stored value comes from the CUDA path).  Start systems of the paper's
@@ -60,16 +61,15 @@ def _contains(S, y, tol=1e-6):
     return bool(np.any(np.all(np.abs(S - y) <= tol * np.maximum(1.0, np.abs(y)), axis=1)))
 
 
-def make_trifocal(max_loops: int = 60, stall_loops: int = 4, seed: int = rng.SEED_TRIFOCAL_MONODROMY):
-    """Monodromy ("monodromy module", SURVEY.md [X6]) with the Z2^3 symmetry of R20:
-    only one representative per orbit is tracked; endpoints are expanded by the 8 group elements."""
-    d = systems.trifocal_unknown_f()
-    p0, x0 = rng.trifocal_complex_start(seed)
+def _monodromy(d, p0, x0, orbit, seed, max_loops, stall_loops, label):
+    """Monodromy ("monodromy module", SURVEY.md [X6]) with a solution symmetry `orbit`:
+    only one representative per orbit is tracked; endpoints are expanded by the group."""
     reps = [x0]
-    full = np.array(_orbit(x0))
+    full = np.array(orbit(x0))
     g = rng.gen(seed + 1)
     stall = 0
     t0 = time.time()
+    loop = 0
     for loop in range(max_loops):
         p1 = rng.complex_normal(g, d.n_params)
         p2 = rng.complex_normal(g, d.n_params)
@@ -84,25 +84,47 @@ def make_trifocal(max_loops: int = 60, stall_loops: int = 4, seed: int = rng.SEE
         for y in X:
             if not _contains(full, y):
                 reps.append(y)
-                full = np.concatenate([full, np.array(_orbit(y))])
+                full = np.concatenate([full, np.array(orbit(y))])
                 new += 1
         stall = stall + 1 if new == 0 else 0
-        print(f"loop {loop}: tracked {len(alive)}/{len(reps) - new} survived, +{new} orbits -> "
+        print(f"{label} loop {loop}: tracked {len(alive)}/{len(reps) - new} survived, +{new} orbits -> "
               f"{len(reps)} orbits = {full.shape[0]} solutions ({time.time() - t0:.0f} s)", flush=True)
         if stall >= stall_loops:
             break
+    return reps, full, loop + 1
+
+
+def make_trifocal(max_loops: int = 60, stall_loops: int = 4, seed: int = rng.SEED_TRIFOCAL_MONODROMY):
+    """Trifocal monodromy with the Z2^3 symmetry of R20."""
+    d = systems.trifocal_unknown_f()
+    p0, x0 = rng.trifocal_complex_start(seed)
+    reps, full, loops = _monodromy(d, p0, x0, _orbit, seed, max_loops, stall_loops, "trifocal")
     hdr = (f"trifocal unknown-f start solutions at the planted complex p0 = rng.trifocal_complex_start({seed}).\n"
-           f"Written by scripts/make_fixtures.py (oracle only): symmetry-aware monodromy, {loop + 1} loops,\n"
+           f"Written by scripts/make_fixtures.py (oracle only): symmetry-aware monodromy, {loops} loops,\n"
            f"{len(reps)} orbits x 8 = {full.shape[0]} solutions (PAPER.md Table 2 P:488 reports 1784).")
     # the full start set is trifocal_reps.sols expanded by the symmetry (hc_inputs.fixtures.trifocal_start)
     fixtures.write_solutions(fixtures.fixture_path("trifocal_reps.sols"), np.array(reps), hdr)
     fixtures.write_params(fixtures.fixture_path("trifocal_p0.params"), p0, hdr)
 
 
+def make_fivepoint(max_loops: int = 40, stall_loops: int = 5, seed: int = rng.SEED_FIVEPOINT_MONODROMY):
+    """5-point relative pose + depth (reading R24) monodromy with the q -> -q symmetry."""
+    d = systems.fivepoint_relpose_depth()
+    p0, x0 = rng.fivepoint_complex_start(seed)
+    reps, full, loops = _monodromy(d, p0, x0, systems.fivepoint_symmetry, seed, max_loops, stall_loops, "5pt")
+    hdr = (f"5-point relative pose + depth start solutions at the planted complex p0 = rng.fivepoint_complex_start({seed}).\n"
+           f"Written by scripts/make_fixtures.py (oracle only): symmetry-aware monodromy, {loops} loops,\n"
+           f"{len(reps)} orbits x 2 = {full.shape[0]} solutions (PAPER.md Table 2 P:492 reports 160; reading R24).")
+    fixtures.write_solutions(fixtures.fixture_path("fivepoint_start.sols"), full, hdr)
+    fixtures.write_params(fixtures.fixture_path("fivepoint_p0.params"), p0, hdr)
+
+
 if __name__ == "__main__":
     oracle.build()
-    what = sys.argv[1:] or ["fourview", "trifocal"]
+    what = sys.argv[1:] or ["fourview", "trifocal", "fivepoint"]
     if "fourview" in what:
         make_fourview()
     if "trifocal" in what:
         make_trifocal()
+    if "fivepoint" in what:
+        make_fivepoint()

@@ -227,6 +227,39 @@ def test_trifocal_ph_parity_sampled(hc, orc):
     assert close.mean() >= 0.97
 
 
+def test_fivepoint_ph_parity(hc, orc):
+    """N2 workload (5-point relative pose + depth, 16x16, reading R24): 40 starts (oracle monodromy
+    fixture) -> planted real instances; GPU and oracle sets identical (R21), planted ground truth
+    and its q -> -q image recovered."""
+    d = systems.fivepoint_relpose_depth()
+    start = fixtures.read_solutions(fixtures.fixture_path("fivepoint_start.sols"))
+    p0 = fixtures.read_params(fixtures.fixture_path("fivepoint_p0.params"))
+    assert start.shape == (40, 16)
+    B = 8
+    p1s, xs = rng.fivepoint_batch(B)
+    res = run_ph(hc, d, start, p0, p1s)
+    ref = orc.track(orc.ph_homotopy(d, p0), start, p1s=p1s)
+    for b in range(B):
+        A = orc.dedup(ref.x[b][ref.status[b] == 0])[0]
+        G = gpu_set(orc, res, b)
+        assert_same_set_r21(orc, d, p1s[b], A, G, f"5-point instance {b}")
+        for y in systems.fivepoint_symmetry(xs[b]):
+            assert np.min(np.max(np.abs(G - y), axis=1)) < 1e-8
+
+
+def test_monodromy_fivepoint_matches_oracle_fixture(hc, orc):
+    """GPU monodromy (q -> -q symmetry) from the planted complex start reproduces the oracle's 40."""
+    from paper_2112_03444_b200.monodromy import monodromy_solve
+    d = systems.fivepoint_relpose_depth()
+    p0, x0 = rng.fivepoint_complex_start()
+    fix = fixtures.read_solutions(fixtures.fixture_path("fivepoint_start.sols"))
+    assert np.array_equal(fixtures.read_params(fixtures.fixture_path("fivepoint_p0.params")), p0)
+    s = hc.System(d, device=0)
+    res = monodromy_solve(s, x0, p0, symmetry=systems.fivepoint_symmetry, seed=5, stall_loops=5)
+    assert res.solutions.shape[0] == 40, res.history
+    assert_same_set_r21(orc, d, p0, fix, res.solutions, "5-point monodromy")
+
+
 # ------------------------------------------------------------------ edge cases
 
 def _linear_plus_quadratic(n, nq, seed):

@@ -19,6 +19,7 @@ SYSTEMS = {
     "cyclic-5": lambda: systems.cyclic(5),
     "4-view": lambda: systems.nview_triangulation(4),
     "trifocal": lambda: systems.trifocal_unknown_f(),
+    "5pt-relpose": lambda: systems.fivepoint_relpose_depth(),
     "univ-param": lambda: systems.univariate_param(5),
 }
 
@@ -350,3 +351,76 @@ def test_two_view_triangulation_six(orc):
     td8 = _frozen(d, rng.complex_normal(rng.gen(102), d.n_params))
     res8 = orc.track(orc.td_homotopy(td8, rng.gamma(0)), orc.td_start(td8.degrees()))
     assert len(orc.dedup(orc.finite_solutions(res8))[0]) == 8
+
+
+# ---------------------------------------------------------------- 5-point relative pose + depth (N2, R24)
+
+def _essential(x):
+    """E = [T]_x R(q) of a 5-point solution vector (numpy, independent of both evaluators)."""
+    R = np.array(systems.quat_rot(*x[10:14]))
+    return rng.skew(np.array([x[14], x[15], 1.0])) @ R
+
+
+def test_fivepoint_planted_is_exact(orc):
+    """Planted ground truth: F(x_gt; p) ~ 0 (oracle and the defining-sum evaluator) for generated
+    instances and the complex monodromy start; q -> -q maps solutions to solutions."""
+    d = systems.fivepoint_relpose_depth()
+    assert (d.n_vars, d.n_params) == (16, 20)
+    for b in range(5):
+        p, x = rng.fivepoint_instance(rng.SEED_FIVEPOINT_INSTANCE + b)
+        assert np.all(p.imag == 0)
+        for y in systems.fivepoint_symmetry(x):
+            assert np.max(np.abs(orc.eval_F(d, p, y))) < 1e-13
+    p0, x0 = rng.fivepoint_complex_start()
+    assert np.max(np.abs(orc.eval_F(d, p0, x0))) < 1e-12
+
+
+def test_fivepoint_forty_solutions_ten_essentials(orc):
+    """The oracle's monodromy fixture against the 5-point theory: the 40 solutions at p0 solve the
+    equations (defining sums), and their essential matrices E = [T]_x R fall into exactly 10 classes
+    up to scale -- the 10 roots of the classical tenth-order polynomial -- with 4
+    solutions each (q -> -q times the twisted pair); every E is essential (det E = 0,
+    2 E E^T E - tr(E E^T) E = 0) and satisfies the five epipolar constraints gb^T E g = 0."""
+    from hc_inputs import fixtures
+    d = systems.fivepoint_relpose_depth()
+    X = fixtures.read_solutions(fixtures.fixture_path("fivepoint_start.sols"))
+    p0 = fixtures.read_params(fixtures.fixture_path("fivepoint_p0.params"))
+    assert X.shape == (40, 16)
+    for x in X[:8]:
+        assert max(abs(eval_poly(f, x, p0)) for f in d.polys) < 1e-9
+    Es = []
+    for x in X:
+        E = _essential(x)
+        E = E / E.flat[np.argmax(np.abs(E))]
+        assert abs(np.linalg.det(E)) < 1e-9
+        assert np.max(np.abs(2 * E @ E.T @ E - np.trace(E @ E.T) * E)) < 1e-8
+        for i in range(5):
+            g = np.array([p0[systems.fivepoint_param_index(0, i, 0)], p0[systems.fivepoint_param_index(0, i, 1)], 1])
+            gb = np.array([p0[systems.fivepoint_param_index(1, i, 0)], p0[systems.fivepoint_param_index(1, i, 1)], 1])
+            assert abs(gb @ E @ g) < 1e-9
+        Es.append(E.reshape(-1))
+    Es = np.array(Es)
+    classes = []
+    for e in Es:
+        for c in classes:
+            if np.max(np.abs(c[0] - e)) < 1e-7:
+                c.append(e)
+                break
+        else:
+            classes.append([e])
+    assert len(classes) == 10 and all(len(c) == 4 for c in classes)
+
+
+def test_fivepoint_planted_recovered_by_tracking(orc):
+    """Parameter homotopy from the 40 fixture starts to planted real instances reaches the planted
+    ground truth (and its q -> -q image)."""
+    from hc_inputs import fixtures
+    d = systems.fivepoint_relpose_depth()
+    X = fixtures.read_solutions(fixtures.fixture_path("fivepoint_start.sols"))
+    p0 = fixtures.read_params(fixtures.fixture_path("fivepoint_p0.params"))
+    p1s, xs = rng.fivepoint_batch(3)
+    res = orc.track(orc.ph_homotopy(d, p0), X, p1s)
+    for b in range(3):
+        S = res.x[b][res.status[b] == orc.CONVERGED]
+        for y in systems.fivepoint_symmetry(xs[b]):
+            assert np.min(np.max(np.abs(S - y), axis=1)) < 1e-8
