@@ -167,6 +167,18 @@ def run_reference(args):
 
 # ------------------------------------------------------------------------------ our arm
 
+def traffic_bytes(config: str, B: int, S: int):
+    """DRAM bytes (read + write) per launch of the tracker kernel for this exact workload, as
+    captured by ncu (dram__bytes_read.sum + dram__bytes_write.sum) and recorded in
+    profiles/traffic.json by scripts/record_traffic.py; None when no capture of this shape exists."""
+    try:
+        rec = json.load(open(os.path.join(ROOT, "profiles", "traffic.json")))
+    except (OSError, ValueError):
+        return None
+    e = rec.get(f"{config}:{B}x{S}")
+    return None if e is None else e.get("bytes")
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
@@ -229,8 +241,13 @@ def run_ours(args):
     barrier()
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
     e0.record(stream)
-    results = [step() for _ in range(args.steps)]
+    results = []
+    for i in range(args.steps):
+        ev[i].record(stream)
+        results.append(step())
+    ev[-1].record(stream)
     e1.record(stream)
     torch.cuda.synchronize()
     barrier()
@@ -240,6 +257,7 @@ def run_ours(args):
     if distributed:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     elapsed_max = float(t.item())
+    step_ms = [ev[i].elapsed_time(ev[i + 1]) for i in range(args.steps)]   # this rank, per step
     launch = results[0].launch()
     per_launch = [r.elapsed_ms() for r in results]   # (total, prologue, tracker) events on the launch stream
     tracker_ms = statistics.mean(p[2] for p in per_launch)
@@ -313,7 +331,7 @@ def run_ours(args):
                        "warmup_instances": wb,
                        "launch": launch},
             "roofline": {"bound": "alu", "achieved": achieved, "peak": peak_max, "unit": "TFLOP/s",
-                         "frac": achieved / peak_max, "traffic": None,
+                         "frac": achieved / peak_max, "traffic": traffic_bytes(args.config, B, S),
                          "kernel": "hcb::hc_track_kernel<%d>" % N,
                          "peak_note": "FP64 vector: 148 SM x 64 DFMA/clk x 2 x 1965 MHz (derived, DESIGN.md); "
                                       "frac at the measured median clock: %.3f" %
@@ -323,6 +341,8 @@ def run_ours(args):
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": 2 * args.steps,
             "clocks": ck, "converged_fraction": converged / (B * S), "gather_ms": gather_ms,
             "solves_per_track": solves / (B * S),
+            "step_ms": {"median": statistics.median(step_ms), "p10": float(np.percentile(step_ms, 10)),
+                        "p90": float(np.percentile(step_ms, 90)), "n": len(step_ms)},
         }
         print(json.dumps(line), flush=True)
     if distributed:

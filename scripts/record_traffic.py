@@ -1,0 +1,62 @@
+"""Capture the tracker kernel's DRAM traffic per launch with ncu for one bench workload.
+
+  python scripts/record_traffic.py <config> <instances> [out.json]
+
+Runs `bench.py --config C --instances B --steps 1 --warmup 3` under
+`ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum`, restricted to the
+first full-batch launch of hc_track_kernel (the 3 warm-up launches are skipped), and merges
+{"<config>:<B>x<S>": {"bytes": read + write, ...}} into out.json (default gpurun_out/traffic.json;
+the committed copy is profiles/traffic.json, read by bench.py for roofline.traffic).
+"""
+import csv
+import io
+import json
+import os
+import subprocess
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def main():
+    cfg, B = sys.argv[1], int(sys.argv[2])
+    out = sys.argv[3] if len(sys.argv) > 3 else os.path.join(ROOT, "gpurun_out", "traffic.json")
+    cmd = ["ncu", "--metrics", "dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum",
+           "--clock-control", "none", "-k", "regex:hc_track_kernel", "--launch-skip", "3", "-c", "1", "--csv",
+           sys.executable, os.path.join(ROOT, "bench.py"), "--config", cfg, "--instances", str(B), "--steps", "1",
+           "--warmup", "3", "--no-cpu-baseline", "--no-e2e"]
+    p = subprocess.run(cmd, capture_output=True, text=True, cwd=ROOT)
+    txt = p.stdout
+    bench_line = None
+    rows = []
+    for line in txt.splitlines():
+        if line.startswith("{"):
+            bench_line = json.loads(line)
+        elif line.startswith('"'):
+            rows.append(line)
+    vals = {}
+    kernel = None
+    for r in csv.DictReader(io.StringIO("\n".join(rows))):
+        name, unit, v = r["Metric Name"], r["Metric Unit"], float(r["Metric Value"].replace(",", ""))
+        scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12,
+                 "nsecond": 1e-9, "usecond": 1e-6, "msecond": 1e-3, "second": 1.0}.get(unit, 1.0)
+        vals[name] = v * scale
+        kernel = r["Kernel Name"]
+    if bench_line is None or "dram__bytes_read.sum" not in vals:
+        sys.stderr.write(p.stdout[-3000:] + p.stderr[-3000:])
+        raise SystemExit("ncu capture failed")
+    S = bench_line["config"]["tracks_per_instance"]
+    key = f"{cfg}:{B}x{S}"
+    rec = json.load(open(out)) if os.path.exists(out) else {}
+    rec[key] = {"bytes": vals["dram__bytes_read.sum"] + vals["dram__bytes_write.sum"],
+                "read": vals["dram__bytes_read.sum"], "write": vals["dram__bytes_write.sum"],
+                "kernel_s_under_ncu": vals.get("gpu__time_duration.sum"), "kernel": kernel,
+                "tracks": B * S, "source": "ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum "
+                                          "(scripts/record_traffic.py), first full-batch launch"}
+    os.makedirs(os.path.dirname(out), exist_ok=True)
+    json.dump(rec, open(out, "w"), indent=1)
+    print(key, rec[key])
+
+
+if __name__ == "__main__":
+    main()
