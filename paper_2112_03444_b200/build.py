@@ -31,6 +31,9 @@ if VARIANT == "timing":
     FLAGS = FLAGS + ["-DHCB_PHASE_TIMING"]
 elif VARIANT == "hybrid":   # experiment: 16-lane hybrid layout for N = 17, 18 (csrc/hc_internal.h)
     FLAGS = FLAGS + ["-DHCB_HYBRID_LAYOUT=1"]
+# any variant may add preprocessor switches for A/B experiments, e.g.
+# HCB_VARIANT=w16 HCB_DEFINES="HCB_MAXW_MID=16" (see the #ifndef switches in kernels/tracker.cuh)
+FLAGS = FLAGS + ["-D" + d for d in os.environ.get("HCB_DEFINES", "").split()] if VARIANT else FLAGS
 
 
 def sources():

@@ -45,13 +45,19 @@ constexpr unsigned FULL = 0xffffffffu;
 //   2 CTAs.  The launcher shrinks the CTA when the shared memory does not fit.
 //   Hybrid layout (hy_layout(N), 16-lane tracks with column-distributed extra rows): one 8-warp CTA
 //   (16 tracks; shared memory bound).
+#ifndef HCB_MAXW_MID   // warps per CTA for 15 <= N <= 20 (A/B experiments override it)
+#define HCB_MAXW_MID 12
+#endif
+#ifndef HCB_OPS_PIPE   // op list: prefetch the next block's op records (A/B switch)
+#define HCB_OPS_PIPE 1
+#endif
 template <int N>
 struct TrackerShape {
   static constexpr bool HY = hy_layout(N);
   static constexpr int L = lanes_for(N);
   static constexpr int E = HY ? N - 16 : 0;   // extra rows (hybrid layout)
   static constexpr int NC = HY ? 2 : 1;       // unknown components per lane
-  static constexpr int MAXW = HY ? 8 : (N >= 15 && N <= 20) ? 12 : 4;
+  static constexpr int MAXW = HY ? 8 : (N >= 15 && N <= 20) ? HCB_MAXW_MID : 4;
   static constexpr int MINB = (N <= 14) ? 4 : (N <= 20) ? 1 : 2;
 };
 
@@ -475,7 +481,32 @@ __device__ __forceinline__ void run_ops(const uint2 *__restrict__ ops_s, int Q, 
   double2 acc = make_double2(0.0, 0.0), acc2 = make_double2(0.0, 0.0);
   double acc_abs = 0.0;
   int q = 0;
-  for (; q + 4 <= Q; q += 4) {
+  // software pipeline over blocks of 4 ops: the records of block b+1 and the operands of block b
+  // are loaded before block b's FMAs and stores, so each block waits for at most one shared-memory
+  // round trip that the previous block's work has not already covered
+  const int QB = Q & ~3;
+  if (HCB_OPS_PIPE && QB > 0) {
+    uint2 op[4], nop[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) op[i] = ops_s[i * L + r];
+    for (; q < QB; q += 4) {
+      double2 c[4], m[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        c[i] = cval[(int)(op[i].x & 0xFFFFu) + (((op[i].y >> 16) & OP_RHS) ? rhs_off : 0)];
+        m[i] = mono[op[i].x >> 16];
+      }
+      if (q + 4 < QB) {
+#pragma unroll
+        for (int i = 0; i < 4; ++i) nop[i] = ops_s[(q + 4 + i) * L + r];
+      }
+#pragma unroll
+      for (int i = 0; i < 4; ++i) op_accumulate<N, ABS>(op[i], c[i], m[i], acc, acc2, acc_abs, M, rabs, row_of);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) op[i] = nop[i];
+    }
+  }
+  for (; q + 4 <= Q; q += 4) {   // (HCB_OPS_PIPE == 0) records and operands of one block, then its FMAs
     uint2 op[4];
     double2 c[4], m[4];
 #pragma unroll
