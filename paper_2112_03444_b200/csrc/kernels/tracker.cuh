@@ -48,8 +48,11 @@ constexpr unsigned FULL = 0xffffffffu;
 #ifndef HCB_MAXW_MID   // warps per CTA for 15 <= N <= 20 (A/B experiments override it)
 #define HCB_MAXW_MID 12
 #endif
-#ifndef HCB_OPS_PIPE   // op list: prefetch the next block's op records (A/B switch)
-#define HCB_OPS_PIPE 1
+#ifndef HCB_ROWS_ALL   // elimination: every lane keeps its row in shared memory (A/B switch, see lu_rows)
+#define HCB_ROWS_ALL 1
+#endif
+#ifndef HCB_JMAX_OPS_MIN_N   // N from which the op stores (not the row load) produce max |A_ij|^2
+#define HCB_JMAX_OPS_MIN_N 1
 #endif
 template <int N>
 struct TrackerShape {
@@ -59,6 +62,7 @@ struct TrackerShape {
   static constexpr int NC = HY ? 2 : 1;       // unknown components per lane
   static constexpr int MAXW = HY ? 8 : (N >= 15 && N <= 20) ? HCB_MAXW_MID : 4;
   static constexpr int MINB = (N <= 14) ? 4 : (N <= 20) ? 1 : 2;
+  static constexpr bool JMAX_OPS = (N >= HCB_JMAX_OPS_MIN_N);
 };
 
 __device__ __forceinline__ double2 cmul(double2 a, double2 b) {
@@ -205,9 +209,15 @@ __device__ __forceinline__ int seg_argmax(double v, int r, double &vmax) {
 // Returns the solution component y_r in lane r and a slot-uniform success flag.
 // prow: 2 * (N + 1) double2; pl: N bytes (per slot shared memory).
 // ------------------------------------------------------------------------------------------
-template <int N, int L>
+// ROWS (tracker, HCB_ROWS_ALL): instead of the pivot lane publishing its row once the arg-max has
+// named it, every lane keeps its own row's trailing columns in rows[r * (N + 1) + j] (stored right
+// after its update, off the arg-max -> load chain), and the readers load row p directly.  The same
+// number of store instructions (all lanes active instead of one), one __syncwarp per column; a
+// lane's stored values change only when it is not the pivot, and row p is only read after the
+// column's __syncwarp, so no double buffer is needed.
+template <int N, int L, bool ROWS = false>
 __device__ __forceinline__ bool lu_rows(double2 (&a)[N + 1], int r, int seg, double2 *prow, uint8_t *pl,
-                                        double pivot_rel, double lane_max, double2 &y) {
+                                        double pivot_rel, double lane_max, double2 &y, double2 *rows = nullptr) {
   bool used = (r >= N);
   int mystep = used ? N : -1;
   double2 myinv = make_double2(0.0, 0.0);
@@ -221,16 +231,26 @@ __device__ __forceinline__ bool lu_rows(double2 (&a)[N + 1], int r, int seg, dou
   if (!(v0 >= 0.0)) v0 = -1.0;   // NaN is never a pivot
   int p = seg_argmax_thr<L>(v0, r, thr, sing);
   double2 spec = crecip(a[0]);   // speculative 1/a_rk of this lane's candidate (overlaps the search)
+  double2 *myrow = rows + (r < N ? r : 0) * (N + 1);
+  if constexpr (ROWS) {
+    __syncwarp();   // the row buffer aliases the evaluation's scratch that other lanes may still read
+    if (r < N) {
+#pragma unroll
+      for (int j = 2; j <= N; ++j) myrow[j] = a[j];
+    }
+  }
 #pragma unroll
   for (int k = 0; k < N; ++k) {
-    double2 *pr = prow + (k & 1) * (N + 1);
+    double2 *pr = ROWS ? rows + p * (N + 1) : prow + (k & 1) * (N + 1);
     // early broadcast from the pivot lane by shuffles: 1/pivot and the pivot row's column k+1
     const double2 inv = shfl2(spec, p, L);
     const double2 u1 = shfl2(a[k + 1], p, L);
     const bool me = (r == p);
     if (me) {   // the pivot lane publishes the rest of its row (columns k+2..N) through shared memory
+      if constexpr (!ROWS) {
 #pragma unroll
-      for (int j = k + 2; j <= N; ++j) pr[j] = a[j];
+        for (int j = k + 2; j <= N; ++j) pr[j] = a[j];
+      }
       used = true;
       mystep = k;
       myinv = spec;
@@ -258,6 +278,13 @@ __device__ __forceinline__ bool lu_rows(double2 (&a)[N + 1], int r, int seg, dou
 #pragma unroll
         for (int i = 0; i < 4; ++i)
           if (j0 + i <= N) a[j0 + i] = cfms(a[j0 + i], l, u[i]);
+        if constexpr (ROWS) {   // columns k+3..N of the updated row, for the next column's readers
+          if (r < N && k + 2 < N) {
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+              if (j0 + i >= k + 3 && j0 + i <= N) myrow[j0 + i] = a[j0 + i];
+          }
+        }
       }
     }
   }
@@ -451,8 +478,8 @@ __device__ __forceinline__ bool lu_rows_hy(double2 (&a)[N + 1], double2 (&e)[E][
 // the previous op's same-part accumulator (chain of 1).
 template <int N, bool ABS>
 __device__ __forceinline__ void op_accumulate(uint2 op, double2 c, double2 m, double2 &acc, double2 &acc2,
-                                              double &acc_abs, double2 *__restrict__ M, double *__restrict__ rabs,
-                                              const int16_t *row_of) {
+                                              double &acc_abs, double &jm, double2 *__restrict__ M,
+                                              double *__restrict__ rabs, const int16_t *row_of) {
   const uint32_t fl = op.y >> 16;
   if (ABS) acc_abs += sqrt(abs2(cmul(c, m)));
   acc.x = fma(c.x, m.x, acc.x);
@@ -461,7 +488,9 @@ __device__ __forceinline__ void op_accumulate(uint2 op, double2 c, double2 m, do
   acc2.y = fma(c.y, m.x, acc2.y);
   if (fl & OP_LAST) {
     const uint32_t dest = op.y & 0xFFFFu;
-    M[dest] = make_double2(acc.x + acc2.x, acc.y + acc2.y);
+    const double2 v = make_double2(acc.x + acc2.x, acc.y + acc2.y);
+    M[dest] = v;
+    if (TrackerShape<N>::JMAX_OPS && !(fl & OP_RHS)) jm = fmax(jm, abs2(v));   // max |A_ij|^2 (R9); NaN ignored
     if (ABS && (fl & OP_RHS)) rabs[row_of[dest]] = acc_abs;
     acc = make_double2(0.0, 0.0);
     acc2 = make_double2(0.0, 0.0);
@@ -477,36 +506,11 @@ template <int N, int L, bool ABS>
 __device__ __forceinline__ void run_ops(const uint2 *__restrict__ ops_s, int Q, int rhs_off,
                                         const double2 *__restrict__ cval, const double2 *__restrict__ mono,
                                         double2 *__restrict__ M, double *__restrict__ rabs, const int16_t *row_of,
-                                        int r) {
+                                        int r, double &jm) {
   double2 acc = make_double2(0.0, 0.0), acc2 = make_double2(0.0, 0.0);
   double acc_abs = 0.0;
   int q = 0;
-  // software pipeline over blocks of 4 ops: the records of block b+1 and the operands of block b
-  // are loaded before block b's FMAs and stores, so each block waits for at most one shared-memory
-  // round trip that the previous block's work has not already covered
-  const int QB = Q & ~3;
-  if (HCB_OPS_PIPE && QB > 0) {
-    uint2 op[4], nop[4];
-#pragma unroll
-    for (int i = 0; i < 4; ++i) op[i] = ops_s[i * L + r];
-    for (; q < QB; q += 4) {
-      double2 c[4], m[4];
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        c[i] = cval[(int)(op[i].x & 0xFFFFu) + (((op[i].y >> 16) & OP_RHS) ? rhs_off : 0)];
-        m[i] = mono[op[i].x >> 16];
-      }
-      if (q + 4 < QB) {
-#pragma unroll
-        for (int i = 0; i < 4; ++i) nop[i] = ops_s[(q + 4 + i) * L + r];
-      }
-#pragma unroll
-      for (int i = 0; i < 4; ++i) op_accumulate<N, ABS>(op[i], c[i], m[i], acc, acc2, acc_abs, M, rabs, row_of);
-#pragma unroll
-      for (int i = 0; i < 4; ++i) op[i] = nop[i];
-    }
-  }
-  for (; q + 4 <= Q; q += 4) {   // (HCB_OPS_PIPE == 0) records and operands of one block, then its FMAs
+  for (; q + 4 <= Q; q += 4) {
     uint2 op[4];
     double2 c[4], m[4];
 #pragma unroll
@@ -517,12 +521,12 @@ __device__ __forceinline__ void run_ops(const uint2 *__restrict__ ops_s, int Q, 
       m[i] = mono[op[i].x >> 16];
     }
 #pragma unroll
-    for (int i = 0; i < 4; ++i) op_accumulate<N, ABS>(op[i], c[i], m[i], acc, acc2, acc_abs, M, rabs, row_of);
+    for (int i = 0; i < 4; ++i) op_accumulate<N, ABS>(op[i], c[i], m[i], acc, acc2, acc_abs, jm, M, rabs, row_of);
   }
   for (; q < Q; ++q) {
     const uint2 o = ops_s[q * L + r];
     const double2 c = cval[(int)(o.x & 0xFFFFu) + (((o.y >> 16) & OP_RHS) ? rhs_off : 0)];
-    op_accumulate<N, ABS>(o, c, mono[o.x >> 16], acc, acc2, acc_abs, M, rabs, row_of);
+    op_accumulate<N, ABS>(o, c, mono[o.x >> 16], acc, acc2, acc_abs, jm, M, rabs, row_of);
   }
 }
 
@@ -630,8 +634,11 @@ __device__ __forceinline__ bool eval_solve(const TrackArgs &A, const uint2 *__re
   HCB_T(c2);
   HCB_ACC(1, c1, c2);
   // ---- homogenised term evaluation, lane-balanced op list ----
-  if (want_abs) run_ops<N, L, true>(ops_s, A.Q, rhs_off, cval, mono, M, rabs, row_of, r);
-  else run_ops<N, L, false>(ops_s, A.Q, rhs_off, cval, mono, M, rabs, row_of, r);
+  // jmax: max |A_ij|^2 over the Jacobian entries this lane stored (the elimination takes the maximum
+  // over the track's lanes for the singularity threshold, R9)
+  double jmax = 0.0;
+  if (want_abs) run_ops<N, L, true>(ops_s, A.Q, rhs_off, cval, mono, M, rabs, row_of, r, jmax);
+  else run_ops<N, L, false>(ops_s, A.Q, rhs_off, cval, mono, M, rabs, row_of, r, jmax);
   __syncwarp();
   HCB_T(c3);
   HCB_ACC(2, c2, c3);
@@ -639,19 +646,14 @@ __device__ __forceinline__ bool eval_solve(const TrackArgs &A, const uint2 *__re
   if constexpr (NC == 2) {
     // hybrid layout: row r plus the extra rows' columns r and r + 16
     double2 a[N + 1], e[E][2];
-    double jmax = 0.0;
 #pragma unroll
-    for (int j = 0; j <= N; ++j) {
-      a[j] = M[mpos_s[r * (N + 1) + j]];
-      if (j < N) jmax = fmax(jmax, abs2(a[j]));
-    }
+    for (int j = 0; j <= N; ++j) a[j] = M[mpos_s[r * (N + 1) + j]];
 #pragma unroll
     for (int q = 0; q < E; ++q)
 #pragma unroll
       for (int c = 0; c < 2; ++c) {
         const int col = r + 16 * c;
         e[q][c] = (col <= N) ? M[mpos_s[(16 + q) * (N + 1) + col]] : make_double2(0.0, 0.0);
-        if (col < N) jmax = fmax(jmax, abs2(e[q][c]));
       }
     fr[0] = a[N];
     fr[NC - 1] = (r < E) ? M[mpos_s[(16 + (r < E ? r : 0)) * (N + 1) + N]] : make_double2(0.0, 0.0);
@@ -666,14 +668,13 @@ __device__ __forceinline__ bool eval_solve(const TrackArgs &A, const uint2 *__re
   }
   double2 a[N + 1];
   const int rr = (r < N) ? r : 0;
-  double jmax = 0.0;   // max |A_rj|^2 of this row, for the singularity threshold (R9)
 #pragma unroll
   for (int j = 0; j <= N; ++j) {
     a[j] = M[mpos_s[rr * (N + 1) + j]];
-    if (j < N) jmax = fmax(jmax, abs2(a[j]));
+    if (!TrackerShape<N>::JMAX_OPS && j < N) jmax = fmax(jmax, abs2(a[j]));
   }
   if (r >= N) {
-    jmax = 0.0;
+    if (!TrackerShape<N>::JMAX_OPS) jmax = 0.0;
 #pragma unroll
     for (int j = 0; j <= N; ++j) a[j] = make_double2(0.0, 0.0);
   }
@@ -681,7 +682,7 @@ __device__ __forceinline__ bool eval_solve(const TrackArgs &A, const uint2 *__re
   fabs_r[0] = (r < N && want_abs) ? rabs[r] : 0.0;
   HCB_T(c4);
   HCB_ACC(3, c3, c4);
-  const bool ok = lu_rows<N, L>(a, r, seg, prow, pl, A.st.pivot_rel, jmax, y[0]);
+  const bool ok = lu_rows<N, L, HCB_ROWS_ALL != 0>(a, r, seg, prow, pl, A.st.pivot_rel, jmax, y[0], mono);
   HCB_T(c5);
   HCB_ACC(4, c4, c5);
   return ok;
@@ -721,7 +722,7 @@ __global__ void __launch_bounds__(TrackerShape<N>::MAXW * 32, TrackerShape<N>::M
   double2 *cval = reinterpret_cast<double2 *>(sb);
   double2 *mono = cval + ncoef + A.ncoef_src;
   double2 *M = mono + A.n_mono;
-  double2 *prow = M + A.n_entries + 1;
+  double2 *prow = mono + scratch_c128(N, A.n_mono, A.n_entries + 1);   // mono + M, or the LU row buffer
   double *rabs = reinterpret_cast<double *>(prow + 2 * (N + 1));
   uint8_t *pl = reinterpret_cast<uint8_t *>(rabs + N);
   if (r == 0) {

@@ -1,0 +1,4 @@
+set -x
+python -c "import __graft_entry__ as g; g.build()" 2>&1 | tail -1
+bash scripts/gpu_ab.sh lib_base lib_rows0 lib lib_base lib
+timeout 1200 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; tail -3 gpurun_out/pytest_gpu.log

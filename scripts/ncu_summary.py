@@ -29,6 +29,19 @@ for key in ["dram__bytes_read.sum", "dram__bytes_write.sum", "sm__pipe_fp64_cycl
     for i, h in enumerate(rr[0]):
         if key in h:
             print(f"{h:70s} {rr[2][i]:>16s} {rr[1][i]}")
+# warp-state (stall reason) breakdown from the PC sampler: share of samples per reason
+stall = []
+for i, h in enumerate(rr[0]):
+    if h.startswith("smsp__pcsamp_warps_issue_stalled_") and not h.endswith("_not_issued"):
+        try:
+            stall.append((float(rr[2][i].replace(",", "")), h[len("smsp__pcsamp_warps_issue_stalled_"):]))
+        except ValueError:
+            pass
+tot_st = sum(v for v, _ in stall)
+if tot_st > 0:
+    print("\nstall reasons (PC sampling, share of samples)")
+    for v, n in sorted(stall, reverse=True)[:12]:
+        print(f"  {n:28s} {100 * v / tot_st:5.1f}%")
 src = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "cuda,sass"],
                      capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(src)))
