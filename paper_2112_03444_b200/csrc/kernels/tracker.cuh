@@ -51,9 +51,6 @@ constexpr unsigned FULL = 0xffffffffu;
 #ifndef HCB_ROWS_ALL   // elimination: every lane keeps its row in shared memory (A/B switch, see lu_rows)
 #define HCB_ROWS_ALL 1
 #endif
-#ifndef HCB_JMAX_OPS_MIN_N   // N from which the op stores (not the row load) produce max |A_ij|^2
-#define HCB_JMAX_OPS_MIN_N 1
-#endif
 template <int N>
 struct TrackerShape {
   static constexpr bool HY = hy_layout(N);
@@ -62,7 +59,6 @@ struct TrackerShape {
   static constexpr int NC = HY ? 2 : 1;       // unknown components per lane
   static constexpr int MAXW = HY ? 8 : (N >= 15 && N <= 20) ? HCB_MAXW_MID : 4;
   static constexpr int MINB = (N <= 14) ? 4 : (N <= 20) ? 1 : 2;
-  static constexpr bool JMAX_OPS = (N >= HCB_JMAX_OPS_MIN_N);
 };
 
 __device__ __forceinline__ double2 cmul(double2 a, double2 b) {
@@ -478,8 +474,8 @@ __device__ __forceinline__ bool lu_rows_hy(double2 (&a)[N + 1], double2 (&e)[E][
 // the previous op's same-part accumulator (chain of 1).
 template <int N, bool ABS>
 __device__ __forceinline__ void op_accumulate(uint2 op, double2 c, double2 m, double2 &acc, double2 &acc2,
-                                              double &acc_abs, double &jm, double2 *__restrict__ M,
-                                              double *__restrict__ rabs, const int16_t *row_of) {
+                                              double &acc_abs, double2 *__restrict__ M, double *__restrict__ rabs,
+                                              const int16_t *row_of) {
   const uint32_t fl = op.y >> 16;
   if (ABS) acc_abs += sqrt(abs2(cmul(c, m)));
   acc.x = fma(c.x, m.x, acc.x);
@@ -488,9 +484,7 @@ __device__ __forceinline__ void op_accumulate(uint2 op, double2 c, double2 m, do
   acc2.y = fma(c.y, m.x, acc2.y);
   if (fl & OP_LAST) {
     const uint32_t dest = op.y & 0xFFFFu;
-    const double2 v = make_double2(acc.x + acc2.x, acc.y + acc2.y);
-    M[dest] = v;
-    if (TrackerShape<N>::JMAX_OPS && !(fl & OP_RHS)) jm = fmax(jm, abs2(v));   // max |A_ij|^2 (R9); NaN ignored
+    M[dest] = make_double2(acc.x + acc2.x, acc.y + acc2.y);
     if (ABS && (fl & OP_RHS)) rabs[row_of[dest]] = acc_abs;
     acc = make_double2(0.0, 0.0);
     acc2 = make_double2(0.0, 0.0);
@@ -506,7 +500,7 @@ template <int N, int L, bool ABS>
 __device__ __forceinline__ void run_ops(const uint2 *__restrict__ ops_s, int Q, int rhs_off,
                                         const double2 *__restrict__ cval, const double2 *__restrict__ mono,
                                         double2 *__restrict__ M, double *__restrict__ rabs, const int16_t *row_of,
-                                        int r, double &jm) {
+                                        int r) {
   double2 acc = make_double2(0.0, 0.0), acc2 = make_double2(0.0, 0.0);
   double acc_abs = 0.0;
   int q = 0;
@@ -521,12 +515,12 @@ __device__ __forceinline__ void run_ops(const uint2 *__restrict__ ops_s, int Q, 
       m[i] = mono[op[i].x >> 16];
     }
 #pragma unroll
-    for (int i = 0; i < 4; ++i) op_accumulate<N, ABS>(op[i], c[i], m[i], acc, acc2, acc_abs, jm, M, rabs, row_of);
+    for (int i = 0; i < 4; ++i) op_accumulate<N, ABS>(op[i], c[i], m[i], acc, acc2, acc_abs, M, rabs, row_of);
   }
   for (; q < Q; ++q) {
     const uint2 o = ops_s[q * L + r];
     const double2 c = cval[(int)(o.x & 0xFFFFu) + (((o.y >> 16) & OP_RHS) ? rhs_off : 0)];
-    op_accumulate<N, ABS>(o, c, mono[o.x >> 16], acc, acc2, acc_abs, jm, M, rabs, row_of);
+    op_accumulate<N, ABS>(o, c, mono[o.x >> 16], acc, acc2, acc_abs, M, rabs, row_of);
   }
 }
 
@@ -588,6 +582,10 @@ __device__ __forceinline__ bool eval_solve(const TrackArgs &A, const uint2 *__re
   HCB_T(c0);
   constexpr int E = TrackerShape<N>::E;
   if (r < N) mono[r] = xr[0];
+  if (HCB_ROWS_ALL && r == 0) {   // the elimination's row buffer overwrote the constants of the scratch
+    mono[N] = make_double2(1.0, 0.0);            // constant-one slot
+    M[A.n_entries] = make_double2(0.0, 0.0);     // the entry every structural zero reads
+  }
   if constexpr (NC == 2) {
     if (r < E) mono[16 + r] = xr[NC - 1];
   }
@@ -634,11 +632,8 @@ __device__ __forceinline__ bool eval_solve(const TrackArgs &A, const uint2 *__re
   HCB_T(c2);
   HCB_ACC(1, c1, c2);
   // ---- homogenised term evaluation, lane-balanced op list ----
-  // jmax: max |A_ij|^2 over the Jacobian entries this lane stored (the elimination takes the maximum
-  // over the track's lanes for the singularity threshold, R9)
-  double jmax = 0.0;
-  if (want_abs) run_ops<N, L, true>(ops_s, A.Q, rhs_off, cval, mono, M, rabs, row_of, r, jmax);
-  else run_ops<N, L, false>(ops_s, A.Q, rhs_off, cval, mono, M, rabs, row_of, r, jmax);
+  if (want_abs) run_ops<N, L, true>(ops_s, A.Q, rhs_off, cval, mono, M, rabs, row_of, r);
+  else run_ops<N, L, false>(ops_s, A.Q, rhs_off, cval, mono, M, rabs, row_of, r);
   __syncwarp();
   HCB_T(c3);
   HCB_ACC(2, c2, c3);
@@ -646,14 +641,19 @@ __device__ __forceinline__ bool eval_solve(const TrackArgs &A, const uint2 *__re
   if constexpr (NC == 2) {
     // hybrid layout: row r plus the extra rows' columns r and r + 16
     double2 a[N + 1], e[E][2];
+    double jmax = 0.0;
 #pragma unroll
-    for (int j = 0; j <= N; ++j) a[j] = M[mpos_s[r * (N + 1) + j]];
+    for (int j = 0; j <= N; ++j) {
+      a[j] = M[mpos_s[r * (N + 1) + j]];
+      if (j < N) jmax = fmax(jmax, abs2(a[j]));
+    }
 #pragma unroll
     for (int q = 0; q < E; ++q)
 #pragma unroll
       for (int c = 0; c < 2; ++c) {
         const int col = r + 16 * c;
         e[q][c] = (col <= N) ? M[mpos_s[(16 + q) * (N + 1) + col]] : make_double2(0.0, 0.0);
+        if (col < N) jmax = fmax(jmax, abs2(e[q][c]));
       }
     fr[0] = a[N];
     fr[NC - 1] = (r < E) ? M[mpos_s[(16 + (r < E ? r : 0)) * (N + 1) + N]] : make_double2(0.0, 0.0);
@@ -668,13 +668,14 @@ __device__ __forceinline__ bool eval_solve(const TrackArgs &A, const uint2 *__re
   }
   double2 a[N + 1];
   const int rr = (r < N) ? r : 0;
+  double jmax = 0.0;   // max |A_rj|^2 of this row, for the singularity threshold (R9)
 #pragma unroll
   for (int j = 0; j <= N; ++j) {
     a[j] = M[mpos_s[rr * (N + 1) + j]];
-    if (!TrackerShape<N>::JMAX_OPS && j < N) jmax = fmax(jmax, abs2(a[j]));
+    if (j < N) jmax = fmax(jmax, abs2(a[j]));
   }
   if (r >= N) {
-    if (!TrackerShape<N>::JMAX_OPS) jmax = 0.0;
+    jmax = 0.0;
 #pragma unroll
     for (int j = 0; j <= N; ++j) a[j] = make_double2(0.0, 0.0);
   }
