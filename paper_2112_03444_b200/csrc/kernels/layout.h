@@ -8,20 +8,12 @@ namespace hcb {
 
 __host__ __device__ inline size_t align16(size_t b) { return (b + 15) & ~size_t(15); }
 
-// Complex slots of the evaluation scratch: mono[n_mono] followed by M[n_entries]; the elimination
-// reuses the same region as its row buffer rows[N][N + 1] once the rows are in registers.
-__host__ __device__ inline size_t scratch_c128(int N, int n_mono, int n_entries) {
-  const size_t ev = (size_t)n_mono + n_entries, lu = (size_t)N * (N + 1);
-  return ev > lu ? ev : lu;
-}
-
 // Per track slot: cval[ncoef + ncoef_src] (c(t) for every slot, c'(t) for the rhs slots),
-// scratch (mono[n_mono] (x_0..x_{N-1}, 1, shared products) + M[n_entries] (non-zero entries of
-// [dH/dx | rhs]) | rows[N][N + 1] during the elimination), prow[2 * (N + 1)] (double-buffered pivot
-// row / solution), rabs[N] (doubles), pl[N] (bytes: pivot lane of each elimination step).
+// mono[n_mono] (x_0..x_{N-1}, 1, shared products), M[n_entries] (non-zero entries of
+// [dH/dx | rhs]), prow[2 * (N + 1)] (double-buffered pivot row), rabs[N] (doubles), pl[N] (bytes:
+// pivot lane of each elimination step).
 __host__ __device__ inline size_t slot_bytes(int N, int ncoef, int ncoef_src, int n_mono, int n_entries) {
-  return align16(sizeof(double) * 2 * ((size_t)ncoef + ncoef_src + scratch_c128(N, n_mono, n_entries) +
-                                       2 * (N + 1)) +
+  return align16(sizeof(double) * 2 * ((size_t)ncoef + ncoef_src + n_mono + n_entries + 2 * (N + 1)) +
                  sizeof(double) * N + N);
 }
 

@@ -48,9 +48,6 @@ constexpr unsigned FULL = 0xffffffffu;
 #ifndef HCB_MAXW_MID   // warps per CTA for 15 <= N <= 20 (A/B experiments override it)
 #define HCB_MAXW_MID 12
 #endif
-#ifndef HCB_ROWS_ALL   // elimination: every lane keeps its row in shared memory (A/B switch, see lu_rows)
-#define HCB_ROWS_ALL 1
-#endif
 template <int N>
 struct TrackerShape {
   static constexpr bool HY = hy_layout(N);
@@ -205,15 +202,9 @@ __device__ __forceinline__ int seg_argmax(double v, int r, double &vmax) {
 // Returns the solution component y_r in lane r and a slot-uniform success flag.
 // prow: 2 * (N + 1) double2; pl: N bytes (per slot shared memory).
 // ------------------------------------------------------------------------------------------
-// ROWS (tracker, HCB_ROWS_ALL): instead of the pivot lane publishing its row once the arg-max has
-// named it, every lane keeps its own row's trailing columns in rows[r * (N + 1) + j] (stored right
-// after its update, off the arg-max -> load chain), and the readers load row p directly.  The same
-// number of store instructions (all lanes active instead of one), one __syncwarp per column; a
-// lane's stored values change only when it is not the pivot, and row p is only read after the
-// column's __syncwarp, so no double buffer is needed.
-template <int N, int L, bool ROWS = false>
+template <int N, int L>
 __device__ __forceinline__ bool lu_rows(double2 (&a)[N + 1], int r, int seg, double2 *prow, uint8_t *pl,
-                                        double pivot_rel, double lane_max, double2 &y, double2 *rows = nullptr) {
+                                        double pivot_rel, double lane_max, double2 &y) {
   bool used = (r >= N);
   int mystep = used ? N : -1;
   double2 myinv = make_double2(0.0, 0.0);
@@ -227,26 +218,16 @@ __device__ __forceinline__ bool lu_rows(double2 (&a)[N + 1], int r, int seg, dou
   if (!(v0 >= 0.0)) v0 = -1.0;   // NaN is never a pivot
   int p = seg_argmax_thr<L>(v0, r, thr, sing);
   double2 spec = crecip(a[0]);   // speculative 1/a_rk of this lane's candidate (overlaps the search)
-  double2 *myrow = rows + (r < N ? r : 0) * (N + 1);
-  if constexpr (ROWS) {
-    __syncwarp();   // the row buffer aliases the evaluation's scratch that other lanes may still read
-    if (r < N) {
-#pragma unroll
-      for (int j = 2; j <= N; ++j) myrow[j] = a[j];
-    }
-  }
 #pragma unroll
   for (int k = 0; k < N; ++k) {
-    double2 *pr = ROWS ? rows + p * (N + 1) : prow + (k & 1) * (N + 1);
+    double2 *pr = prow + (k & 1) * (N + 1);
     // early broadcast from the pivot lane by shuffles: 1/pivot and the pivot row's column k+1
     const double2 inv = shfl2(spec, p, L);
     const double2 u1 = shfl2(a[k + 1], p, L);
     const bool me = (r == p);
     if (me) {   // the pivot lane publishes the rest of its row (columns k+2..N) through shared memory
-      if constexpr (!ROWS) {
 #pragma unroll
-        for (int j = k + 2; j <= N; ++j) pr[j] = a[j];
-      }
+      for (int j = k + 2; j <= N; ++j) pr[j] = a[j];
       used = true;
       mystep = k;
       myinv = spec;
@@ -274,13 +255,6 @@ __device__ __forceinline__ bool lu_rows(double2 (&a)[N + 1], int r, int seg, dou
 #pragma unroll
         for (int i = 0; i < 4; ++i)
           if (j0 + i <= N) a[j0 + i] = cfms(a[j0 + i], l, u[i]);
-        if constexpr (ROWS) {   // columns k+3..N of the updated row, for the next column's readers
-          if (r < N && k + 2 < N) {
-#pragma unroll
-            for (int i = 0; i < 4; ++i)
-              if (j0 + i >= k + 3 && j0 + i <= N) myrow[j0 + i] = a[j0 + i];
-          }
-        }
       }
     }
   }
@@ -582,10 +556,6 @@ __device__ __forceinline__ bool eval_solve(const TrackArgs &A, const uint2 *__re
   HCB_T(c0);
   constexpr int E = TrackerShape<N>::E;
   if (r < N) mono[r] = xr[0];
-  if (HCB_ROWS_ALL && r == 0) {   // the elimination's row buffer overwrote the constants of the scratch
-    mono[N] = make_double2(1.0, 0.0);            // constant-one slot
-    M[A.n_entries] = make_double2(0.0, 0.0);     // the entry every structural zero reads
-  }
   if constexpr (NC == 2) {
     if (r < E) mono[16 + r] = xr[NC - 1];
   }
@@ -683,7 +653,7 @@ __device__ __forceinline__ bool eval_solve(const TrackArgs &A, const uint2 *__re
   fabs_r[0] = (r < N && want_abs) ? rabs[r] : 0.0;
   HCB_T(c4);
   HCB_ACC(3, c3, c4);
-  const bool ok = lu_rows<N, L, HCB_ROWS_ALL != 0>(a, r, seg, prow, pl, A.st.pivot_rel, jmax, y[0], mono);
+  const bool ok = lu_rows<N, L>(a, r, seg, prow, pl, A.st.pivot_rel, jmax, y[0]);
   HCB_T(c5);
   HCB_ACC(4, c4, c5);
   return ok;
@@ -693,7 +663,7 @@ __device__ __forceinline__ bool eval_solve(const TrackArgs &A, const uint2 *__re
 // The persistent tracker kernel.
 // ------------------------------------------------------------------------------------------
 template <int N>
-__global__ void __launch_bounds__(TrackerShape<N>::MAXW * 32, TrackerShape<N>::MINB) hc_track_kernel(const TrackArgs A) {
+__device__ __forceinline__ void track_body(const TrackArgs &A) {
   constexpr int L = TrackerShape<N>::L;
   constexpr int NC = TrackerShape<N>::NC;   // unknown components per lane (2: hybrid layout)
   constexpr int E = TrackerShape<N>::E;
@@ -723,7 +693,7 @@ __global__ void __launch_bounds__(TrackerShape<N>::MAXW * 32, TrackerShape<N>::M
   double2 *cval = reinterpret_cast<double2 *>(sb);
   double2 *mono = cval + ncoef + A.ncoef_src;
   double2 *M = mono + A.n_mono;
-  double2 *prow = mono + scratch_c128(N, A.n_mono, A.n_entries + 1);   // mono + M, or the LU row buffer
+  double2 *prow = M + A.n_entries + 1;
   double *rabs = reinterpret_cast<double *>(prow + 2 * (N + 1));
   uint8_t *pl = reinterpret_cast<uint8_t *>(rabs + N);
   if (r == 0) {
@@ -982,6 +952,23 @@ __global__ void __launch_bounds__(TrackerShape<N>::MAXW * 32, TrackerShape<N>::M
 #endif
 }
 
+// Kernel entry points.  The register budget comes from __launch_bounds__ (MAXW warps, MINB CTAs per
+// SM), or, for 15 <= N <= 20 when HCB_MID_MAXREG is set, from an explicit __maxnreg__ (which allows
+// warp counts that are not a multiple of 4 at a budget between 128 and 168 registers).
+#ifndef HCB_MID_MAXREG
+#define HCB_MID_MAXREG 0
+#endif
+template <int N>
+constexpr bool use_maxnreg() { return HCB_MID_MAXREG > 0 && N >= 15 && N <= 20 && !hy_layout(N); }
+template <int N>
+__global__ void __launch_bounds__(TrackerShape<N>::MAXW * 32, TrackerShape<N>::MINB) hc_track_kernel(const TrackArgs A) {
+  track_body<N>(A);
+}
+template <int N>
+__global__ void __maxnreg__(HCB_MID_MAXREG > 0 ? HCB_MID_MAXREG : 128) hc_track_kernel_r(const TrackArgs A) {
+  track_body<N>(A);
+}
+
 template <int N>
 cudaError_t launch_tracker_n(const TrackArgs &A, int device, cudaStream_t stream, TrackerPlan *plan) {
   constexpr int L = TrackerShape<N>::L;
@@ -998,10 +985,13 @@ cudaError_t launch_tracker_n(const TrackArgs &A, int device, cudaStream_t stream
   while (warps > 1 && tables + warps * per_warp > (size_t)smem_max) --warps;
   const size_t smem = tables + warps * per_warp;
   if (smem > (size_t)smem_max) return cudaErrorInvalidConfiguration;
-  cudaError_t e = cudaFuncSetAttribute(hc_track_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  const void *fn;
+  if constexpr (use_maxnreg<N>()) fn = (const void *)hc_track_kernel_r<N>;
+  else fn = (const void *)hc_track_kernel<N>;
+  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   int per_sm = 0;
-  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, hc_track_kernel<N>, warps * 32, smem);
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, warps * 32, smem);
   if (e != cudaSuccess) return e;
   if (per_sm < 1) return cudaErrorInvalidConfiguration;
   int sms = 0;
@@ -1017,7 +1007,8 @@ cudaError_t launch_tracker_n(const TrackArgs &A, int device, cudaStream_t stream
     plan->ctas = (int)ctas;
     plan->smem_bytes = smem;
   }
-  hc_track_kernel<N><<<(unsigned)ctas, warps * 32, smem, stream>>>(A);
+  if constexpr (use_maxnreg<N>()) hc_track_kernel_r<N><<<(unsigned)ctas, warps * 32, smem, stream>>>(A);
+  else hc_track_kernel<N><<<(unsigned)ctas, warps * 32, smem, stream>>>(A);
   return cudaGetLastError();
 }
 
