@@ -1,6 +1,6 @@
 """Benchmark: device-timed tracks/s and instances/s of the fused B200 HC tracker.
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--config trifocal|fourview|fivepoint|cyclic7|katsura6]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config trifocal|fourview|fivepoint|cyclic7|katsura6|eco12]
                   [--instances B] [--impl ours|reference] [--no-e2e] [--no-cpu-baseline]
 
 One "step" = one pass of the whole hot path (coefficient prologue + fused tracker: every
@@ -64,10 +64,11 @@ def make_workload(name: str, B: int, rank: int):
         meta = {"workload": f"5-point rel. pose + depth (16x16, Table 2 P:492; reading R24) PH, S=40 x {B} "
                             f"planted instances per GPU (SURVEY N2)"}
         return d, start, p0, p1s, {}, meta
-    if name in ("cyclic7", "katsura6"):
-        d = systems.cyclic(7) if name == "cyclic7" else systems.katsura(6)
-        meta = {"workload": f"{d.name} total-degree homotopy, gamma seed 2, single instance "
-                            f"({'configs[1]' if name == 'cyclic7' else 'configs[0]'})"}
+    if name in ("cyclic7", "katsura6", "eco12"):
+        d = {"cyclic7": lambda: systems.cyclic(7), "katsura6": lambda: systems.katsura(6),
+             "eco12": lambda: systems.eco(12)}[name]()
+        which = {"cyclic7": "configs[1]", "katsura6": "configs[0]", "eco12": "Table 1 P:469, SURVEY N2"}[name]
+        meta = {"workload": f"{d.name} total-degree homotopy, gamma seed 2, single instance ({which})"}
         return d, None, None, None, {}, meta
     raise SystemExit(f"unknown config {name}")
 
@@ -117,12 +118,12 @@ class ClockSampler:
 
 # ------------------------------------------------------------------------------ oracle (cpu)
 
-def oracle_sample(name: str, budget_s: float, rank: int = 0, B: int = 1):
+def oracle_sample(name: str, budget_s: float, rank: int = 0, B: int = 1, nthreads: int | None = None):
     """Time the CPU oracle (as it stands) on a bounded sample of the workload: the first tracks of
     instance 0, sized to ~budget_s of CPU time.  Returns (tracks/s, cores, sample description)."""
     import oracle
     d, start, p0, p1s, _, _ = make_workload(name, 1, rank)
-    nthreads = oracle.nthreads_default()
+    nthreads = nthreads or oracle.nthreads_default()
     if start is None:   # TD single instance
         from hc_inputs import rng
         hom = oracle.td_homotopy(d, rng.gamma(2))
@@ -319,6 +320,9 @@ def run_ours(args):
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         v, cores, sample = oracle_sample(args.config, args.cpu_budget_s)
         cpu = {"value": v, "unit": "tracks/s", "cores": cores, "kind": "oracle", "sample": sample}
+        if args.config in ("katsura6", "cyclic7", "eco12"):   # TD benchmarks also on 1 thread
+            v1, _, sample1 = oracle_sample(args.config, min(args.cpu_budget_s, 5.0), nthreads=1)
+            cpu["single_thread"] = {"value": v1, "unit": "tracks/s", "cores": 1, "sample": sample1}
 
     if rank == 0:
         line = {
@@ -354,7 +358,7 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=1)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", default="trifocal", choices=["trifocal", "fourview", "fivepoint", "cyclic7", "katsura6"])
+    ap.add_argument("--config", default="trifocal", choices=["trifocal", "fourview", "fivepoint", "cyclic7", "katsura6", "eco12"])
     ap.add_argument("--instances", type=int, default=1024)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--warmup-instances", type=int, default=16)

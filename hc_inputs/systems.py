@@ -65,6 +65,28 @@ def cyclic(n: int) -> SystemDesc:
     return desc_from_equations(eqs, name=f"cyclic-{n}", var_names=[f"x{i}" for i in range(n)])
 
 
+def eco(n: int) -> SystemDesc:
+    """eco-n (Table 1: eco-12, 12 unknowns, 1024 solutions; the paper cites the
+    benchmark without writing it down -- standard economics-modelling family, reading R25):
+
+    f_k = (x_k + sum_{i=1}^{n-k-1} x_i x_{i+k}) x_n - k   (k = 1..n-1),   f_n = x_1 + ... + x_{n-1} + 1.
+    Degrees 3 (k <= n-2), 2 (k = n-1), 1: total degree 2 * 3^(n-2) (eco-12: 118,098 tracks); the
+    family has 2^(n-2) finite solutions (eco-12: 1024 = Table 1).
+    """
+    X = [var_x(n, 0, i) for i in range(n)]   # X[i] = x_{i+1}
+    eqs = []
+    for k in range(1, n):
+        inner = X[k - 1]
+        for i in range(1, n - k):
+            inner = inner + X[i - 1] * X[i + k - 1]
+        eqs.append(inner * X[n - 1] - k)
+    lin = const(n, 0, 1)
+    for i in range(n - 1):
+        lin = lin + X[i]
+    eqs.append(lin)
+    return desc_from_equations(eqs, name=f"eco-{n}", var_names=[f"x{i + 1}" for i in range(n)])
+
+
 def univariate(coeffs) -> SystemDesc:
     """f(x) = sum_k coeffs[k] x^k  (one equation, one unknown; test system)."""
     X = var_x(1, 0, 0)

@@ -3,6 +3,7 @@
   python scripts/make_fixtures.py fourview   # 4-view TD solve at generic complex p0 -> 296 starts
   python scripts/make_fixtures.py trifocal   # trifocal monodromy from a planted (x0, p0)
   python scripts/make_fixtures.py fivepoint  # 5-point relpose + depth monodromy (reading R24)
+  python scripts/make_fixtures.py eco12      # eco-12 TD solve (118,098 tracks) -> the oracle's finite set
 
 This script imports only `oracle` and `hc_inputs`; the CUDA path never writes fixtures
 (prompt rule ③: no stored value comes from the CUDA path).  Start systems of the paper's
@@ -119,6 +120,25 @@ def make_fivepoint(max_loops: int = 40, stall_loops: int = 5, seed: int = rng.SE
     fixtures.write_params(fixtures.fixture_path("fivepoint_p0.params"), p0, hdr)
 
 
+ECO12_GAMMA_SEED = 2
+
+
+def make_eco12():
+    """The oracle's finite solution set of eco-12 (Table 1: 1024 solutions), used by the GPU
+    parity test as the expected set (the oracle needs minutes for 118,098 tracks)."""
+    d = systems.eco(12)
+    t0 = time.time()
+    res = oracle.track(oracle.td_homotopy(d, rng.gamma(ECO12_GAMMA_SEED)), oracle.td_start(d.degrees()))
+    U, mult = oracle.dedup(oracle.finite_solutions(res))
+    st = np.bincount(res.status.reshape(-1), minlength=6)
+    print(f"eco-12 TD: {len(U)} distinct finite of {res.status.size} tracks (statuses {st.tolist()}), "
+          f"max mult {mult.max()}, {time.time() - t0:.1f} s", flush=True)
+    hdr = (f"eco-12 finite solutions (PAPER.md Table 1 P:469: 1024), reading R25 (standard eco-n).\n"
+           f"Written by scripts/make_fixtures.py (oracle only): TD homotopy, gamma seed {ECO12_GAMMA_SEED},\n"
+           f"{res.status.size} tracks -> {len(U)} distinct finite solutions; statuses {st.tolist()}.")
+    fixtures.write_solutions(fixtures.fixture_path("eco12_solutions.sols"), U, hdr)
+
+
 if __name__ == "__main__":
     oracle.build()
     what = sys.argv[1:] or ["fourview", "trifocal", "fivepoint"]
@@ -128,3 +148,5 @@ if __name__ == "__main__":
         make_trifocal()
     if "fivepoint" in what:
         make_fivepoint()
+    if "eco12" in what:
+        make_eco12()

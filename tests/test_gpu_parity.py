@@ -159,6 +159,34 @@ def test_cyclic7_parity(hc, orc):
     assert r[st == 0, 0].max() < 1e-10
 
 
+@pytest.mark.parametrize("n", [6, 8, 10])
+def test_eco_parity(hc, orc, n):
+    """eco-n (reading R25): 2^(n-2) solutions, the same set as the oracle on the same gamma."""
+    d = systems.eco(n)
+    gam = rng.gamma(2)
+    res, _ = run_td(hc, d, gam)
+    B = gpu_set(orc, res)
+    ref = orc.track(orc.td_homotopy(d, gam), orc.td_start(d.degrees()))
+    A = orc.dedup(orc.finite_solutions(ref))[0]
+    assert len(A) == 2 ** (n - 2)
+    assert_same_set(orc, A, B, f"eco-{n}")
+
+
+@pytest.mark.skipif(not fixtures.have_fixture("eco12_solutions.sols"), reason="eco-12 fixture missing")
+def test_eco12_table1_count(hc, orc):
+    """Table 1: eco-12 has 1024 solutions.  GPU TD solve (118,098 tracks) vs the oracle's set
+    (fixture written by scripts/make_fixtures.py, oracle only; the same gamma seed)."""
+    d = systems.eco(12)
+    res, _ = run_td(hc, d, rng.gamma(2))
+    B = gpu_set(orc, res)
+    A = fixtures.read_solutions(fixtures.fixture_path("eco12_solutions.sols"))
+    assert len(A) == 1024
+    assert_same_set(orc, A, B, "eco-12")
+    r = res.resid.cpu().numpy()[0]
+    st = res.status.cpu().numpy()[0]
+    assert r[st == 0, 0].max() < 1e-10
+
+
 def test_counters_and_determinism(hc, orc):
     d = systems.katsura(5)
     gam = rng.gamma(7)

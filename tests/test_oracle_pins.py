@@ -266,6 +266,31 @@ def test_cyclic7_924(orc):
     assert _cyclic_closed(U, 7)
 
 
+def test_eco3_closed_form(orc):
+    """eco-3 (reading R25) by hand: x1 + x2 + 1 = 0, x2 x3 = 2, (x1 + x1 x2) x3 = 1 give
+    2 x2^2 + 5 x2 + 2 = 0, i.e. (x1, x2, x3) = (-1/2, -1/2, -4) and (1, -2, -1)."""
+    d = systems.eco(3)
+    res = orc.track(orc.td_homotopy(d, rng.gamma(2)), orc.td_start(d.degrees()))
+    U, _ = orc.dedup(orc.finite_solutions(res))
+    want = np.array([[-0.5, -0.5, -4.0], [1.0, -2.0, -1.0]], dtype=np.complex128)
+    assert len(U) == 2
+    for w in want:
+        assert np.min(np.max(np.abs(U - w), axis=1)) < 1e-12
+
+
+@pytest.mark.parametrize("n,count", [(5, 8), (6, 16), (8, 64)])
+def test_eco_counts(orc, n, count):
+    """eco-n has 2^(n-2) finite roots (eco-12: 1024, Table 1); every endpoint solves the
+    system as written by its builder (independent evaluator hc_inputs.evalpoly)."""
+    d = systems.eco(n)
+    res = orc.track(orc.td_homotopy(d, rng.gamma(2)), orc.td_start(d.degrees()))
+    assert res.status.size == 2 * 3 ** (n - 2)   # total degree 3^(n-2) * 2 * 1
+    U, mult = orc.dedup(orc.finite_solutions(res))
+    assert len(U) == count and mult.max() == 1
+    for x in U:
+        assert max(abs(eval_poly(f, x)) for f in d.polys) < 1e-10
+
+
 def test_determinism_across_thread_counts(orc):
     """bit-identical results for 1 and 8 threads."""
     d = systems.cyclic(5)
