@@ -105,7 +105,7 @@ hc_status hc_total_degree_start(hc_system sys, hc_complex *start_x);
 typedef struct {
   int32_t n_vars, n_params, n_coefs;
   int32_t coef_degree_t;      /* D: degree of the coefficient polynomials in t */
-  int32_t lanes_per_track;    /* L = next power of two >= N */
+  int32_t lanes_per_track;    /* L = next power of two >= N (throughput layout; see hc_track_batch) */
   int32_t tracks_per_warp;    /* 32 / L */
   int32_t op_steps;           /* Q: evaluation op steps per lane (lane-balanced) */
   int32_t max_factors;        /* M: max monomial degree (paper's M) */
@@ -182,7 +182,13 @@ typedef struct {
 } hc_batch;
 
 /* Enqueue (or, for HC_MEM_HOST, run) one batch.  *out (may be NULL) receives a result handle that
- * must be released with hc_result_destroy; the system must outlive its results. */
+ * must be released with hc_result_destroy; the system must outlive its results.
+ * Lane layout (a launch choice; results agree as solution sets, bits may differ between layouts
+ * because the op list is balanced over a different number of lanes): for N <= 16 a batch of at
+ * most ~2.5 waves of one-track-per-warp slots runs in the wide latency layout (32 lanes per track,
+ * e.g. single-instance katsura-6 / cyclic-7 solves), larger batches in the throughput layout
+ * (next_pow2(N) lanes per track, 32 / that tracks per warp).  Environment HC_LANES=wide|narrow
+ * overrides the choice; hc_result_launch reports it. */
 hc_status hc_track_batch(hc_system sys, const hc_tracker_settings *settings, const hc_batch *batch,
                          hc_result *out);
 /* Block until the batch finished. */

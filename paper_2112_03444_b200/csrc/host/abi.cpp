@@ -1,5 +1,6 @@
 // abi.cpp -- the C ABI (include/hc.h): system handles, batch launch, results, helpers.
 #include <cmath>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <new>
@@ -12,6 +13,10 @@
 
 namespace hcb {
 // per-N launchers defined in csrc/kernels/tracker_n*.cu
+#define HCB_DECLW(N) cudaError_t launch_tracker_wide_##N(const TrackArgs &, int, cudaStream_t, TrackerPlan *);
+HCB_DECLW(1) HCB_DECLW(2) HCB_DECLW(3) HCB_DECLW(4) HCB_DECLW(5) HCB_DECLW(6) HCB_DECLW(7) HCB_DECLW(8)
+HCB_DECLW(9) HCB_DECLW(10) HCB_DECLW(11) HCB_DECLW(12) HCB_DECLW(13) HCB_DECLW(14) HCB_DECLW(15) HCB_DECLW(16)
+#undef HCB_DECLW
 #define HCB_DECL(N)                                                                                      \
   cudaError_t launch_tracker_##N(const TrackArgs &, int, cudaStream_t, TrackerPlan *);                  \
   cudaError_t launch_zgesv_##N(int64_t, const double2 *, const double2 *, double2 *, int32_t *, double, \
@@ -40,6 +45,14 @@ static const zgesv_fn kZgesv[33] = {
     launch_zgesv_30,  launch_zgesv_31, launch_zgesv_32};
 
 tracker_launch_fn tracker_launcher(int N) { return (N >= 1 && N <= 32) ? kTrackers[N] : nullptr; }
+// the wide latency layout (32 lanes per track) for N <= 16
+static const tracker_launch_fn kTrackersWide[17] = {
+    nullptr,               launch_tracker_wide_1,  launch_tracker_wide_2,  launch_tracker_wide_3,
+    launch_tracker_wide_4, launch_tracker_wide_5,  launch_tracker_wide_6,  launch_tracker_wide_7,
+    launch_tracker_wide_8, launch_tracker_wide_9,  launch_tracker_wide_10, launch_tracker_wide_11,
+    launch_tracker_wide_12, launch_tracker_wide_13, launch_tracker_wide_14, launch_tracker_wide_15,
+    launch_tracker_wide_16};
+static tracker_launch_fn tracker_launcher_wide(int N) { return (N >= 1 && N <= 16) ? kTrackersWide[N] : nullptr; }
 
 cudaError_t launch_batched_zgesv(int n, int64_t batch, const double2 *A, const double2 *b, double2 *x,
                                  int32_t *info, double pivot_rel, cudaStream_t s) {
@@ -67,14 +80,22 @@ static hc_status cuda_fail(cudaError_t e, const char *where) {
     if (_e != cudaSuccess) return cuda_fail(_e, #call); \
   } while (0)
 
-struct hc_system_s {
-  int device = 0;
-  CompiledSystem cs;
+// A compiled table set on the device (one per lane layout).
+struct DevTables {
   uint2 *d_ops = nullptr;
   uint32_t *d_mono_prog = nullptr;
   int16_t *d_mpos = nullptr;
   CoefMono *d_mono = nullptr;
   int32_t *d_mono_ptr = nullptr;
+};
+
+struct hc_system_s {
+  int device = 0;
+  CompiledSystem cs;     // throughput layout: lanes_for(N) lanes per track
+  DevTables dt;
+  bool has_wide = false;  // N <= 16: the wide latency layout (32 lanes per track) as well
+  CompiledSystem cs_w;
+  DevTables dt_w;
   // total-degree metadata
   bool td = false;
   std::vector<hc_complex> td_fvals;
@@ -148,36 +169,46 @@ hc_status hc_tracker_settings_default(hc_tracker_settings *s) {
   return HC_OK;
 }
 
-static hc_status upload_system(hc_system sys) {
-  CompiledSystem &cs = sys->cs;
-  CK(cudaSetDevice(sys->device));
-  CK(cudaMalloc(&sys->d_ops, sizeof(uint2) * std::max<size_t>(1, cs.ops.size())));
-  CK(cudaMalloc(&sys->d_mono_prog, sizeof(uint32_t) * std::max<size_t>(1, cs.mono_prog.size())));
+static hc_status upload_tables(const CompiledSystem &cs, DevTables &t) {
+  CK(cudaMalloc(&t.d_ops, sizeof(uint2) * std::max<size_t>(1, cs.ops.size())));
+  CK(cudaMalloc(&t.d_mono_prog, sizeof(uint32_t) * std::max<size_t>(1, cs.mono_prog.size())));
   // device copy of the entry map: structural zeros point at the extra always-zero entry n_entries
   std::vector<int16_t> mp(cs.mpos);
   for (auto &v : mp)
     if (v < 0) v = (int16_t)cs.n_entries;
-  CK(cudaMalloc(&sys->d_mpos, sizeof(int16_t) * mp.size()));
-  CK(cudaMemcpy(sys->d_mpos, mp.data(), sizeof(int16_t) * mp.size(), cudaMemcpyHostToDevice));
-  CK(cudaMalloc(&sys->d_mono, sizeof(CoefMono) * std::max<size_t>(1, cs.mono.size())));
-  CK(cudaMalloc(&sys->d_mono_ptr, sizeof(int32_t) * cs.mono_ptr.size()));
-  if (!cs.ops.empty()) CK(cudaMemcpy(sys->d_ops, cs.ops.data(), sizeof(uint2) * cs.ops.size(), cudaMemcpyHostToDevice));
+  CK(cudaMalloc(&t.d_mpos, sizeof(int16_t) * mp.size()));
+  CK(cudaMemcpy(t.d_mpos, mp.data(), sizeof(int16_t) * mp.size(), cudaMemcpyHostToDevice));
+  CK(cudaMalloc(&t.d_mono, sizeof(CoefMono) * std::max<size_t>(1, cs.mono.size())));
+  CK(cudaMalloc(&t.d_mono_ptr, sizeof(int32_t) * cs.mono_ptr.size()));
+  if (!cs.ops.empty()) CK(cudaMemcpy(t.d_ops, cs.ops.data(), sizeof(uint2) * cs.ops.size(), cudaMemcpyHostToDevice));
   if (!cs.mono_prog.empty())
-    CK(cudaMemcpy(sys->d_mono_prog, cs.mono_prog.data(), sizeof(uint32_t) * cs.mono_prog.size(), cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(t.d_mono_prog, cs.mono_prog.data(), sizeof(uint32_t) * cs.mono_prog.size(), cudaMemcpyHostToDevice));
   if (!cs.mono.empty())
-    CK(cudaMemcpy(sys->d_mono, cs.mono.data(), sizeof(CoefMono) * cs.mono.size(), cudaMemcpyHostToDevice));
-  CK(cudaMemcpy(sys->d_mono_ptr, cs.mono_ptr.data(), sizeof(int32_t) * cs.mono_ptr.size(), cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(t.d_mono, cs.mono.data(), sizeof(CoefMono) * cs.mono.size(), cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(t.d_mono_ptr, cs.mono_ptr.data(), sizeof(int32_t) * cs.mono_ptr.size(), cudaMemcpyHostToDevice));
   return HC_OK;
+}
+
+static hc_status upload_system(hc_system sys) {
+  CK(cudaSetDevice(sys->device));
+  hc_status s = upload_tables(sys->cs, sys->dt);
+  if (s == HC_OK && sys->has_wide) s = upload_tables(sys->cs_w, sys->dt_w);
+  return s;
+}
+
+static void free_tables(DevTables &t) {
+  cudaFree(t.d_ops);
+  cudaFree(t.d_mono_prog);
+  cudaFree(t.d_mpos);
+  cudaFree(t.d_mono);
+  cudaFree(t.d_mono_ptr);
 }
 
 static void free_system(hc_system sys) {
   if (!sys) return;
   cudaSetDevice(sys->device);
-  cudaFree(sys->d_ops);
-  cudaFree(sys->d_mono_prog);
-  cudaFree(sys->d_mpos);
-  cudaFree(sys->d_mono);
-  cudaFree(sys->d_mono_ptr);
+  free_tables(sys->dt);
+  free_tables(sys->dt_w);
   delete sys;
 }
 
@@ -189,6 +220,10 @@ hc_status hc_system_create(const hc_system_desc *desc, int device, hc_system *ou
   sys->device = device;
   std::string err;
   hc_status s = compile_system(*desc, sys->cs, err);
+  if (s == HC_OK && sys->cs.N <= 16 && sys->cs.L < 32) {
+    s = compile_system(*desc, sys->cs_w, err, 32);
+    sys->has_wide = (s == HC_OK);
+  }
   if (s != HC_OK) {
     delete sys;
     return fail(s, err);
@@ -350,6 +385,21 @@ static hc_status check_settings(const hc_tracker_settings &s) {
 
 static bool aligned16(const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
 
+// Wide latency layout when the throughput layout would leave the GPU mostly idle: at most ~2.5
+// waves of one-track-per-warp slots (16 resident warps per SM for N <= 14, 12 for N = 15, 16), i.e.
+// small single-instance solves (katsura-6: 64 tracks, cyclic-7: 5040), where the makespan is one
+// track's chain of solves and spreading its op list over 32 lanes shortens every solve.
+static bool wide_layout(int device, int N, int64_t tracks) {
+  if (const char *ev = getenv("HC_LANES")) {
+    if (!strcmp(ev, "wide")) return true;
+    if (!strcmp(ev, "narrow")) return false;
+  }
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+  const int64_t slots = (int64_t)sms * (N <= 14 ? 16 : 12);
+  return tracks * 2 <= slots * 5;
+}
+
 hc_status hc_track_batch(hc_system sys, const hc_tracker_settings *settings, const hc_batch *bt, hc_result *out) {
   if (out) *out = nullptr;
   if (!sys || !bt) return fail(HC_E_INVALID_ARG, "null argument");
@@ -358,10 +408,15 @@ hc_status hc_track_batch(hc_system sys, const hc_tracker_settings *settings, con
   else hc_tracker_settings_default(&st);
   hc_status s = check_settings(st);
   if (s != HC_OK) return s;
-  const CompiledSystem &cs = sys->cs;
-  const int N = cs.N, P = cs.P;
+  const int N = sys->cs.N, P = sys->cs.P;
   if (bt->n_instances < 1 || bt->n_start < 1) return fail(HC_E_INVALID_ARG, "n_instances and n_start must be >= 1");
   if (bt->n_instances > (1LL << 40) / bt->n_start) return fail(HC_E_TOO_LARGE, "too many tracks");
+  // ---- lane layout: the wide latency layout (one track per warp, 32 lanes) when the batch
+  //      under-fills the GPU in the throughput layout (policy in wide_layout()); HC_LANES=wide|narrow
+  //      overrides it (experiments and tests) ----
+  const bool wide = sys->has_wide && wide_layout(sys->device, N, bt->n_instances * bt->n_start);
+  const CompiledSystem &cs = wide ? sys->cs_w : sys->cs;
+  const DevTables &dt = wide ? sys->dt_w : sys->dt;
   if (!bt->start_x) return fail(HC_E_INVALID_ARG, "start_x is null");
   if (P > 0 && (!bt->p_start || !bt->p_target)) return fail(HC_E_INVALID_ARG, "p_start / p_target null with P > 0");
   if (bt->memory != HC_MEM_DEVICE && bt->memory != HC_MEM_HOST) return fail(HC_E_INVALID_ARG, "memory");
@@ -438,8 +493,8 @@ hc_status hc_track_batch(hc_system sys, const hc_tracker_settings *settings, con
 
   // ---- prologue: per-instance coefficient polynomials in t ----
   PrologueArgs pa{};
-  pa.mono = sys->d_mono;
-  pa.coef_mono_ptr = sys->d_mono_ptr;
+  pa.mono = dt.d_mono;
+  pa.coef_mono_ptr = dt.d_mono_ptr;
   pa.ncoef = cs.ncoef;
   pa.D = cs.D;
   pa.P = P;
@@ -454,15 +509,15 @@ hc_status hc_track_batch(hc_system sys, const hc_tracker_settings *settings, con
 
   // ---- the fused tracker ----
   TrackArgs ta{};
-  ta.ops = sys->d_ops;
+  ta.ops = dt.d_ops;
   ta.Q = cs.Q;
-  ta.mono_prog = sys->d_mono_prog;
+  ta.mono_prog = dt.d_mono_prog;
   ta.n_mono = cs.n_mono;
   ta.n_levels = cs.n_levels;
   for (int l = 0; l < MAX_LEVELS; ++l) ta.level_end[l] = cs.level_end[l];
   ta.ncoef = cs.ncoef;
   ta.ncoef_src = cs.ncoef_src;
-  ta.mpos = sys->d_mpos;
+  ta.mpos = dt.d_mpos;
   ta.n_entries = cs.n_entries;
   ta.D = cs.D;
   ta.coef_t = d_coef;
@@ -500,7 +555,7 @@ hc_status hc_track_batch(hc_system sys, const hc_tracker_settings *settings, con
     r->phase_cycles = pc;
   }
 #endif
-  e = tracker_launcher(N)(ta, sys->device, r->stream, &r->plan);
+  e = (wide ? tracker_launcher_wide(N) : tracker_launcher(N))(ta, sys->device, r->stream, &r->plan);
   if (e != cudaSuccess) return bail(cuda_fail(e, "tracker launch"));
   cudaEventRecord(r->ev[2], r->stream);
 

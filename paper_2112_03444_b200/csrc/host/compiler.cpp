@@ -208,7 +208,7 @@ static std::vector<int> bank_relabel(const std::vector<int> &lab, int Q, int L, 
   return perm;
 }
 
-hc_status compile_system(const hc_system_desc &d, CompiledSystem &cs, std::string &err) {
+hc_status compile_system(const hc_system_desc &d, CompiledSystem &cs, std::string &err, int lanes) {
   hc_status s = validate(d, err);
   if (s != HC_OK) return s;
   const int N = d.n_vars, P = d.n_params;
@@ -217,7 +217,7 @@ hc_status compile_system(const hc_system_desc &d, CompiledSystem &cs, std::strin
   cs.P = P;
   cs.ncoef_src = d.n_coefs;
   cs.n_terms = d.n_terms;
-  cs.L = lanes_for(N);
+  cs.L = lanes > 0 ? lanes : lanes_for(N);
 
   // ---- degrees ----
   cs.degrees.assign(N, 0);
@@ -477,7 +477,7 @@ hc_status compile_system(const hc_system_desc &d, CompiledSystem &cs, std::strin
   //      j at step j; structural zeros all read the single zero entry, a broadcast) ----
   {
     const int NE = cs.n_entries;
-    const int Lr = lanes_for(N);
+    const int Lr = cs.L;
     std::vector<int> lab((size_t)(N + 1) * Lr, NE);
     for (int j = 0; j <= N; ++j)
       for (int r = 0; r < Lr && r < N; ++r) {

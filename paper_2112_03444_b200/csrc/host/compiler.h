@@ -31,7 +31,8 @@ struct CompiledSystem {
 };
 
 // Returns HC_OK or an error code with a message in `err`.
-hc_status compile_system(const hc_system_desc &d, CompiledSystem &out, std::string &err);
+// lanes: lanes per track (0 = lanes_for(N); 32 = the wide latency layout for N <= 16)
+hc_status compile_system(const hc_system_desc &d, CompiledSystem &out, std::string &err, int lanes = 0);
 
 // Descriptor of the total-degree homotopy system built from a constant-coefficient target
 // (SURVEY.md §8(b) "Total degree is a PH"): params = (G x^d coefficients [N], G constants [N],

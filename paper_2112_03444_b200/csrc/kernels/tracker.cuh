@@ -48,10 +48,13 @@ constexpr unsigned FULL = 0xffffffffu;
 #ifndef HCB_MAXW_MID   // warps per CTA for 15 <= N <= 20 (A/B experiments override it)
 #define HCB_MAXW_MID 12
 #endif
-template <int N>
+// LW: lanes per track -- lanes_for(N) (throughput layout, 32/LW tracks per warp) or 32 (the wide
+// latency layout for N <= 16: one track per warp, its op list and monomial program spread over 32
+// lanes and REDUX-based reductions; chosen by the host for batches that under-fill the GPU).
+template <int N, int LW = lanes_for(N)>
 struct TrackerShape {
-  static constexpr bool HY = hy_layout(N);
-  static constexpr int L = lanes_for(N);
+  static constexpr bool HY = hy_layout(N) && LW == lanes_for(N);
+  static constexpr int L = LW;
   static constexpr int E = HY ? N - 16 : 0;   // extra rows (hybrid layout)
   static constexpr int NC = HY ? 2 : 1;       // unknown components per lane
   static constexpr int MAXW = HY ? 8 : (N >= 15 && N <= 20) ? HCB_MAXW_MID : 4;
@@ -554,7 +557,7 @@ __device__ __forceinline__ bool eval_solve(const TrackArgs &A, const uint2 *__re
   // ---- stage x (monomial slots 0..N-1) and coefficient values c(t) (all slots), c'(t) (rhs
   //      slots) by Horner on the prologue's polynomials in t ----
   HCB_T(c0);
-  constexpr int E = TrackerShape<N>::E;
+  constexpr int E = TrackerShape<N, L>::E;
   if (r < N) mono[r] = xr[0];
   if constexpr (NC == 2) {
     if (r < E) mono[16 + r] = xr[NC - 1];
@@ -662,11 +665,11 @@ __device__ __forceinline__ bool eval_solve(const TrackArgs &A, const uint2 *__re
 // ------------------------------------------------------------------------------------------
 // The persistent tracker kernel.
 // ------------------------------------------------------------------------------------------
-template <int N>
+template <int N, int LW>
 __device__ __forceinline__ void track_body(const TrackArgs &A) {
-  constexpr int L = TrackerShape<N>::L;
-  constexpr int NC = TrackerShape<N>::NC;   // unknown components per lane (2: hybrid layout)
-  constexpr int E = TrackerShape<N>::E;
+  constexpr int L = TrackerShape<N, LW>::L;
+  constexpr int NC = TrackerShape<N, LW>::NC;   // unknown components per lane (2: hybrid layout)
+  constexpr int E = TrackerShape<N, LW>::E;
   constexpr int TPW = 32 / L;
   extern __shared__ __align__(16) unsigned char smem_raw[];
 
@@ -958,26 +961,29 @@ __device__ __forceinline__ void track_body(const TrackArgs &A) {
 #ifndef HCB_MID_MAXREG
 #define HCB_MID_MAXREG 0
 #endif
-template <int N>
-constexpr bool use_maxnreg() { return HCB_MID_MAXREG > 0 && N >= 15 && N <= 20 && !hy_layout(N); }
-template <int N>
-__global__ void __launch_bounds__(TrackerShape<N>::MAXW * 32, TrackerShape<N>::MINB) hc_track_kernel(const TrackArgs A) {
-  track_body<N>(A);
+template <int N, int LW>
+constexpr bool use_maxnreg() {
+  return HCB_MID_MAXREG > 0 && N >= 15 && N <= 20 && !hy_layout(N) && LW == lanes_for(N);
 }
-template <int N>
+template <int N, int LW>
+__global__ void __launch_bounds__(TrackerShape<N, LW>::MAXW * 32, TrackerShape<N, LW>::MINB)
+    hc_track_kernel(const TrackArgs A) {
+  track_body<N, LW>(A);
+}
+template <int N, int LW>
 __global__ void __maxnreg__(HCB_MID_MAXREG > 0 ? HCB_MID_MAXREG : 128) hc_track_kernel_r(const TrackArgs A) {
-  track_body<N>(A);
+  track_body<N, LW>(A);
 }
 
-template <int N>
+template <int N, int LW = lanes_for(N)>
 cudaError_t launch_tracker_n(const TrackArgs &A, int device, cudaStream_t stream, TrackerPlan *plan) {
-  constexpr int L = TrackerShape<N>::L;
+  constexpr int L = TrackerShape<N, LW>::L;
   constexpr int TPW = 32 / L;
   const size_t tables = table_bytes(A.Q, L, A.n_mono - (N + 1), N) + align16((size_t)2 * A.n_entries);
   const size_t per_warp = (size_t)TPW * slot_bytes(N, A.ncoef, A.ncoef_src, A.n_mono, A.n_entries + 1);
   int smem_max = 0;
   cudaDeviceGetAttribute(&smem_max, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
-  int warps = TrackerShape<N>::MAXW;
+  int warps = TrackerShape<N, LW>::MAXW;
   if (const char *ev = getenv("HC_TRACKER_WARPS")) {   // experiment override (<= compile-time max)
     const int w = atoi(ev);
     if (w >= 1 && w < warps) warps = w;
@@ -986,8 +992,8 @@ cudaError_t launch_tracker_n(const TrackArgs &A, int device, cudaStream_t stream
   const size_t smem = tables + warps * per_warp;
   if (smem > (size_t)smem_max) return cudaErrorInvalidConfiguration;
   const void *fn;
-  if constexpr (use_maxnreg<N>()) fn = (const void *)hc_track_kernel_r<N>;
-  else fn = (const void *)hc_track_kernel<N>;
+  if constexpr (use_maxnreg<N, LW>()) fn = (const void *)hc_track_kernel_r<N, LW>;
+  else fn = (const void *)hc_track_kernel<N, LW>;
   cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   int per_sm = 0;
@@ -1007,8 +1013,8 @@ cudaError_t launch_tracker_n(const TrackArgs &A, int device, cudaStream_t stream
     plan->ctas = (int)ctas;
     plan->smem_bytes = smem;
   }
-  if constexpr (use_maxnreg<N>()) hc_track_kernel_r<N><<<(unsigned)ctas, warps * 32, smem, stream>>>(A);
-  else hc_track_kernel<N><<<(unsigned)ctas, warps * 32, smem, stream>>>(A);
+  if constexpr (use_maxnreg<N, LW>()) hc_track_kernel_r<N, LW><<<(unsigned)ctas, warps * 32, smem, stream>>>(A);
+  else hc_track_kernel<N, LW><<<(unsigned)ctas, warps * 32, smem, stream>>>(A);
   return cudaGetLastError();
 }
 

@@ -4,6 +4,10 @@ namespace hcb {
 cudaError_t launch_tracker_12(const TrackArgs &A, int device, cudaStream_t s, TrackerPlan *p) {
   return launch_tracker_n<12>(A, device, s, p);
 }
+// the wide latency layout (one track per warp on 32 lanes), chosen for batches that under-fill the GPU
+cudaError_t launch_tracker_wide_12(const TrackArgs &A, int device, cudaStream_t s, TrackerPlan *p) {
+  return launch_tracker_n<12, 32>(A, device, s, p);
+}
 cudaError_t launch_zgesv_12(int64_t batch, const double2 *A, const double2 *b, double2 *x, int32_t *info,
                            double pivot_rel, cudaStream_t s) {
   return launch_zgesv_n<12>(batch, A, b, x, info, pivot_rel, s);

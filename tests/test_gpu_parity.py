@@ -187,6 +187,45 @@ def test_eco12_table1_count(hc, orc):
     assert r[st == 0, 0].max() < 1e-10
 
 
+@pytest.mark.parametrize("lanes", ["narrow", "wide"])
+def test_lane_layouts_parity(hc, orc, monkeypatch, lanes):
+    """Both lane layouts (throughput: next_pow2(N) lanes per track; wide latency layout: 32 lanes per
+    track) give the oracle's sets: katsura-6 (64), cyclic-7 (924), 4-view on 3 instances (296 each)."""
+    monkeypatch.setenv("HC_LANES", lanes)
+    for d, count, seed in ((systems.katsura(6), 64, 0), (systems.cyclic(7), 924, 2)):
+        gam = rng.gamma(seed)
+        res, _ = run_td(hc, d, gam)
+        assert res.launch()["lanes_per_track"] == (32 if lanes == "wide" else 8)
+        B = gpu_set(orc, res)
+        ref = orc.track(orc.td_homotopy(d, gam), orc.td_start(d.degrees()))
+        A = orc.dedup(orc.finite_solutions(ref))[0]
+        assert len(A) == count
+        assert_same_set(orc, A, B, f"{d.name} ({lanes})")
+    d = systems.nview_triangulation(4)
+    start = fixtures.read_solutions(fixtures.fixture_path("fourview_start.sols"))
+    p0 = fixtures.read_params(fixtures.fixture_path("fourview_p0.params"))
+    p1s, _ = rng.fourview_batch(3)
+    res = run_ph(hc, d, start, p0, p1s)
+    assert res.launch()["lanes_per_track"] == (32 if lanes == "wide" else 16)
+    ref = orc.track(orc.ph_homotopy(d, p0), start, p1s=p1s)
+    for b in range(3):
+        A = orc.dedup(orc.finite_solutions(ref, b))[0]
+        assert_same_set_r21(orc, d, p1s[b], A, gpu_set(orc, res, b), f"4-view {b} ({lanes})")
+
+
+def test_lane_layout_policy(hc, monkeypatch):
+    """Auto policy: small single-instance solves run in the wide latency layout, full batches in the
+    throughput layout; N > 16 always in the throughput layout."""
+    monkeypatch.delenv("HC_LANES", raising=False)
+    res, _ = run_td(hc, systems.katsura(6), rng.gamma(0))
+    assert res.launch()["lanes_per_track"] == 32
+    d = systems.nview_triangulation(4)
+    start = fixtures.read_solutions(fixtures.fixture_path("fourview_start.sols"))
+    p0 = fixtures.read_params(fixtures.fixture_path("fourview_p0.params"))
+    p1s, _ = rng.fourview_batch(64)
+    assert run_ph(hc, d, start, p0, p1s).launch()["lanes_per_track"] == 16
+
+
 def test_counters_and_determinism(hc, orc):
     d = systems.katsura(5)
     gam = rng.gamma(7)
