@@ -955,23 +955,12 @@ __device__ __forceinline__ void track_body(const TrackArgs &A) {
 #endif
 }
 
-// Kernel entry points.  The register budget comes from __launch_bounds__ (MAXW warps, MINB CTAs per
-// SM), or, for 15 <= N <= 20 when HCB_MID_MAXREG is set, from an explicit __maxnreg__ (which allows
-// warp counts that are not a multiple of 4 at a budget between 128 and 168 registers).
-#ifndef HCB_MID_MAXREG
-#define HCB_MID_MAXREG 0
-#endif
-template <int N, int LW>
-constexpr bool use_maxnreg() {
-  return HCB_MID_MAXREG > 0 && N >= 15 && N <= 20 && !hy_layout(N) && LW == lanes_for(N);
-}
+// Kernel entry point: the register budget comes from __launch_bounds__ (MAXW warps, MINB CTAs per
+// SM).  (An explicit __maxnreg__ entry for 13-15 warps at 136-152 registers was tried: the launch
+// configuration was rejected on the device.)
 template <int N, int LW>
 __global__ void __launch_bounds__(TrackerShape<N, LW>::MAXW * 32, TrackerShape<N, LW>::MINB)
     hc_track_kernel(const TrackArgs A) {
-  track_body<N, LW>(A);
-}
-template <int N, int LW>
-__global__ void __maxnreg__(HCB_MID_MAXREG > 0 ? HCB_MID_MAXREG : 128) hc_track_kernel_r(const TrackArgs A) {
   track_body<N, LW>(A);
 }
 
@@ -991,9 +980,7 @@ cudaError_t launch_tracker_n(const TrackArgs &A, int device, cudaStream_t stream
   while (warps > 1 && tables + warps * per_warp > (size_t)smem_max) --warps;
   const size_t smem = tables + warps * per_warp;
   if (smem > (size_t)smem_max) return cudaErrorInvalidConfiguration;
-  const void *fn;
-  if constexpr (use_maxnreg<N, LW>()) fn = (const void *)hc_track_kernel_r<N, LW>;
-  else fn = (const void *)hc_track_kernel<N, LW>;
+  const void *fn = (const void *)hc_track_kernel<N, LW>;
   cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   int per_sm = 0;
@@ -1013,8 +1000,7 @@ cudaError_t launch_tracker_n(const TrackArgs &A, int device, cudaStream_t stream
     plan->ctas = (int)ctas;
     plan->smem_bytes = smem;
   }
-  if constexpr (use_maxnreg<N, LW>()) hc_track_kernel_r<N, LW><<<(unsigned)ctas, warps * 32, smem, stream>>>(A);
-  else hc_track_kernel<N, LW><<<(unsigned)ctas, warps * 32, smem, stream>>>(A);
+  hc_track_kernel<N, LW><<<(unsigned)ctas, warps * 32, smem, stream>>>(A);
   return cudaGetLastError();
 }
 
