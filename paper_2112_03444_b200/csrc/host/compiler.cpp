@@ -9,8 +9,9 @@
 //  * s_k is folded into the coefficient (a slot per distinct (c_j, s_k)), evaluated by the
 //    prologue as a polynomial in t;
 //  * the products x_{m1} ... x_{mM} are shared: every monomial any entry needs is computed once
-//    per evaluation from a parent of degree one less (a monomial program, levels by degree; the
-//    unknowns and the constant one are its first N+1 slots);
+//    per evaluation as the product of two monomials of lower degree (a monomial program in
+//    ceil(log2(max degree)) dependent levels; the unknowns and the constant one are its first N+1
+//    slots);
 //  * entries are bin-packed over the L lanes of a track (longest-processing-time first), so each
 //    lane runs ~(total terms / L) uniform ops out(row,col) += coef[slot] * mono[k].
 #include "compiler.h"
@@ -307,7 +308,22 @@ hc_status compile_system(const hc_system_desc &d, CompiledSystem &cs, std::strin
   }
   cs.D = D;
 
-  // ---- monomial program: closure under "divide by one variable", evaluated degree by degree ----
+  // ---- monomial program: every needed monomial of degree d >= 2 is one complex product of two
+  //      monomials from earlier levels.  Log depth: level(d) = ceil(log2 d) (degree 2 -> 1, 3-4 -> 2,
+  //      5-8 -> 3), i.e. ceil(log2 maxdeg) dependent levels (a warp sync each) instead of
+  //      maxdeg - 1.  The split e = a * b (deg a >= deg b, level(deg a) < level(d)) prefers factors
+  //      that are needed anyway (shared work), then the most balanced split. ----
+  auto log_level = [](int dg) {
+    int l = 0;
+    while ((1 << l) < dg) ++l;
+    return l;   // 1 -> 0, 2 -> 1, 3..4 -> 2, 5..8 -> 3
+  };
+  // log depth only when it saves at least two levels: with a single level saved the products whose
+  // both operands are arbitrary monomials (instead of monomial x variable) cost more in bank
+  // conflicts than the saved level (measured: trifocal, max degree 5, +1.5 %; cyclic-7, max degree
+  // 7, 6 -> 3 levels, -3 %).  Otherwise the classic program: degree d = (degree d-1) x variable.
+  const bool logdepth = maxdeg >= 2 && log_level(maxdeg) + 2 <= maxdeg - 1;
+  auto level_of = [&](int dg) { return logdepth ? log_level(dg) : dg - 1; };
   std::map<Expo, int> mono_idx;
   std::set<Expo> need;
   for (auto &kv : entries)
@@ -315,28 +331,61 @@ hc_status compile_system(const hc_system_desc &d, CompiledSystem &cs, std::strin
       if (deg_of(o.mono) >= 2) need.insert(o.mono);
   std::vector<std::set<Expo>> by_deg(maxdeg + 1);
   for (const Expo &e : need) by_deg[deg_of(e)].insert(e);
-  std::map<Expo, std::pair<Expo, int>> parent;   // monomial -> (parent, var)
+  std::map<Expo, std::pair<Expo, Expo>> split;   // monomial -> (a, b)
   for (int dg = maxdeg; dg >= 2; --dg) {
+    const int T = level_of(dg);
     for (const Expo &e : by_deg[dg]) {
-      // prefer a parent that is already needed (shared work), else the one dividing by the
-      // highest variable; every degree-2 monomial has a variable as parent
-      int best = -1;
-      for (int v = 0; v < N && best < 0; ++v) {
-        if (!e[v]) continue;
-        Expo p2 = e;
-        p2[v] -= 1;
-        if (dg - 1 < 2 || by_deg[dg - 1].count(p2)) best = v;
+      if (!logdepth) {
+        // classic program: a parent of degree d-1 times a variable; prefer a parent that is already
+        // needed (shared work, lowest variable first), else divide by the highest variable
+        int best = -1;
+        for (int v = 0; v < N && best < 0; ++v) {
+          if (!e[v]) continue;
+          Expo p2 = e;
+          p2[v] -= 1;
+          if (dg - 1 < 2 || by_deg[dg - 1].count(p2)) best = v;
+        }
+        if (best < 0)
+          for (int v = N - 1; v >= 0; --v)
+            if (e[v]) {
+              best = v;
+              break;
+            }
+        Expo p2 = e, xv(N, 0);
+        p2[best] -= 1;
+        xv[best] = 1;
+        if (dg - 1 >= 2) by_deg[dg - 1].insert(p2);
+        split[e] = {p2, xv};
+        continue;
       }
-      if (best < 0)
-        for (int v = N - 1; v >= 0; --v)
-          if (e[v]) {
-            best = v;
-            break;
-          }
-      Expo p2 = e;
-      p2[best] -= 1;
-      if (dg - 1 >= 2) by_deg[dg - 1].insert(p2);
-      parent[e] = {p2, best};
+      // log depth: enumerate sub-multisets a of e (the larger factor); b = e - a
+      std::vector<int> fac;
+      for (int v = 0; v < N; ++v)
+        for (int c = 0; c < e[v]; ++c) fac.push_back(v);
+      std::set<Expo> seen;
+      int best_score = -1;
+      std::pair<Expo, Expo> best;
+      const int nf = (int)fac.size();
+      for (int mask = 1; mask < (1 << nf); ++mask) {
+        const int da = __builtin_popcount((unsigned)mask), db = dg - da;
+        if (db < 1 || da < db || level_of(da) >= T) continue;
+        Expo a(N, 0);
+        for (int i = 0; i < nf; ++i)
+          if (mask >> i & 1) a[fac[i]] += 1;
+        if (!seen.insert(a).second) continue;
+        Expo b = e;
+        for (int v = 0; v < N; ++v) b[v] -= a[v];
+        auto have = [&](const Expo &m) { const int dm = deg_of(m); return dm < 2 || by_deg[dm].count(m) > 0; };
+        // score: factors already present count most, then balance (larger deg b)
+        const int score = 100 * ((int)have(a) + (int)have(b)) + db;
+        if (score > best_score) {
+          best_score = score;
+          best = {a, b};
+        }
+      }
+      split[e] = best;
+      if (deg_of(best.first) >= 2) by_deg[deg_of(best.first)].insert(best.first);
+      if (deg_of(best.second) >= 2) by_deg[deg_of(best.second)].insert(best.second);
     }
   }
   auto index_of = [&](const Expo &e) -> int {
@@ -348,18 +397,25 @@ hc_status compile_system(const hc_system_desc &d, CompiledSystem &cs, std::strin
     return mono_idx.at(e);
   };
   int next = N + 1;
-  cs.n_levels = std::max(0, maxdeg - 1);
+  cs.n_levels = maxdeg >= 2 ? level_of(maxdeg) : 0;
   if (cs.n_levels > MAX_LEVELS) {
     err = "monomial degree too large";
     return HC_E_TOO_LARGE;
   }
-  for (int dg = 2; dg <= maxdeg; ++dg) {
-    for (const Expo &e : by_deg[dg]) {
-      mono_idx[e] = next++;
-      const auto &pv = parent.at(e);
-      cs.mono_prog.push_back((uint32_t)index_of(pv.first) | ((uint32_t)pv.second << 16));
+  for (int l = 1; l <= cs.n_levels; ++l) {
+    for (int dg = 2; dg <= maxdeg; ++dg) {
+      if (level_of(dg) != l) continue;
+      for (const Expo &e : by_deg[dg]) mono_idx[e] = next++;
     }
-    cs.level_end[dg - 2] = next;
+    // program entries in index order (the loop above numbers a level's monomials consecutively)
+    for (int dg = 2; dg <= maxdeg; ++dg) {
+      if (level_of(dg) != l) continue;
+      for (const Expo &e : by_deg[dg]) {
+        const auto &ab = split.at(e);
+        cs.mono_prog.push_back((uint32_t)index_of(ab.first) | ((uint32_t)index_of(ab.second) << 16));
+      }
+    }
+    cs.level_end[l - 1] = next;
   }
   cs.n_mono = next;
   if (cs.n_mono > 65535) {
@@ -431,19 +487,19 @@ hc_status compile_system(const hc_system_desc &d, CompiledSystem &cs, std::strin
     std::vector<std::vector<int>> sg(2);
     for (int j = 0; j < cs.ncoef; ++j) sg[j < nsrc ? 0 : 1].push_back(j);
     const std::vector<int> ps = bank_relabel(sl, Q, L, cs.ncoef, sg, 2112, 40000);
-    std::vector<std::vector<int>> mg(std::max(0, maxdeg - 1));
+    std::vector<std::vector<int>> mg(std::max(1, cs.n_levels));
     for (int k = N + 1, lvl = 0; k < cs.n_mono; ++k) {
       while (k >= cs.level_end[lvl]) ++lvl;
       mg[lvl].push_back(k);
     }
     const std::vector<int> pm = bank_relabel(mo, Q, L, cs.n_mono, mg, 3444, 40000);
     for (auto &w : cs.ops) w.x = (uint32_t)ps[w.x & 0xFFFFu] | ((uint32_t)pm[w.x >> 16] << 16);
-    // monomial program in the new numbering (permutations stay within a degree level)
+    // monomial program in the new numbering (permutations stay within a level)
     std::vector<uint32_t> prog(cs.mono_prog.size());
     for (int k = N + 1; k < cs.n_mono; ++k) {
       const uint32_t e = cs.mono_prog[k - N - 1];
-      const int parent = (int)(e & 0xFFFFu), var = (int)(e >> 16);
-      prog[pm[k] - N - 1] = (uint32_t)pm[parent] | ((uint32_t)var << 16);
+      const int fa = (int)(e & 0xFFFFu), fb = (int)(e >> 16);
+      prog[pm[k] - N - 1] = (uint32_t)pm[fa] | ((uint32_t)pm[fb] << 16);
     }
     cs.mono_prog = prog;
     // coefficient slots in the new numbering; pad the slot count to a multiple of 8 so that the

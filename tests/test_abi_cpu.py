@@ -45,10 +45,13 @@ def test_settings_defaults_match_readings(hc):
 
 def mono_factors(prog, N):
     """Variable multiset of every monomial-table entry: k < N -> [k], k == N -> [] (constant one),
-    k > N -> factors(parent) + [var] (program order is by degree, parents first)."""
+    k > N -> factors(a) + factors(b) for the entry's two factor indices (program order is by
+    level, factors first)."""
     f = [[k] for k in range(N)] + [[]]
     for e in prog:
-        f.append(f[int(e) & 0xFFFF] + [int(e) >> 16])
+        a, b = int(e) & 0xFFFF, int(e) >> 16
+        assert a < len(f) and b < len(f)   # factors come from earlier entries
+        f.append(f[a] + f[b])
     return f
 
 
