@@ -1,6 +1,6 @@
 """Benchmark: device-timed tracks/s and instances/s of the fused B200 HC tracker.
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--config trifocal|fourview|fivepoint|cyclic7|katsura6|eco12]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config trifocal|fourview|fivepoint|cyclic7|cyclic7ph|katsura6|eco12]
                   [--instances B] [--impl ours|reference] [--no-e2e] [--no-cpu-baseline]
 
 One "step" = one pass of the whole hot path (coefficient prologue + fused tracker: every
@@ -64,6 +64,15 @@ def make_workload(name: str, B: int, rank: int):
         meta = {"workload": f"5-point rel. pose + depth (16x16, Table 2 P:492; reading R24) PH, S=40 x {B} "
                             f"planted instances per GPU (SURVEY N2)"}
         return d, start, p0, p1s, {}, meta
+    if name == "cyclic7ph":
+        d = systems.cyclic_family(7)
+        start = fixtures.read_solutions(fixtures.fixture_path("cyclic7_start.sols"))
+        p0 = fixtures.read_params(fixtures.fixture_path("cyclic7_p0.params"))
+        p1s = systems.cyclic_family_target(7)[None]   # one instance: the standard cyclic-7 (Table 1)
+        meta = {"workload": f"cyclic-7 parameter homotopy from the oracle monodromy start (S={start.shape[0]}, "
+                            f"coefficient family) to the standard cyclic-7, single instance (configs[1] system, "
+                            f"the paper's monodromy-start workflow P:478)"}
+        return d, start, p0, p1s, {}, meta
     if name in ("cyclic7", "katsura6", "eco12"):
         d = {"cyclic7": lambda: systems.cyclic(7), "katsura6": lambda: systems.katsura(6),
              "eco12": lambda: systems.eco(12)}[name]()
@@ -124,7 +133,7 @@ def oracle_sample(name: str, budget_s: float, rank: int = 0, B: int = 1, nthread
     -- all tracks of the first instances of the batch.  Returns (tracks/s, cores, sample description)."""
     import oracle
     max_inst = 256
-    d, start, p0, p1s, _, _ = make_workload(name, 1 if name in ("trifocal",) else max_inst, rank)
+    d, start, p0, p1s, _, _ = make_workload(name, 1 if name in ("trifocal", "cyclic7ph") else max_inst, rank)
     nthreads = nthreads or oracle.nthreads_default()
     if start is None:   # TD single instance
         from hc_inputs import rng
@@ -216,6 +225,8 @@ def run_ours(args):
 
     B = args.instances
     d, start, p0, p1s, _, meta = make_workload(args.config, B, rank)
+    if p1s is not None:
+        B = p1s.shape[0]   # single-instance workloads fix their own batch
     if start is None:
         from hc_inputs import rng
         sysh = hc.System.total_degree_homotopy(d, device=local_rank)
@@ -333,7 +344,7 @@ def run_ours(args):
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         v, cores, sample = oracle_sample(args.config, args.cpu_budget_s)
         cpu = {"value": v, "unit": "tracks/s", "cores": cores, "kind": "oracle", "sample": sample}
-        if args.config in ("katsura6", "cyclic7", "eco12"):   # TD benchmarks also on 1 thread
+        if args.config in ("katsura6", "cyclic7", "cyclic7ph", "eco12"):   # benchmarks also on 1 thread
             v1, _, sample1 = oracle_sample(args.config, min(args.cpu_budget_s, 5.0), nthreads=1)
             cpu["single_thread"] = {"value": v1, "unit": "tracks/s", "cores": 1, "sample": sample1}
 
@@ -371,7 +382,7 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=1)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", default="trifocal", choices=["trifocal", "fourview", "fivepoint", "cyclic7", "katsura6", "eco12"])
+    ap.add_argument("--config", default="trifocal", choices=["trifocal", "fourview", "fivepoint", "cyclic7", "cyclic7ph", "katsura6", "eco12"])
     ap.add_argument("--instances", type=int, default=1024)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--warmup-instances", type=int, default=16)

@@ -248,6 +248,7 @@ def fourview_complex_start(seed: int = 23, nv: int = 4):
 
 SEED_FIVEPOINT_INSTANCE = 6_000_000
 SEED_FIVEPOINT_MONODROMY = 13
+SEED_CYCLIC_MONODROMY = 17
 
 
 def fivepoint_project(x: np.ndarray, gam: np.ndarray) -> np.ndarray:
@@ -287,6 +288,24 @@ def fivepoint_instance(seed: int):
 def fivepoint_batch(n_instances: int, base: int = SEED_FIVEPOINT_INSTANCE):
     ps, xs = zip(*(fivepoint_instance(base + b) for b in range(n_instances)))
     return np.stack(ps), np.stack(xs)
+
+
+def cyclic_family_start(n: int = 7, seed: int = SEED_CYCLIC_MONODROMY):
+    """Planted generic complex (p0, x0) of systems.cyclic_family(n): x0 and p complex Gaussian, then
+    the first term's parameter of every equation is set so that x0 solves it (each equation is
+    linear in its parameters)."""
+    from .systems import cyclic_family
+    d = cyclic_family(n)
+    g = gen(seed)
+    x0 = complex_normal(g, n)
+    p = complex_normal(g, d.n_params)
+    mono = np.prod(x0[None, :] ** d.term_xexp, axis=1)          # term q's monomial at x0
+    coef_param = [int(np.nonzero(d.coef_pexp[d.coef_ptr[c]])[0][0]) for c in d.term_coef]
+    for i in range(n):
+        qs = [q for q in range(d.n_terms) if d.term_eq[q] == i]
+        rest = sum(p[coef_param[q]] * mono[q] for q in qs[1:])
+        p[coef_param[qs[0]]] = -rest / mono[qs[0]]
+    return p, x0
 
 
 def fivepoint_complex_start(seed: int = SEED_FIVEPOINT_MONODROMY):

@@ -65,6 +65,31 @@ def cyclic(n: int) -> SystemDesc:
     return desc_from_equations(eqs, name=f"cyclic-{n}", var_names=[f"x{i}" for i in range(n)])
 
 
+def cyclic_family(n: int) -> SystemDesc:
+    """cyclic-n with a free coefficient per term (the paper's monodromy + parameter
+    homotopy workflow, applied to the Table 1 benchmark P:467): the same monomial support as
+    cyclic(n), term q of the flattened term list multiplied by parameter p_q.  The standard cyclic-n
+    is the member cyclic_family_target(n) (all ones, the constant -1)."""
+    base = cyclic(n)
+    T = base.n_terms
+    eqs = [const(n, T, 0) for _ in range(n)]
+    for q in range(T):
+        i = int(base.term_eq[q])
+        m = var_p(n, T, q)
+        for v in range(n):
+            for _ in range(int(base.term_xexp[q, v])):
+                m = m * var_x(n, T, v)
+        eqs[i] = eqs[i] + m
+    return desc_from_equations(eqs, name=f"cyclic-{n}-family", var_names=[f"x{i}" for i in range(n)])
+
+
+def cyclic_family_target(n: int):
+    """Parameters of cyclic_family(n) that give the standard cyclic-n."""
+    import numpy as np
+    base = cyclic(n)
+    return np.array([complex(base.coef_w[base.coef_ptr[base.term_coef[q]]]) for q in range(base.n_terms)])
+
+
 def eco(n: int) -> SystemDesc:
     """eco-n (Table 1: eco-12, 12 unknowns, 1024 solutions; the paper cites the
     benchmark without writing it down -- standard economics-modelling family, reading R25):

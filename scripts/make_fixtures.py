@@ -4,6 +4,7 @@
   python scripts/make_fixtures.py trifocal   # trifocal monodromy from a planted (x0, p0)
   python scripts/make_fixtures.py fivepoint  # 5-point relpose + depth monodromy (reading R24)
   python scripts/make_fixtures.py eco12      # eco-12 TD solve (118,098 tracks) -> the oracle's finite set
+  python scripts/make_fixtures.py cyclic7    # cyclic-7 coefficient-family monodromy (Table 1: 924)
 
 This script imports only `oracle` and `hc_inputs`; the CUDA path never writes fixtures
 (prompt rule ③: no stored value comes from the CUDA path).  Start systems of the paper's
@@ -123,6 +124,20 @@ def make_fivepoint(max_loops: int = 40, stall_loops: int = 5, seed: int = rng.SE
 ECO12_GAMMA_SEED = 2
 
 
+def make_cyclic7(max_loops: int = 60, stall_loops: int = 4, seed: int = rng.SEED_CYCLIC_MONODROMY):
+    """Monodromy start set of the cyclic-7 coefficient family (systems.cyclic_family) at a planted
+    generic complex p0: the paper's start-system workflow (monodromy) for its Table 1
+    benchmark (cyclic-7: 924 solutions)."""
+    d = systems.cyclic_family(7)
+    p0, x0 = rng.cyclic_family_start(7, seed)
+    reps, full, loops = _monodromy(d, p0, x0, lambda x: [x], seed, max_loops, stall_loops, "cyclic7")
+    hdr = (f"cyclic-7 coefficient family start solutions at the planted complex p0 = rng.cyclic_family_start(7, {seed}).\n"
+           f"Written by scripts/make_fixtures.py (oracle only): monodromy, {loops} loops,\n"
+           f"{full.shape[0]} solutions (PAPER.md Table 1 P:467: cyclic-7 has 924).")
+    fixtures.write_solutions(fixtures.fixture_path("cyclic7_start.sols"), full, hdr)
+    fixtures.write_params(fixtures.fixture_path("cyclic7_p0.params"), p0, hdr)
+
+
 def make_eco12():
     """The oracle's finite solution set of eco-12 (Table 1: 1024 solutions), used by the GPU
     parity test as the expected set (the oracle needs minutes for 118,098 tracks)."""
@@ -150,3 +165,5 @@ if __name__ == "__main__":
         make_fivepoint()
     if "eco12" in what:
         make_eco12()
+    if "cyclic7" in what:
+        make_cyclic7()

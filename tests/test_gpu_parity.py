@@ -159,6 +159,23 @@ def test_cyclic7_parity(hc, orc):
     assert r[st == 0, 0].max() < 1e-10
 
 
+def test_cyclic7_monodromy_ph_parity(hc, orc):
+    """The paper's workflow for Table 1 (monodromy start): parameter homotopy from the oracle's
+    924-point monodromy start of the cyclic-7 coefficient family to the standard cyclic-7 (one
+    instance).  All 924 tracks converge to the oracle's total-degree solution set."""
+    d = systems.cyclic_family(7)
+    S = fixtures.read_solutions(fixtures.fixture_path("cyclic7_start.sols"))
+    p0 = fixtures.read_params(fixtures.fixture_path("cyclic7_p0.params"))
+    res = run_ph(hc, d, S, p0, systems.cyclic_family_target(7)[None])
+    st = res.status.cpu().numpy()[0]
+    assert np.all(st == 0), np.bincount(st)
+    B = gpu_set(orc, res)
+    td = orc.track(orc.td_homotopy(systems.cyclic(7), rng.gamma(2)), orc.td_start(systems.cyclic(7).degrees()))
+    A = orc.dedup(orc.finite_solutions(td))[0]
+    assert len(A) == 924
+    assert_same_set(orc, A, B, "cyclic-7 (monodromy start PH)")
+
+
 @pytest.mark.parametrize("n", [6, 8, 10])
 def test_eco_parity(hc, orc, n):
     """eco-n (reading R25): 2^(n-2) solutions, the same set as the oracle on the same gamma."""

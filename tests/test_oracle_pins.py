@@ -266,6 +266,30 @@ def test_cyclic7_924(orc):
     assert _cyclic_closed(U, 7)
 
 
+def test_cyclic7_family_monodromy_fixture(orc):
+    """The monodromy start set of the cyclic-7 coefficient family (fixtures/cyclic7_start.sols,
+    written by scripts/make_fixtures.py from the oracle) has 924 distinct solutions (= Table 1
+    P:467), each solving F(x; p0) by the defining sum; the parameter homotopy from it to the standard
+    cyclic-7 reaches the same 924-point set as the total-degree homotopy."""
+    from hc_inputs import fixtures
+    d = systems.cyclic_family(7)
+    S = fixtures.read_solutions(fixtures.fixture_path("cyclic7_start.sols"))
+    p0 = fixtures.read_params(fixtures.fixture_path("cyclic7_p0.params"))
+    assert S.shape == (924, 7)
+    U, mult = orc.dedup(S)
+    assert len(U) == 924 and mult.max() == 1
+    for x in S[::37]:
+        assert max(abs(eval_poly(f, x, p0)) for f in d.polys) < 1e-10
+    ph = orc.track(orc.ph_homotopy(d, p0), S, p1s=systems.cyclic_family_target(7)[None])
+    assert np.all(ph.status == orc.CONVERGED)
+    B = orc.dedup(orc.finite_solutions(ph))[0]
+    td = orc.track(orc.td_homotopy(systems.cyclic(7), rng.gamma(CYCLIC7_GAMMA_SEED)),
+                   orc.td_start(systems.cyclic(7).degrees()))
+    A = orc.dedup(orc.finite_solutions(td))[0]
+    ok, ua, ub = orc.match_sets(A, B, tol=1e-8)
+    assert ok and len(B) == 924, (len(A), len(B), ua, ub)
+
+
 def test_eco3_closed_form(orc):
     """eco-3 (reading R25) by hand: x1 + x2 + 1 = 0, x2 x3 = 2, (x1 + x1 x2) x3 = 1 give
     2 x2^2 + 5 x2 + 2 = 0, i.e. (x1, x2, x3) = (-1/2, -1/2, -4) and (1, -2, -1)."""
