@@ -72,10 +72,6 @@ __device__ __forceinline__ double2 cfma(double2 a, double2 b, double2 c) {
 __device__ __forceinline__ double2 cfms(double2 c, double2 a, double2 b) {
   return make_double2(fma(-a.x, b.x, fma(a.y, b.y, c.x)), fma(-a.x, b.y, fma(-a.y, b.x, c.y)));
 }
-// -(a * b)
-__device__ __forceinline__ double2 cmul_neg(double2 a, double2 b) {
-  return make_double2(fma(-a.x, b.x, a.y * b.y), fma(-a.x, b.y, -a.y * b.x));
-}
 __device__ __forceinline__ double abs2(double2 a) { return fma(a.x, a.x, a.y * a.y); }
 // 1/x for x > 0: MUFU reciprocal estimate + two Newton steps (full FP64 accuracy, no slow-path
 // call; non-finite or zero x gives a non-finite or huge result, and such pivots fail the
@@ -214,6 +210,7 @@ __device__ __forceinline__ bool lu_rows(double2 (&a)[N + 1], int r, int seg, dou
                                         double pivot_rel, double lane_max, double2 &y) {
   bool used = (r >= N);
   int mystep = used ? N : -1;
+  double2 myinv = make_double2(0.0, 0.0);
   // lane_max: max |A_ij|^2 over the entries this lane holds or produced (NaN entries are ignored by
   // fmax; they make the solve fail through the non-finite solution check)
   const double am = seg_max<L>(lane_max);
@@ -231,22 +228,19 @@ __device__ __forceinline__ bool lu_rows(double2 (&a)[N + 1], int r, int seg, dou
     const double2 inv = shfl2(spec, p, L);
     const double2 u1 = shfl2(a[k + 1], p, L);
     const bool me = (r == p);
-    if (me) {   // the pivot lane publishes the rest of its row (columns k+2..N) through shared memory,
-                // and keeps 1/pivot in the buffer's free slot k (never written by a later column)
+    if (me) {   // the pivot lane publishes the rest of its row (columns k+2..N) through shared memory
 #pragma unroll
       for (int j = k + 2; j <= N; ++j) pr[j] = a[j];
-      pr[k] = spec;
       used = true;
       mystep = k;
+      myinv = spec;
     }
     // Gauss-Jordan: every row except the pivot row eliminates column k -- the rows pivoted earlier
     // too, which in this one-row-per-lane layout costs no extra instruction (the whole warp runs
     // the update anyway) and removes the sequential back-substitution.  Padding rows are zero.
-    // The multiplier is kept negated (nl = -a_rk / pivot) so every update is a plain complex FMA
-    // whose operand negations are free in DFMA.
-    const double2 nlc = cmul_neg(a[k], inv);
-    const double2 nl = me ? make_double2(0.0, 0.0) : nlc;
-    a[k + 1] = cfma(nl, u1, a[k + 1]);   // column k+1 first (k + 1 == N: the right-hand side)
+    const double2 lc = cmul(a[k], inv);
+    const double2 l = me ? make_double2(0.0, 0.0) : lc;
+    a[k + 1] = cfms(a[k + 1], l, u1);   // column k+1 first (k + 1 == N: the right-hand side)
     if (k + 1 < N) {
       double v = abs2(a[k + 1]);
       if (used || (L < 32 && !(v >= 0.0))) v = -1.0;   // NaN is never a pivot (the REDUX path excludes it itself)
@@ -263,19 +257,14 @@ __device__ __forceinline__ bool lu_rows(double2 (&a)[N + 1], int r, int seg, dou
           if (j0 + i <= N) u[i] = pr[j0 + i];
 #pragma unroll
         for (int i = 0; i < 4; ++i)
-          if (j0 + i <= N) a[j0 + i] = cfma(nl, u[i], a[j0 + i]);
+          if (j0 + i <= N) a[j0 + i] = cfms(a[j0 + i], l, u[i]);
       }
     }
   }
   __syncwarp();
-  // ---- the system is now diagonal in pivot order: x_{mystep} = b' / pivot, routed through shared
-  //      memory (1/pivot of step m sits in slot m of buffer m & 1; the solution goes to buffer 0,
-  //      and no lane's write hits another lane's 1/pivot slot) ----
+  // ---- the system is now diagonal in pivot order: x_{mystep} = b' / pivot, routed through shared memory ----
   double2 *xsol = prow;
-  if (mystep < N) {
-    const double2 myinv = prow[(mystep & 1) * (N + 1) + mystep];
-    xsol[mystep] = cmul(a[N], myinv);
-  }
+  if (mystep < N) xsol[mystep] = cmul(a[N], myinv);
   __syncwarp();
   const double2 sol = (r < N) ? xsol[r] : make_double2(0.0, 0.0);
   y = sol;
