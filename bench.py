@@ -1,6 +1,6 @@
 """Benchmark: device-timed tracks/s and instances/s of the fused B200 HC tracker.
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--config trifocal|fourview|fivepoint|cyclic7|cyclic7ph|katsura6|eco12]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config trifocal|fourview|fivepoint|p3p|cyclic7|cyclic7ph|katsura6|eco12]
                   [--instances B] [--impl ours|reference] [--no-e2e] [--no-cpu-baseline]
 
 One "step" = one pass of the whole hot path (coefficient prologue + fused tracker: every
@@ -63,6 +63,14 @@ def make_workload(name: str, B: int, rank: int):
         p1s = np.stack([rng.fivepoint_instance(rng.SEED_FIVEPOINT_INSTANCE + rank * B + b)[0] for b in range(B)])
         meta = {"workload": f"5-point rel. pose + depth (16x16, Table 2 P:492; reading R24) PH, S=40 x {B} "
                             f"planted instances per GPU (SURVEY N2)"}
+        return d, start, p0, p1s, {}, meta
+    if name == "p3p":
+        d = systems.p3p_depth()
+        start = fixtures.read_solutions(fixtures.fixture_path("p3p_start.sols"))
+        p0 = fixtures.read_params(fixtures.fixture_path("p3p_p0.params"))
+        p1s = np.stack([rng.p3p_instance(rng.SEED_P3P_INSTANCE + rank * B + b)[0] for b in range(B)])
+        meta = {"workload": f"P3P absolute pose, depth form (3x3, Eq. P3PafterElim P:260-273, Table 2 P:512) PH, "
+                            f"S={start.shape[0]} x {B} planted instances per GPU (SURVEY N2)"}
         return d, start, p0, p1s, {}, meta
     if name == "cyclic7ph":
         d = systems.cyclic_family(7)
@@ -382,7 +390,7 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=1)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", default="trifocal", choices=["trifocal", "fourview", "fivepoint", "cyclic7", "cyclic7ph", "katsura6", "eco12"])
+    ap.add_argument("--config", default="trifocal", choices=["trifocal", "fourview", "fivepoint", "p3p", "cyclic7", "cyclic7ph", "katsura6", "eco12"])
     ap.add_argument("--instances", type=int, default=1024)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--warmup-instances", type=int, default=16)

@@ -249,6 +249,8 @@ def fourview_complex_start(seed: int = 23, nv: int = 4):
 SEED_FIVEPOINT_INSTANCE = 6_000_000
 SEED_FIVEPOINT_MONODROMY = 13
 SEED_CYCLIC_MONODROMY = 17
+SEED_P3P_INSTANCE = 7_000_000
+SEED_P3P_P0 = 31
 
 
 def fivepoint_project(x: np.ndarray, gam: np.ndarray) -> np.ndarray:
@@ -290,12 +292,11 @@ def fivepoint_batch(n_instances: int, base: int = SEED_FIVEPOINT_INSTANCE):
     return np.stack(ps), np.stack(xs)
 
 
-def cyclic_family_start(n: int = 7, seed: int = SEED_CYCLIC_MONODROMY):
-    """Planted generic complex (p0, x0) of systems.cyclic_family(n): x0 and p complex Gaussian, then
-    the first term's parameter of every equation is set so that x0 solves it (each equation is
-    linear in its parameters)."""
-    from .systems import cyclic_family
-    d = cyclic_family(n)
+def family_start(d, seed: int):
+    """Planted generic complex (p0, x0) of a coefficient family (systems.coefficient_family): x0 and
+    p complex Gaussian, then the first term's parameter of every equation is set so that x0 solves
+    it (each equation is linear in its parameters)."""
+    n = d.n_vars
     g = gen(seed)
     x0 = complex_normal(g, n)
     p = complex_normal(g, d.n_params)
@@ -308,6 +309,11 @@ def cyclic_family_start(n: int = 7, seed: int = SEED_CYCLIC_MONODROMY):
     return p, x0
 
 
+def cyclic_family_start(n: int = 7, seed: int = SEED_CYCLIC_MONODROMY):
+    from .systems import cyclic_family
+    return family_start(cyclic_family(n), seed)
+
+
 def fivepoint_complex_start(seed: int = SEED_FIVEPOINT_MONODROMY):
     """Planted generic complex (x0, p0) for monodromy: complex depths, T, first-view points and q
     normalised by the complex square root of q.q; the second view from the closed form."""
@@ -317,3 +323,36 @@ def fivepoint_complex_start(seed: int = SEED_FIVEPOINT_MONODROMY):
     gam = complex_normal(g, (5, 2))
     p, x = fivepoint_project(x, gam)
     return p, x
+
+
+def p3p_instance(seed: int):
+    """Planted real P3P instance: camera [I | 0]; world points Gamma_i = rho_i gamma_i with
+    depths rho_i ~ U[3, 6] and calibrated image points |u|, |v| <= 0.4, then moved to a world frame
+    by a random rotation (0.1-0.5 rad) and translation N(0, 1) (the equations only see distances
+    and dot products of the Gamma differences, so the frame does not matter).
+    Returns (p [15] complex, x_gt [3] complex = the depths)."""
+    from .systems import p3p_param_index
+    g = gen(seed)
+    rho = g.uniform(3, 6, 3)
+    uv = g.uniform(-0.4, 0.4, (3, 2))
+    Rw, _ = random_rotation(g)
+    tw = g.normal(0, 1, 3)
+    p = np.zeros(15, np.complex128)
+    for i in range(3):
+        gam = np.array([uv[i, 0], uv[i, 1], 1.0])
+        Gam = Rw @ (rho[i] * gam) + tw
+        p[p3p_param_index(0, i, 0)], p[p3p_param_index(0, i, 1)] = uv[i]
+        for c in range(3):
+            p[p3p_param_index(1, i, c)] = Gam[c]
+    return p, rho.astype(np.complex128)
+
+
+def p3p_batch(n_instances: int, base: int = SEED_P3P_INSTANCE):
+    P, X = zip(*(p3p_instance(base + b) for b in range(n_instances)))
+    return np.stack(P), np.stack(X)
+
+
+def p3p_p0(seed: int = SEED_P3P_P0) -> np.ndarray:
+    """Generic complex start parameters for the P3P parameter homotopy."""
+    return complex_normal(gen(seed), 15)
+

@@ -65,13 +65,12 @@ def cyclic(n: int) -> SystemDesc:
     return desc_from_equations(eqs, name=f"cyclic-{n}", var_names=[f"x{i}" for i in range(n)])
 
 
-def cyclic_family(n: int) -> SystemDesc:
-    """cyclic-n with a free coefficient per term (the paper's monodromy + parameter
-    homotopy workflow, applied to the Table 1 benchmark P:467): the same monomial support as
-    cyclic(n), term q of the flattened term list multiplied by parameter p_q.  The standard cyclic-n
-    is the member cyclic_family_target(n) (all ones, the constant -1)."""
-    base = cyclic(n)
-    T = base.n_terms
+def coefficient_family(base: SystemDesc, name: str = "") -> SystemDesc:
+    """The family of `base` (a system with constant coefficients) with a free coefficient per term:
+    the same monomial support, term q of base's flattened term list multiplied by parameter p_q
+    (the paper's monodromy-start + parameter-homotopy workflow, applied to its
+    Table 1 benchmarks).  `base` itself is the member family_target(base)."""
+    n, T = base.n_vars, base.n_terms
     eqs = [const(n, T, 0) for _ in range(n)]
     for q in range(T):
         i = int(base.term_eq[q])
@@ -80,14 +79,22 @@ def cyclic_family(n: int) -> SystemDesc:
             for _ in range(int(base.term_xexp[q, v])):
                 m = m * var_x(n, T, v)
         eqs[i] = eqs[i] + m
-    return desc_from_equations(eqs, name=f"cyclic-{n}-family", var_names=[f"x{i}" for i in range(n)])
+    return desc_from_equations(eqs, name=name or f"{base.name}-family", var_names=base.var_names)
+
+
+def family_target(base: SystemDesc):
+    """Parameters of coefficient_family(base) that give `base`."""
+    import numpy as np
+    return np.array([complex(base.coef_w[base.coef_ptr[base.term_coef[q]]]) for q in range(base.n_terms)])
+
+
+def cyclic_family(n: int) -> SystemDesc:
+    """cyclic-n coefficient family (Table 1); the standard cyclic-n is cyclic_family_target(n)."""
+    return coefficient_family(cyclic(n), name=f"cyclic-{n}-family")
 
 
 def cyclic_family_target(n: int):
-    """Parameters of cyclic_family(n) that give the standard cyclic-n."""
-    import numpy as np
-    base = cyclic(n)
-    return np.array([complex(base.coef_w[base.coef_ptr[base.term_coef[q]]]) for q in range(base.n_terms)])
+    return family_target(cyclic(n))
 
 
 def eco(n: int) -> SystemDesc:
@@ -313,3 +320,38 @@ def fivepoint_symmetry(x):
     y = x.copy()
     y[10:14] = -y[10:14]
     return [x, y]
+
+
+# ---------------------------------------------------------------------------
+# P3P absolute pose, depth form (PAPER.md Eq. P3PafterElim; Table 2: 3 unknowns,
+# 8 solutions)
+# ---------------------------------------------------------------------------
+
+P3P_VARS = ["rho1", "rho2", "rho3"]
+
+
+def p3p_param_index(kind: int, point: int, coord: int) -> int:
+    """kind 0: image point gamma_i = (u_i, v_i, 1), coord 0..1 -> 0..5; kind 1: world point Gamma_i,
+    coord 0..2 -> 6..14."""
+    return 2 * point + coord if kind == 0 else 6 + 3 * point + coord
+
+
+def p3p_depth() -> SystemDesc:
+    """(Gamma_j - Gamma_1)^T (Gamma_k - Gamma_1) = (rho_j gamma_j - rho_1 gamma_1)^T (rho_k gamma_k - rho_1 gamma_1)
+    for (j, k) = (2, 2), (3, 3), (2, 3): three quadratics in the depths rho_1..3 with
+    gamma_i = (u_i, v_i, 1) (calibrated image points) and the world points Gamma_i as parameters
+    (p3p_param_index).  Bezout number 8 = the 8 solutions of Table 2 P:512 (4 poses x rho -> -rho,
+    P:242)."""
+    n, P = 3, 15
+    X = [var_x(n, P, i) for i in range(n)]
+    Pv = [var_p(n, P, q) for q in range(P)]
+    one = const(n, P, 1)
+    gam = [[Pv[p3p_param_index(0, i, 0)], Pv[p3p_param_index(0, i, 1)], one] for i in range(3)]
+    Gam = [[Pv[p3p_param_index(1, i, c)] for c in range(3)] for i in range(3)]
+    def dotp(a, b):
+        return a[0] * b[0] + a[1] * b[1] + a[2] * b[2]
+    D = [[Gam[j][c] - Gam[0][c] for c in range(3)] for j in range(3)]
+    V = [[X[j] * gam[j][c] - X[0] * gam[0][c] for c in range(3)] for j in range(3)]
+    eqs = [dotp(D[j], D[k]) - dotp(V[j], V[k]) for j, k in ((1, 1), (2, 2), (1, 2))]
+    return desc_from_equations(eqs, name="p3p-depth", var_names=P3P_VARS)
+

@@ -5,6 +5,7 @@
   python scripts/make_fixtures.py fivepoint  # 5-point relpose + depth monodromy (reading R24)
   python scripts/make_fixtures.py eco12      # eco-12 TD solve (118,098 tracks) -> the oracle's finite set
   python scripts/make_fixtures.py cyclic7    # cyclic-7 coefficient-family monodromy (Table 1: 924)
+  python scripts/make_fixtures.py p3p        # P3P depth form: TD at a generic p0 -> 8 starts (Table 2)
 
 This script imports only `oracle` and `hc_inputs`; the CUDA path never writes fixtures
 (prompt rule ③: no stored value comes from the CUDA path).  Start systems of the paper's
@@ -122,6 +123,23 @@ def make_fivepoint(max_loops: int = 40, stall_loops: int = 5, seed: int = rng.SE
 
 
 ECO12_GAMMA_SEED = 2
+P3P_TD_GAMMA_SEED = 3
+
+
+def make_p3p():
+    """P3P depth form (Eq. P3PafterElim): total-degree solve (2^3 = 8 tracks) at the
+    generic complex p0 = rng.p3p_p0() -> the 8 start solutions (Table 2: 8)."""
+    d = systems.p3p_depth()
+    p0 = rng.p3p_p0()
+    td = constant_system_at(d, p0)
+    res = oracle.track(oracle.td_homotopy(td, rng.gamma(P3P_TD_GAMMA_SEED)), oracle.td_start(td.degrees()))
+    U, mult = oracle.dedup(oracle.finite_solutions(res))
+    print(f"P3P TD at p0: {len(U)} distinct finite of {res.status.size} tracks", flush=True)
+    hdr = (f"P3P depth-form start solutions at p0 = rng.p3p_p0() (seed {rng.SEED_P3P_P0}).\n"
+           f"Written by scripts/make_fixtures.py (oracle only): TD homotopy, gamma seed {P3P_TD_GAMMA_SEED},\n"
+           f"{res.status.size} tracks -> {len(U)} distinct finite solutions (PAPER.md Table 2 P:512: 8).")
+    fixtures.write_solutions(fixtures.fixture_path("p3p_start.sols"), U, hdr)
+    fixtures.write_params(fixtures.fixture_path("p3p_p0.params"), p0, hdr)
 
 
 def make_cyclic7(max_loops: int = 60, stall_loops: int = 4, seed: int = rng.SEED_CYCLIC_MONODROMY):
@@ -138,22 +156,6 @@ def make_cyclic7(max_loops: int = 60, stall_loops: int = 4, seed: int = rng.SEED
     fixtures.write_params(fixtures.fixture_path("cyclic7_p0.params"), p0, hdr)
 
 
-def make_eco12():
-    """The oracle's finite solution set of eco-12 (Table 1: 1024 solutions), used by the GPU
-    parity test as the expected set (the oracle needs minutes for 118,098 tracks)."""
-    d = systems.eco(12)
-    t0 = time.time()
-    res = oracle.track(oracle.td_homotopy(d, rng.gamma(ECO12_GAMMA_SEED)), oracle.td_start(d.degrees()))
-    U, mult = oracle.dedup(oracle.finite_solutions(res))
-    st = np.bincount(res.status.reshape(-1), minlength=6)
-    print(f"eco-12 TD: {len(U)} distinct finite of {res.status.size} tracks (statuses {st.tolist()}), "
-          f"max mult {mult.max()}, {time.time() - t0:.1f} s", flush=True)
-    hdr = (f"eco-12 finite solutions (PAPER.md Table 1 P:469: 1024), reading R25 (standard eco-n).\n"
-           f"Written by scripts/make_fixtures.py (oracle only): TD homotopy, gamma seed {ECO12_GAMMA_SEED},\n"
-           f"{res.status.size} tracks -> {len(U)} distinct finite solutions; statuses {st.tolist()}.")
-    fixtures.write_solutions(fixtures.fixture_path("eco12_solutions.sols"), U, hdr)
-
-
 if __name__ == "__main__":
     oracle.build()
     what = sys.argv[1:] or ["fourview", "trifocal", "fivepoint"]
@@ -167,3 +169,5 @@ if __name__ == "__main__":
         make_eco12()
     if "cyclic7" in what:
         make_cyclic7()
+    if "p3p" in what:
+        make_p3p()

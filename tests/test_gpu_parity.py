@@ -176,6 +176,24 @@ def test_cyclic7_monodromy_ph_parity(hc, orc):
     assert_same_set(orc, A, B, "cyclic-7 (monodromy start PH)")
 
 
+def test_p3p_ph_parity(hc, orc):
+    """P3P depth form (Eq. P3PafterElim, Table 2: 8 solutions): parameter homotopy
+    from the oracle's 8 starts at a generic p0 to 64 planted real instances; per instance the GPU
+    set equals the oracle's (8 solutions, closed under rho -> -rho) and contains the planted depths."""
+    d = systems.p3p_depth()
+    S = fixtures.read_solutions(fixtures.fixture_path("p3p_start.sols"))
+    p0 = fixtures.read_params(fixtures.fixture_path("p3p_p0.params"))
+    p1s, X = rng.p3p_batch(64)
+    res = run_ph(hc, d, S, p0, p1s)
+    ref = orc.track(orc.ph_homotopy(d, p0), S, p1s=p1s)
+    for b in range(64):
+        A = orc.dedup(orc.finite_solutions(ref, b))[0]
+        B = gpu_set(orc, res, b)
+        assert len(A) == 8, (b, len(A))
+        assert_same_set_r21(orc, d, p1s[b], A, B, f"P3P instance {b}")
+        assert np.min(np.max(np.abs(B - X[b]), axis=1)) < 1e-8
+
+
 @pytest.mark.parametrize("n", [6, 8, 10])
 def test_eco_parity(hc, orc, n):
     """eco-n (reading R25): 2^(n-2) solutions, the same set as the oracle on the same gamma."""

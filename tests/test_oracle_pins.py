@@ -290,6 +290,26 @@ def test_cyclic7_family_monodromy_fixture(orc):
     assert ok and len(B) == 924, (len(A), len(B), ua, ub)
 
 
+def test_p3p_planted_and_symmetry(orc):
+    """P3P depth form (Eq. P3PafterElim): for planted real instances the total-degree
+    homotopy (8 tracks) gives 8 distinct finite solutions (Table 2), closed under
+    rho -> -rho (4 poses), containing the planted depths."""
+    import os
+    import sys
+    sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "scripts"))
+    from make_fixtures import constant_system_at   # oracle-only helper (coefficients frozen at p)
+    d = systems.p3p_depth()
+    for b in range(3):
+        p, x = rng.p3p_instance(rng.SEED_P3P_INSTANCE + b)
+        td = constant_system_at(d, p)
+        res = orc.track(orc.td_homotopy(td, rng.gamma(3)), orc.td_start(td.degrees()))
+        U, mult = orc.dedup(orc.finite_solutions(res))
+        assert len(U) == 8 and mult.max() == 1
+        for y in U:
+            assert np.min(np.max(np.abs(U + y), axis=1)) < 1e-8   # -y is a solution too
+        assert np.min(np.max(np.abs(U - x), axis=1)) < 1e-9
+
+
 def test_eco3_closed_form(orc):
     """eco-3 (reading R25) by hand: x1 + x2 + 1 = 0, x2 x3 = 2, (x1 + x1 x2) x3 = 1 give
     2 x2^2 + 5 x2 + 2 = 0, i.e. (x1, x2, x3) = (-1/2, -1/2, -4) and (1, -2, -1)."""
