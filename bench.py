@@ -161,8 +161,11 @@ def oracle_sample(name: str, budget_s: float, rank: int = 0, B: int = 1, nthread
     if m == S and p1s is not None and p1s.shape[0] > 1:   # a whole instance fits: take more instances
         k = int(min(p1s.shape[0], max(1, budget_s / max(dt * S / n, 1e-3))))
     reps = 1
-    if m == S and k == 1:   # a single-instance workload shorter than the budget: repeat the whole solve
-        reps = int(min(1000, max(1, budget_s / max(dt * S / n, 1e-4))))
+    if m == S:   # the whole sample is shorter than the budget: repeat it
+        t = time.perf_counter()
+        run(start[:m], k)
+        d1 = time.perf_counter() - t
+        reps = int(min(1000, max(1, budget_s / max(d1, 1e-4))))
     t = time.perf_counter()
     for _ in range(reps):
         run(start[:m], k)
