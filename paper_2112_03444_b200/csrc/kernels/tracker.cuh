@@ -48,6 +48,12 @@ constexpr unsigned FULL = 0xffffffffu;
 #ifndef HCB_MAXW_MID   // warps per CTA for 15 <= N <= 20 (A/B experiments override it)
 #define HCB_MAXW_MID 12
 #endif
+#ifndef HCB_MAXW_LOW   // warps per CTA and CTAs per SM for N <= 14 (A/B experiments override them)
+#define HCB_MAXW_LOW 4
+#endif
+#ifndef HCB_MINB_LOW
+#define HCB_MINB_LOW 4
+#endif
 // LW: lanes per track -- lanes_for(N) (throughput layout, 32/LW tracks per warp) or 32 (the wide
 // latency layout for N <= 16: one track per warp, its op list and monomial program spread over 32
 // lanes and REDUX-based reductions; chosen by the host for batches that under-fill the GPU).
@@ -57,8 +63,8 @@ struct TrackerShape {
   static constexpr int L = LW;
   static constexpr int E = HY ? N - 16 : 0;   // extra rows (hybrid layout)
   static constexpr int NC = HY ? 2 : 1;       // unknown components per lane
-  static constexpr int MAXW = HY ? 8 : (N >= 15 && N <= 20) ? HCB_MAXW_MID : 4;
-  static constexpr int MINB = (N <= 14) ? 4 : (N <= 20) ? 1 : 2;
+  static constexpr int MAXW = HY ? 8 : (N >= 15 && N <= 20) ? HCB_MAXW_MID : (N <= 14) ? HCB_MAXW_LOW : 4;
+  static constexpr int MINB = (N <= 14) ? HCB_MINB_LOW : (N <= 20) ? 1 : 2;
 };
 
 __device__ __forceinline__ double2 cmul(double2 a, double2 b) {
