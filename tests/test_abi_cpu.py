@@ -136,12 +136,16 @@ def test_paper_index_format_example(hc):
     assert facs[n] == []
 
 
-@pytest.mark.parametrize("name", ["katsura-6", "cyclic-7", "4-view", "trifocal"])
+@pytest.mark.parametrize("name", ["katsura-6", "cyclic-7", "4-view", "trifocal", "5-point", "P3P", "eco-8",
+                                  "cyclic-7 family"])
 def test_compiled_table_matches_oracle_evaluation(hc, orc, name):
     """The compiled op table, interpreted directly in Python, reproduces the oracle's J_F and F
-    (PH: coefficients at p) -- pins the host compiler (differentiation, folding, lane packing)."""
+    (PH: coefficients at p) -- pins the host compiler (differentiation, folding, lane packing, the
+    classic and the log-depth monomial programs: cyclic-7 uses the latter)."""
     d = {"katsura-6": lambda: systems.katsura(6), "cyclic-7": lambda: systems.cyclic(7),
-         "4-view": lambda: systems.nview_triangulation(4), "trifocal": systems.trifocal_unknown_f}[name]()
+         "4-view": lambda: systems.nview_triangulation(4), "trifocal": systems.trifocal_unknown_f,
+         "5-point": systems.fivepoint_relpose_depth, "P3P": systems.p3p_depth, "eco-8": lambda: systems.eco(8),
+         "cyclic-7 family": lambda: systems.cyclic_family(7)}[name]()
     ops, prog, smap, emap, info = hc.hc_system_compile_tables(d)
     N = d.n_vars
     assert info["n_ops_rhs"] == d.n_terms

@@ -1,0 +1,39 @@
+"""bench.py host logic without a GPU: every workload builds its seeded inputs with consistent
+shapes, and the traffic lookup reads the committed ncu record."""
+import os
+import sys
+
+import numpy as np
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import bench  # noqa: E402
+
+CONFIGS = ["trifocal", "fourview", "fivepoint", "p3p", "cyclic7", "cyclic7ph", "katsura6", "eco12"]
+
+
+@pytest.mark.parametrize("name", CONFIGS)
+def test_workload_shapes(name):
+    d, start, p0, p1s, _, meta = bench.make_workload(name, 2, 0)
+    assert meta["workload"]
+    if start is None:   # total-degree single instance: the library builds start and parameters
+        assert d.n_params == 0
+        return
+    assert start.ndim == 2 and start.shape[1] == d.n_vars and start.shape[0] >= 1
+    assert p0.shape == (d.n_params,)
+    assert p1s.ndim == 2 and p1s.shape[1] == d.n_params and p1s.shape[0] in (1, 2)
+    assert np.all(np.isfinite(start)) and np.all(np.isfinite(p1s))
+
+
+def test_rank_offsets_give_distinct_instances():
+    """Weak scaling: rank r owns instances r*B .. r*B+B-1 (distinct seeds per rank)."""
+    a = bench.make_workload("fourview", 2, 0)[3]
+    b = bench.make_workload("fourview", 2, 1)[3]
+    assert not np.allclose(a, b)
+
+
+def test_traffic_lookup():
+    assert bench.traffic_bytes("trifocal", 1024, 5328) > 0
+    assert bench.traffic_bytes("trifocal", 7, 5328) is None
