@@ -211,8 +211,9 @@ hc_status hc_result_get(hc_result res, int64_t instance, int64_t track, hc_compl
 hc_status hc_result_destroy(hc_result res);
 
 /* ---------------------------------------------------------------------------------------------
- * Batched fused LU + solve (kernel fusion, augmented matrix [A b], back-substitution
- * on the cached U).  Solves A_k x_k = b_k for k < batch; A row-major [batch][n][n], b [batch][n],
+ * Batched fused LU + solve (kernel fusion, augmented matrix [A b]; the elimination
+ * runs Gauss-Jordan in the one-row-per-lane layout, so no separate back-substitution).  Solves
+ * A_k x_k = b_k for k < batch; A row-major [batch][n][n], b [batch][n],
  * x [batch][n], info [batch] (0 ok, 1 singular: pivot <= pivot_rel * max|A_ij| or non-finite).
  * Device pointers, async on stream.  n in [1, 32].
  * --------------------------------------------------------------------------------------------- */
@@ -222,6 +223,21 @@ hc_status hc_batched_zgesv(int32_t n, int64_t batch, const hc_complex *A, const 
 /* FP64 DFMA throughput probe (SURVEY.md §8(d) "FP64 peak"): runs ~`ms` milliseconds of
  * independent DFMA chains on every SM of `device`; *tflops receives the achieved FLOP/s / 1e12. */
 hc_status hc_fp64_peak_probe(int device, double *tflops);
+
+/* ---------------------------------------------------------------------------------------------
+ * Endpoint post-processing (host, not timed; readings R11, R12 -- SPEC
+ * S:266-274): greedy deduplication in track order of one instance's CONVERGED endpoints -- track s
+ * merges into the first kept endpoint x with |x_i - y_i| <= dedup_tol * max(1, |x_i|) for every
+ * i -- and real classification of the kept ones (max_i |Im x_i| <= real_tol * max(1, |x_i|)).
+ * Host arrays: x [S * N] endpoints (e.g. one instance's slice of x_out), status [S] (hc_track_status,
+ * NULL = all CONVERGED).  Caller-owned outputs, [S] each, may be NULL: rep[s] = the track index of
+ * the kept endpoint s merged into (s itself when kept), -1 when s is not CONVERGED; is_real[s] = 1
+ * for a kept real endpoint, else 0.  *n_unique = number of kept endpoints.
+ * Errors: HC_E_INVALID_ARG for null n_unique, null x with S > 0, S < 0, N outside [1, 32], negative
+ * tolerances.
+ * --------------------------------------------------------------------------------------------- */
+hc_status hc_solutions(const hc_complex *x, const int32_t *status, int64_t S, int32_t N, double dedup_tol,
+                       double real_tol, int64_t *rep, int32_t *is_real, int64_t *n_unique);
 
 /* Experiment hook: per-phase cycle sums of the tracker kernel (coefficients, monomials, ops, row
  * load, elimination, state machine, eval+solve, iterations) -- only in libraries built with

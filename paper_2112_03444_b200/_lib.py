@@ -21,7 +21,7 @@ EXPORTED = [
     "hc_system_create", "hc_system_create_total_degree", "hc_total_degree_params", "hc_total_degree_count",
     "hc_total_degree_start", "hc_system_info_get", "hc_system_destroy", "hc_system_compile_info",
     "hc_system_compile_tables", "hc_tracker_settings_default", "hc_track_batch", "hc_result_wait",
-    "hc_result_elapsed_ms", "hc_result_launch", "hc_result_get", "hc_result_destroy", "hc_batched_zgesv", "hc_fp64_peak_probe",
+    "hc_result_elapsed_ms", "hc_result_launch", "hc_result_get", "hc_result_destroy", "hc_batched_zgesv", "hc_fp64_peak_probe", "hc_solutions",
     "hc_last_error", "hc_version", "hc_debug_phase_cycles",
 ]
 
@@ -111,6 +111,8 @@ def lib() -> C.CDLL:
     L.hc_batched_zgesv.argtypes = [C.c_int32, C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
                                    C.c_double, C.c_void_p]
     L.hc_fp64_peak_probe.argtypes = [C.c_int, P(C.c_double)]
+    L.hc_solutions.argtypes = [C.c_void_p, C.c_void_p, C.c_int64, C.c_int32, C.c_double, C.c_double, C.c_void_p,
+                               C.c_void_p, P(C.c_int64)]
     L.hc_debug_phase_cycles.argtypes = [C.c_void_p, C.c_void_p]
     L.hc_last_error.restype = C.c_char_p
     L.hc_version.restype = C.c_char_p

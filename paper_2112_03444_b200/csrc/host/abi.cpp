@@ -1,4 +1,5 @@
 // abi.cpp -- the C ABI (include/hc.h): system handles, batch launch, results, helpers.
+#include <algorithm>
 #include <cmath>
 #include <cstdlib>
 #include <cstdio>
@@ -363,6 +364,49 @@ hc_status hc_system_compile_tables(const hc_system_desc *desc, uint32_t *ops, ui
   if (mono_prog) std::memcpy(mono_prog, cs.mono_prog.data(), sizeof(uint32_t) * cs.mono_prog.size());
   if (slot_map) std::memcpy(slot_map, cs.slot_map.data(), sizeof(int32_t) * cs.slot_map.size());
   if (entry_map) std::memcpy(entry_map, cs.mpos.data(), sizeof(int16_t) * cs.mpos.size());
+  return HC_OK;
+}
+
+hc_status hc_solutions(const hc_complex *x, const int32_t *status, int64_t S, int32_t N, double dedup_tol,
+                       double real_tol, int64_t *rep, int32_t *is_real, int64_t *n_unique) {
+  if ((!x && S > 0) || !n_unique) return fail(HC_E_INVALID_ARG, "null argument");
+  if (S < 0 || N < 1 || N > 32) return fail(HC_E_INVALID_ARG, "S >= 0 and 1 <= N <= 32 required");
+  if (!(dedup_tol >= 0.0) || !(real_tol >= 0.0)) return fail(HC_E_INVALID_ARG, "negative tolerance");
+  std::vector<int64_t> kept;   // track indices of the kept endpoints, in track order (reading R11)
+  for (int64_t s = 0; s < S; ++s) {
+    const bool conv = !status || status[s] == HC_CONVERGED;
+    if (is_real) is_real[s] = 0;
+    if (!conv) {
+      if (rep) rep[s] = -1;
+      continue;
+    }
+    const hc_complex *y = x + s * N;
+    int64_t into = -1;
+    for (int64_t u : kept) {
+      const hc_complex *k = x + u * N;
+      bool same = true;
+      for (int i = 0; i < N && same; ++i) {
+        const double d = std::hypot(k[i].re - y[i].re, k[i].im - y[i].im);
+        same = d <= dedup_tol * std::max(1.0, std::hypot(k[i].re, k[i].im));
+      }
+      if (same) {
+        into = u;
+        break;
+      }
+    }
+    if (into < 0) {
+      kept.push_back(s);
+      into = s;
+      if (is_real) {   // reading R12
+        bool real = true;
+        for (int i = 0; i < N && real; ++i)
+          real = std::fabs(y[i].im) <= real_tol * std::max(1.0, std::hypot(y[i].re, y[i].im));
+        is_real[s] = real ? 1 : 0;
+      }
+    }
+    if (rep) rep[s] = into;
+  }
+  *n_unique = (int64_t)kept.size();
   return HC_OK;
 }
 

@@ -255,6 +255,24 @@ def batched_zgesv(A, b, pivot_rel: float = 1e-14, stream=None):
     return x, info
 
 
+def solutions(x, status=None, tol: float = 1e-6, real_tol: float = 1e-6):
+    """Endpoint post-processing of one instance (hc_solutions; readings R11, R12): greedy dedup in
+    track order of the CONVERGED endpoints and real classification.  x [S, N] complex128 and
+    status [S] (host arrays or tensors).  Returns (unique [U, N], multiplicity [U], is_real [U] bool,
+    rep [S] int64: kept track each track merged into, -1 if not converged)."""
+    X = _c128(x.cpu().numpy() if hasattr(x, "cpu") else x)
+    S, N = X.shape
+    st = None if status is None else _i32(status.cpu().numpy() if hasattr(status, "cpu") else status)
+    rep = np.zeros(S, np.int64)
+    real = np.zeros(S, np.int32)
+    nu = C.c_int64()
+    check(L.lib().hc_solutions(_ptr(X), _ptr(st), S, N, float(tol), float(real_tol), _ptr(rep), _ptr(real),
+                               C.byref(nu)), "hc_solutions")
+    kept = np.nonzero(rep == np.arange(S))[0]
+    mult = np.array([np.sum(rep == k) for k in kept], dtype=np.int64)
+    return X[kept], mult, real[kept].astype(bool), rep
+
+
 def fp64_peak_probe(device: int = 0) -> float:
     """Measured FP64 DFMA throughput of `device` in TFLOP/s (hc_fp64_peak_probe)."""
     v = C.c_double()

@@ -210,3 +210,22 @@ def test_product_never_imports_oracle():
             if f.endswith((".py", ".cpp", ".cu", ".cuh", ".h")):
                 txt = open(os.path.join(dirpath, f)).read()
                 assert "import oracle" not in txt and "from oracle" not in txt and "hc_oracle" not in txt, f
+
+
+def test_solutions_post_processing_matches_oracle(hc, orc):
+    """hc_solutions (a11, readings R11/R12) against the oracle's dedup / is_real on synthetic
+    endpoints: planted near-duplicates (inside and well outside the 1e-6 tolerance), real and
+    complex points, large coordinates, non-converged tracks."""
+    g = rng.gen(5)
+    S, N = 400, 6
+    base = (g.standard_normal((60, N)) + 1j * g.standard_normal((60, N))) * 10.0 ** g.integers(-2, 5, (60, 1))
+    base[::3] = base[::3].real   # some real points
+    X = base[g.integers(0, 60, S)].copy()
+    X *= 1 + np.where(g.random((S, 1)) < 0.5, 1e-9, 1e-4) * (g.standard_normal((S, N)) + 1j * g.standard_normal((S, N)))
+    status = np.where(g.random(S) < 0.85, 0, 2).astype(np.int32)
+    U, mult, real, rep = hc.solutions(X, status)
+    A, mA = orc.dedup(X[status == 0])
+    assert U.shape == A.shape and np.array_equal(U, A) and np.array_equal(mult, mA)
+    assert np.array_equal(real, orc.is_real(A))
+    assert np.all(rep[status != 0] == -1) and np.all(rep[status == 0] >= 0)
+    assert hc.solutions(X[:0])[0].shape == (0, N)   # empty instance

@@ -144,6 +144,17 @@ def test_katsura6_parity(hc, orc):
         assert agree >= 0.95
 
 
+def test_solutions_post_processing_on_device_results(hc, orc):
+    """hc.solutions (a11) on a GPU result: katsura-6 gives 64 distinct endpoints, 32 of them real
+    (SURVEY [X2]); the unique set equals the oracle's dedup of the same endpoints."""
+    res, _ = run_td(hc, systems.katsura(6), rng.gamma(0))
+    U, mult, real, rep = hc.solutions(res.x[0], res.status[0])
+    assert len(U) == 64 and np.all(mult == 1) and int(real.sum()) == 32
+    X = res.x.cpu().numpy()[0]
+    A = orc.dedup(X[res.status.cpu().numpy()[0] == 0])[0]
+    assert np.array_equal(U, A)
+
+
 def test_cyclic7_parity(hc, orc):
     """Table 1: 924 solutions, same set as the oracle (gamma seed of config 2)."""
     d = systems.cyclic(7)
