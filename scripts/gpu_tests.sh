@@ -1,0 +1,3 @@
+python -c "import __graft_entry__ as g; g.build()" 2>&1 | tail -1
+timeout 120 python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -1
+timeout 1500 python -m pytest tests -m gpu -q > gpurun_out/pytest_gpu.log 2>&1; tail -3 gpurun_out/pytest_gpu.log
