@@ -209,10 +209,10 @@ __device__ __forceinline__ int seg_argmax(double v, int r, double &vmax) {
 // column k+1 first, and the arg-max for step k+1 starts on it while the remaining columns are
 // updated.  Solution components are collected through shared memory.
 // Returns the solution component y_r in lane r and a slot-uniform success flag.
-// prow: 2 * (N + 1) double2; pl: N bytes (per slot shared memory).
+// prow: 2 * (N + 1) double2 (per slot shared memory).
 // ------------------------------------------------------------------------------------------
 template <int N, int L>
-__device__ __forceinline__ bool lu_rows(double2 (&a)[N + 1], int r, int seg, double2 *prow, uint8_t *pl,
+__device__ __forceinline__ bool lu_rows(double2 (&a)[N + 1], int r, int seg, double2 *prow,
                                         double pivot_rel, double lane_max, double2 &y) {
   bool used = (r >= N);
   int mystep = used ? N : -1;
@@ -552,7 +552,7 @@ __device__ __forceinline__ bool eval_solve(const TrackArgs &A, const uint2 *__re
                                            const int16_t *__restrict__ row_of, const double2 *__restrict__ ct,
                                            double t, bool need_coef, int rhs_off, bool want_abs, double2 *cval,
                                            double2 *mono,
-                                           double2 *M, double2 *prow, double *rabs, uint8_t *pl, int r, int seg,
+                                           double2 *M, double2 *prow, double *rabs, int r, int seg,
                                            const double2 (&xr)[NC],
                                            double2 (&y)[NC], double2 (&fr)[NC], double (&fabs_r)[NC]
 #ifdef HCB_PHASE_TIMING
@@ -662,7 +662,7 @@ __device__ __forceinline__ bool eval_solve(const TrackArgs &A, const uint2 *__re
   fabs_r[0] = (r < N && want_abs) ? rabs[r] : 0.0;
   HCB_T(c4);
   HCB_ACC(3, c3, c4);
-  const bool ok = lu_rows<N, L>(a, r, seg, prow, pl, A.st.pivot_rel, jmax, y[0]);
+  const bool ok = lu_rows<N, L>(a, r, seg, prow, A.st.pivot_rel, jmax, y[0]);
   HCB_T(c5);
   HCB_ACC(4, c4, c5);
   return ok;
@@ -704,7 +704,6 @@ __device__ __forceinline__ void track_body(const TrackArgs &A) {
   double2 *M = mono + A.n_mono;
   double2 *prow = M + A.n_entries + 1;
   double *rabs = reinterpret_cast<double *>(prow + 2 * (N + 1));
-  uint8_t *pl = reinterpret_cast<uint8_t *>(rabs + N);
   if (r == 0) {
     mono[N] = make_double2(1.0, 0.0);            // constant-one slot
     M[A.n_entries] = make_double2(0.0, 0.0);     // the entry every structural zero reads
@@ -830,7 +829,7 @@ __device__ __forceinline__ void track_body(const TrackArgs &A) {
     cval_t = te;
     const bool ok = eval_solve<N, L, NC>(A, ops_s, prog_s, mpos_s, row_of, ct, te, need_coef, rhs_off, want_abs, cval, mono,
                                      M, prow, rabs,
-                                     pl, r, seg, xe, yv, fr, fa
+                                     r, seg, xe, yv, fr, fa
 #ifdef HCB_PHASE_TIMING
                                      , hcb_phase
 #endif

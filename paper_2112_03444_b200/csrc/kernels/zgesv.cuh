@@ -16,11 +16,9 @@ __global__ void __launch_bounds__(128) batched_zgesv_kernel(const double2 *__res
   constexpr int L = (N <= 1) ? 1 : (N <= 2) ? 2 : (N <= 4) ? 4 : (N <= 8) ? 8 : (N <= 16) ? 16 : 32;
   constexpr int TPW = 32 / L;
   __shared__ double2 prow_s[4 * TPW][2 * (N + 1)];
-  __shared__ uint8_t pl_s[4 * TPW][N];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int seg = lane / L, r = lane % L;
   double2 *prow = prow_s[warp * TPW + seg];
-  uint8_t *pl = pl_s[warp * TPW + seg];
   const long long slots = (long long)gridDim.x * 4 * TPW;
   for (long long base = ((long long)blockIdx.x * 4 + warp) * TPW; base < batch; base += slots) {
     const long long k = base + seg;   // warp-uniform loop; idle segments solve a dummy copy
@@ -33,7 +31,7 @@ __global__ void __launch_bounds__(128) batched_zgesv_kernel(const double2 *__res
     double amax = 0.0;
 #pragma unroll
     for (int j = 0; j < N; ++j) amax = fmax(amax, abs2(a[j]));
-    const bool ok = lu_rows<N, L>(a, r, seg, prow, pl, pivot_rel, amax, y);
+    const bool ok = lu_rows<N, L>(a, r, seg, prow, pivot_rel, amax, y);
     if (k < batch) {
       if (r < N) x[(size_t)k * N + r] = y;
       if (r == 0) info[k] = ok ? 0 : 1;
