@@ -1,13 +1,14 @@
 """Benchmark: device-timed tracks/s and instances/s of the fused B200 HC tracker.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--config trifocal|fourview|fivepoint|p3p|cyclic7|cyclic7ph|katsura6|eco12]
-                  [--instances B] [--impl ours|reference] [--no-e2e] [--no-cpu-baseline]
+                  [--instances B | --total-instances T] [--impl ours|reference] [--no-e2e] [--no-cpu-baseline]
 
 One "step" = one pass of the whole hot path (coefficient prologue + fused tracker: every
 §8(a) row a2-a10) over one batch.  Default workload: trifocal pose with unknown focal length,
 parameter homotopy from the oracle-generated start fixture (S = 5328 start solutions) to
 B = 1024 planted synthetic instances per GPU (BASELINE.json configs[3]; at 8 GPUs the job is
-configs[4], 8192 instances) -> weak scaling.  Under torchrun each rank owns its own
+configs[4], 8192 instances) -> weak scaling; `--total-instances 8192` runs configs[4] as a fixed
+job split over the GPUs (strong scaling).  Under torchrun each rank owns its own
 instance block (no collective on the data path); solutions are gathered to rank 0 with NCCL
 after the timed region (timed separately, `gather_ms`).
 
@@ -235,6 +236,10 @@ def run_ours(args):
             dist.barrier(device_ids=[local_rank])
 
     B = args.instances
+    if args.total_instances:   # strong scaling: a fixed job (configs[4]: 8192 instances) split over the ranks
+        if args.total_instances % world:
+            raise SystemExit(f"--total-instances {args.total_instances} is not a multiple of {world} GPUs")
+        B = args.total_instances // world
     d, start, p0, p1s, _, meta = make_workload(args.config, B, rank)
     if p1s is not None:
         B = p1s.shape[0]   # single-instance workloads fix their own batch
@@ -363,8 +368,8 @@ def run_ours(args):
         line = {
             "metric": METRIC, "value": value, "unit": "tracks/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": elapsed_max / args.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "c128 (fp64)", "data": "synthetic",
-            "instances_per_sec": world * B * args.steps / (elapsed_max / 1e3),
+            "scaling": "strong" if args.total_instances else "weak", "vs_baseline": None, "dtype": "c128 (fp64)",
+            "data": "synthetic", "instances_per_sec": world * B * args.steps / (elapsed_max / 1e3),
             "config": {"workload": meta["workload"], "instances_per_gpu": B, "tracks_per_instance": S,
                        "N": N, "l2": "256 MB buffer written between steps (flush)", "parallelism": f"dp{world}",
                        "warmup_instances": wb,
@@ -394,7 +399,9 @@ def main():
     ap.add_argument("--steps", type=int, default=1)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="trifocal", choices=["trifocal", "fourview", "fivepoint", "p3p", "cyclic7", "cyclic7ph", "katsura6", "eco12"])
-    ap.add_argument("--instances", type=int, default=1024)
+    ap.add_argument("--instances", type=int, default=1024, help="instances per GPU (weak scaling)")
+    ap.add_argument("--total-instances", type=int, default=0,
+                    help="fixed total instances split over the GPUs (strong scaling, e.g. configs[4]: 8192)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--warmup-instances", type=int, default=16)
     ap.add_argument("--e2e-steps", type=int, default=1)
