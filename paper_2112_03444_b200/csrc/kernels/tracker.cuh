@@ -40,13 +40,18 @@ constexpr unsigned FULL = 0xffffffffu;
 #define HCB_ACC(i, a, b)
 #endif
 // Warps per CTA and minimum resident CTAs per SM, by N (register budget 65536 / (32 * warps * ctas)):
-//   N <= 14: 4 warps x 4 CTAs (128 regs);  15..20: one 12-warp CTA per SM (168 regs; measured on the
-//   trifocal system: 12 warps at 168 regs beat 16 at 128 (spills) and 8 at 218);  N > 20: 4 warps x
-//   2 CTAs.  The launcher shrinks the CTA when the shared memory does not fit.
+//   N <= 14: 4 warps x 4 CTAs (128 regs);  N = 15, 16 (two 16-lane tracks per warp): one 16-warp CTA
+//   (128 regs; 5-point relpose: 2.7 % faster than 12 warps at 168);  17..20: one 12-warp CTA per SM
+//   (168 regs; measured on the trifocal system: 12 warps at 168 regs beat 16 at 128 (spills) and 8
+//   at 218);  N > 20: 4 warps x 2 CTAs.  The launcher shrinks the CTA when the shared memory does
+//   not fit.
 //   Hybrid layout (hy_layout(N), 16-lane tracks with column-distributed extra rows): one 8-warp CTA
 //   (16 tracks; shared memory bound).
-#ifndef HCB_MAXW_MID   // warps per CTA for 15 <= N <= 20 (A/B experiments override it)
+#ifndef HCB_MAXW_MID   // warps per CTA for 17 <= N <= 20 (A/B experiments override it)
 #define HCB_MAXW_MID 12
+#endif
+#ifndef HCB_MAXW_MID16   // warps per CTA for N = 15, 16 (16-lane tracks; A/B experiments override it)
+#define HCB_MAXW_MID16 16
 #endif
 #ifndef HCB_MAXW_LOW   // warps per CTA and CTAs per SM for N <= 14 (A/B experiments override them)
 #define HCB_MAXW_LOW 4
@@ -63,7 +68,11 @@ struct TrackerShape {
   static constexpr int L = LW;
   static constexpr int E = HY ? N - 16 : 0;   // extra rows (hybrid layout)
   static constexpr int NC = HY ? 2 : 1;       // unknown components per lane
-  static constexpr int MAXW = HY ? 8 : (N >= 15 && N <= 20) ? HCB_MAXW_MID : (N <= 14) ? HCB_MAXW_LOW : 4;
+  static constexpr int MAXW = HY                          ? 8
+                              : (N == 15 || N == 16)      ? HCB_MAXW_MID16
+                              : (N >= 17 && N <= 20)      ? HCB_MAXW_MID
+                              : (N <= 14)                 ? HCB_MAXW_LOW
+                                                          : 4;
   static constexpr int MINB = (N <= 14) ? HCB_MINB_LOW : (N <= 20) ? 1 : 2;
 };
 
