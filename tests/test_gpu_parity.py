@@ -377,6 +377,20 @@ def test_monodromy_fivepoint_matches_oracle_fixture(hc, orc):
     assert_same_set_r21(orc, d, p0, fix, res.solutions, "5-point monodromy")
 
 
+def test_monodromy_cyclic7_family_924(hc, orc):
+    """GPU monodromy of the cyclic-7 coefficient family from the planted generic start reaches the
+    Table 1 count 924 and the oracle's monodromy fixture as a set."""
+    from paper_2112_03444_b200.monodromy import monodromy_solve
+    d = systems.cyclic_family(7)
+    p0, x0 = rng.cyclic_family_start(7)
+    fix = fixtures.read_solutions(fixtures.fixture_path("cyclic7_start.sols"))
+    assert np.array_equal(fixtures.read_params(fixtures.fixture_path("cyclic7_p0.params")), p0)
+    s = hc.System(d, device=0)
+    res = monodromy_solve(s, x0, p0, seed=3, stall_loops=4)
+    assert res.solutions.shape[0] == 924, res.history
+    assert_same_set_r21(orc, d, p0, fix, res.solutions, "cyclic-7 family monodromy")
+
+
 # ------------------------------------------------------------------ edge cases
 
 def _linear_plus_quadratic(n, nq, seed):
