@@ -14,9 +14,6 @@
 
 namespace hcb {
 // per-N launchers defined in csrc/kernels/tracker_n*.cu
-#define HCB_DECLM(N) cudaError_t launch_tracker_mid_##N(const TrackArgs &, int, cudaStream_t, TrackerPlan *);
-HCB_DECLM(1) HCB_DECLM(2) HCB_DECLM(3) HCB_DECLM(4) HCB_DECLM(5) HCB_DECLM(6) HCB_DECLM(7) HCB_DECLM(8)
-#undef HCB_DECLM
 #define HCB_DECLW(N) cudaError_t launch_tracker_wide_##N(const TrackArgs &, int, cudaStream_t, TrackerPlan *);
 HCB_DECLW(1) HCB_DECLW(2) HCB_DECLW(3) HCB_DECLW(4) HCB_DECLW(5) HCB_DECLW(6) HCB_DECLW(7) HCB_DECLW(8)
 HCB_DECLW(9) HCB_DECLW(10) HCB_DECLW(11) HCB_DECLW(12) HCB_DECLW(13) HCB_DECLW(14) HCB_DECLW(15) HCB_DECLW(16)
@@ -57,11 +54,6 @@ static const tracker_launch_fn kTrackersWide[17] = {
     launch_tracker_wide_12, launch_tracker_wide_13, launch_tracker_wide_14, launch_tracker_wide_15,
     launch_tracker_wide_16};
 static tracker_launch_fn tracker_launcher_wide(int N) { return (N >= 1 && N <= 16) ? kTrackersWide[N] : nullptr; }
-// the middle layout (16 lanes per track, two tracks per warp) for N <= 8
-static const tracker_launch_fn kTrackersMid[9] = {
-    nullptr, launch_tracker_mid_1, launch_tracker_mid_2, launch_tracker_mid_3, launch_tracker_mid_4,
-    launch_tracker_mid_5, launch_tracker_mid_6, launch_tracker_mid_7, launch_tracker_mid_8};
-static tracker_launch_fn tracker_launcher_mid(int N) { return (N >= 1 && N <= 8) ? kTrackersMid[N] : nullptr; }
 
 cudaError_t launch_batched_zgesv(int n, int64_t batch, const double2 *A, const double2 *b, double2 *x,
                                  int32_t *info, double pivot_rel, cudaStream_t s) {
@@ -105,9 +97,6 @@ struct hc_system_s {
   bool has_wide = false;  // N <= 16: the wide latency layout (32 lanes per track) as well
   CompiledSystem cs_w;
   DevTables dt_w;
-  bool has_mid = false;   // N <= 8: the middle layout (16 lanes per track) as well
-  CompiledSystem cs_m;
-  DevTables dt_m;
   // total-degree metadata
   bool td = false;
   std::vector<hc_complex> td_fvals;
@@ -205,7 +194,6 @@ static hc_status upload_system(hc_system sys) {
   CK(cudaSetDevice(sys->device));
   hc_status s = upload_tables(sys->cs, sys->dt);
   if (s == HC_OK && sys->has_wide) s = upload_tables(sys->cs_w, sys->dt_w);
-  if (s == HC_OK && sys->has_mid) s = upload_tables(sys->cs_m, sys->dt_m);
   return s;
 }
 
@@ -222,7 +210,6 @@ static void free_system(hc_system sys) {
   cudaSetDevice(sys->device);
   free_tables(sys->dt);
   free_tables(sys->dt_w);
-  free_tables(sys->dt_m);
   delete sys;
 }
 
@@ -237,10 +224,6 @@ hc_status hc_system_create(const hc_system_desc *desc, int device, hc_system *ou
   if (s == HC_OK && sys->cs.N <= 16 && sys->cs.L < 32) {
     s = compile_system(*desc, sys->cs_w, err, 32);
     sys->has_wide = (s == HC_OK);
-  }
-  if (s == HC_OK && sys->cs.N <= 8 && sys->cs.L < 16) {
-    s = compile_system(*desc, sys->cs_m, err, 16);
-    sys->has_mid = (s == HC_OK);
   }
   if (s != HC_OK) {
     delete sys;
@@ -475,11 +458,9 @@ hc_status hc_track_batch(hc_system sys, const hc_tracker_settings *settings, con
   // ---- lane layout: the wide latency layout (one track per warp, 32 lanes) when the batch
   //      under-fills the GPU in the throughput layout (policy in wide_layout()); HC_LANES=wide|narrow
   //      overrides it (experiments and tests) ----
-  const char *lv = getenv("HC_LANES");
-  const bool mid = sys->has_mid && lv && !strcmp(lv, "mid");   // experiment: 16 lanes per track
-  const bool wide = !mid && sys->has_wide && wide_layout(sys->device, N, bt->n_instances * bt->n_start);
-  const CompiledSystem &cs = mid ? sys->cs_m : wide ? sys->cs_w : sys->cs;
-  const DevTables &dt = mid ? sys->dt_m : wide ? sys->dt_w : sys->dt;
+  const bool wide = sys->has_wide && wide_layout(sys->device, N, bt->n_instances * bt->n_start);
+  const CompiledSystem &cs = wide ? sys->cs_w : sys->cs;
+  const DevTables &dt = wide ? sys->dt_w : sys->dt;
   if (!bt->start_x) return fail(HC_E_INVALID_ARG, "start_x is null");
   if (P > 0 && (!bt->p_start || !bt->p_target)) return fail(HC_E_INVALID_ARG, "p_start / p_target null with P > 0");
   if (bt->memory != HC_MEM_DEVICE && bt->memory != HC_MEM_HOST) return fail(HC_E_INVALID_ARG, "memory");
@@ -618,8 +599,7 @@ hc_status hc_track_batch(hc_system sys, const hc_tracker_settings *settings, con
     r->phase_cycles = pc;
   }
 #endif
-  e = (mid ? tracker_launcher_mid(N) : wide ? tracker_launcher_wide(N) : tracker_launcher(N))(ta, sys->device, r->stream,
-                                                                                          &r->plan);
+  e = (wide ? tracker_launcher_wide(N) : tracker_launcher(N))(ta, sys->device, r->stream, &r->plan);
   if (e != cudaSuccess) return bail(cuda_fail(e, "tracker launch"));
   cudaEventRecord(r->ev[2], r->stream);
 

@@ -8,10 +8,6 @@ cudaError_t launch_tracker_3(const TrackArgs &A, int device, cudaStream_t s, Tra
 cudaError_t launch_tracker_wide_3(const TrackArgs &A, int device, cudaStream_t s, TrackerPlan *p) {
   return launch_tracker_n<3, 32>(A, device, s, p);
 }
-// the middle layout (16 lanes per track, two tracks per warp)
-cudaError_t launch_tracker_mid_3(const TrackArgs &A, int device, cudaStream_t s, TrackerPlan *p) {
-  return launch_tracker_n<3, 16>(A, device, s, p);
-}
 cudaError_t launch_zgesv_3(int64_t batch, const double2 *A, const double2 *b, double2 *x, int32_t *info,
                            double pivot_rel, cudaStream_t s) {
   return launch_zgesv_n<3>(batch, A, b, x, info, pivot_rel, s);
