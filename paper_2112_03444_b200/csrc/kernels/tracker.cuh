@@ -47,9 +47,6 @@ constexpr unsigned FULL = 0xffffffffu;
 //   not fit.
 //   Hybrid layout (hy_layout(N), 16-lane tracks with column-distributed extra rows): one 8-warp CTA
 //   (16 tracks; shared memory bound).
-#ifndef HCB_OPB   // op list: ops per block whose loads are all issued before its FMAs (A/B switch)
-#define HCB_OPB 4
-#endif
 #ifndef HCB_MAXW_MID   // warps per CTA for 17 <= N <= 20 (A/B experiments override it)
 #define HCB_MAXW_MID 12
 #endif
@@ -499,34 +496,18 @@ __device__ __forceinline__ void run_ops(const uint2 *__restrict__ ops_s, int Q, 
   double2 acc = make_double2(0.0, 0.0), acc2 = make_double2(0.0, 0.0);
   double acc_abs = 0.0;
   int q = 0;
-  constexpr int B = HCB_OPB;   // ops per block
-  for (; q + B <= Q; q += B) {
-    uint2 op[B];
-    double2 c[B], m[B];
+  for (; q + 4 <= Q; q += 4) {
+    uint2 op[4];
+    double2 c[4], m[4];
 #pragma unroll
-    for (int i = 0; i < B; ++i) op[i] = ops_s[(q + i) * L + r];
+    for (int i = 0; i < 4; ++i) op[i] = ops_s[(q + i) * L + r];
 #pragma unroll
-    for (int i = 0; i < B; ++i) {
+    for (int i = 0; i < 4; ++i) {
       c[i] = cval[(int)(op[i].x & 0xFFFFu) + (((op[i].y >> 16) & OP_RHS) ? rhs_off : 0)];
       m[i] = mono[op[i].x >> 16];
     }
 #pragma unroll
-    for (int i = 0; i < B; ++i) op_accumulate<N, ABS>(op[i], c[i], m[i], acc, acc2, acc_abs, M, rabs, row_of);
-  }
-  if (B > 4) {   // remaining whole blocks of 4
-    for (; q + 4 <= Q; q += 4) {
-      uint2 op[4];
-      double2 c[4], m[4];
-#pragma unroll
-      for (int i = 0; i < 4; ++i) op[i] = ops_s[(q + i) * L + r];
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        c[i] = cval[(int)(op[i].x & 0xFFFFu) + (((op[i].y >> 16) & OP_RHS) ? rhs_off : 0)];
-        m[i] = mono[op[i].x >> 16];
-      }
-#pragma unroll
-      for (int i = 0; i < 4; ++i) op_accumulate<N, ABS>(op[i], c[i], m[i], acc, acc2, acc_abs, M, rabs, row_of);
-    }
+    for (int i = 0; i < 4; ++i) op_accumulate<N, ABS>(op[i], c[i], m[i], acc, acc2, acc_abs, M, rabs, row_of);
   }
   for (; q < Q; ++q) {
     const uint2 o = ops_s[q * L + r];
