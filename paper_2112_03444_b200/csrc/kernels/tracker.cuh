@@ -11,13 +11,15 @@
 // global atomic queue (persistent kernel); tracks are ordered instance-major so concurrently
 // running slots share an instance's coefficient table in L1/L2.
 //
-// Evaluation: the host compiler turned dH/dx, H and dH/dt into homogenised terms
-// (coef, scale, factor indices with a constant-one slot) and balanced them over the L lanes; the
-// table sits in shared memory for the whole kernel.  Coefficient values c_j(t), c_j'(t) come from
-// per-instance polynomials in t (prologue kernel) by Horner.  The LU keeps row r in lane r's
-// registers, pivots by a shuffle arg-max of |a|^2 (ties -> lower row), broadcasts the pivot row
-// through shared memory, and back-substitutes on the cached U with the pivot rows still held by
-// their lanes (kernel fusion + augmented matrix).
+// Evaluation: the host compiler turned dH/dx, H and dH/dt into coefficient slots, a
+// shared monomial program and a lane-balanced op list (a constant-one slot pads); the tables sit
+// in shared memory for the whole kernel.  Coefficient values c_j(t), c_j'(t) come from
+// per-instance polynomials in t (prologue kernel) by Horner.  The elimination keeps row r of
+// [J | rhs] in lane r's registers, pivots by an arg-max of |a|^2 (REDUX for 32-lane tracks,
+// shuffles otherwise; ties -> lower row), broadcasts the pivot row through shared memory, and
+// eliminates above and below the pivot (Gauss-Jordan), so the solution needs one division per row
+// and no back-substitution (kernel fusion + augmented matrix).
+// Lane layouts: L = next_pow2(N) lanes per track (throughput) or 32 (wide latency layout, N <= 16).
 #pragma once
 
 #include <cstdint>
