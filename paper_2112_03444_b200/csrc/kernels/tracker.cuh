@@ -49,6 +49,9 @@ constexpr unsigned FULL = 0xffffffffu;
 //   not fit.
 //   Hybrid layout (hy_layout(N), 16-lane tracks with column-distributed extra rows): one 8-warp CTA
 //   (16 tracks; shared memory bound).
+#ifndef HCB_SEG16_REDUX   // 16-lane tracks: REDUX-based arg-max fast path (A/B switch)
+#define HCB_SEG16_REDUX 1
+#endif
 #ifndef HCB_MAXW_MID   // warps per CTA for 17 <= N <= 20 (A/B experiments override it)
 #define HCB_MAXW_MID 12
 #endif
@@ -165,6 +168,27 @@ __device__ __forceinline__ int seg_argmax_thr(double v, int r, double thr, bool 
     if (__popc(b1) == 1 && mhi != thr_hi1 && mhi != 0u) {   // warp-uniform branch
       sing |= (mhi < thr_hi1);
       return __ffs(b1) - 1;
+    }
+    double vmax;
+    const int idx = seg_argmax<L>(v, r, vmax);
+    sing |= !(vmax > thr);
+    return idx;
+  } else if constexpr (L == 16 && HCB_SEG16_REDUX) {
+    // two 16-lane tracks per warp: the high-word maximum of each segment by one full-warp REDUX
+    // each (the other segment contributes 0), then the same unique-maximum test as for 32 lanes;
+    // the fast path is taken only when both segments pass it (warp-uniform), else the exact
+    // butterfly of seg_argmax
+    const int sg = (threadIdx.x & 31) >> 4;
+    const unsigned long long bits = (unsigned long long)__double_as_longlong(v);
+    const unsigned hi = (v >= 0.0) ? (unsigned)(bits >> 32) + 1u : 0u;
+    const unsigned m0 = __reduce_max_sync(FULL, sg == 0 ? hi : 0u);
+    const unsigned m1 = __reduce_max_sync(FULL, sg == 1 ? hi : 0u);
+    const unsigned mhi = sg ? m1 : m0;
+    const unsigned b1 = __ballot_sync(FULL, hi == mhi) & (0xFFFFu << (16 * sg));
+    const unsigned thr_hi1 = (unsigned)((unsigned long long)__double_as_longlong(thr) >> 32) + 1u;
+    if (__all_sync(FULL, __popc(b1) == 1 && mhi != thr_hi1 && mhi != 0u)) {
+      sing |= (mhi < thr_hi1);
+      return __ffs(b1) - 1 - 16 * sg;
     }
     double vmax;
     const int idx = seg_argmax<L>(v, r, vmax);
