@@ -49,9 +49,6 @@ constexpr unsigned FULL = 0xffffffffu;
 //   not fit.
 //   Hybrid layout (hy_layout(N), 16-lane tracks with column-distributed extra rows): one 8-warp CTA
 //   (16 tracks; shared memory bound).
-#ifndef HCB_SEG16_REDUX   // 16-lane tracks: REDUX-based arg-max fast path (A/B switch)
-#define HCB_SEG16_REDUX 1
-#endif
 #ifndef HCB_MAXW_MID   // warps per CTA for 17 <= N <= 20 (A/B experiments override it)
 #define HCB_MAXW_MID 12
 #endif
@@ -115,12 +112,37 @@ __device__ __forceinline__ double2 shfl2(double2 v, int src, int width) {
   return make_double2(__shfl_sync(FULL, v.x, src, width), __shfl_sync(FULL, v.y, src, width));
 }
 
-// Maximum over the L lanes of a segment of a value that is >= 0 or NaN.  L == 32: exact max by two
-// REDUX on the IEEE bit pattern (non-negative doubles order like their bits; a NaN lane yields a
-// NaN result, which every caller treats like a failure); L < 32: butterfly of fmax (NaN ignored).
+#ifndef HCB_SEG16_REDUX   // 8- and 16-lane tracks: REDUX-based segment max / arg-max (A/B switch)
+#define HCB_SEG16_REDUX 1
+#endif
+template <int L>
+__host__ __device__ constexpr unsigned seg_mask();
+// Per-segment maximum of an unsigned value for 32/L tracks per warp: one full-warp REDUX per segment
+// (lanes of the other segments contribute 0), each lane takes its own segment's result.
+template <int L>
+__device__ __forceinline__ unsigned seg_redux_max(unsigned x) {
+  const int sg = (threadIdx.x & 31) / L;
+  unsigned m = 0u;
+#pragma unroll
+  for (int k = 0; k < 32 / L; ++k) {
+    const unsigned mk = __reduce_max_sync(FULL, sg == k ? x : 0u);
+    if (sg == k) m = mk;
+  }
+  return m;
+}
+
+// Maximum over the L lanes of a segment of a value that is >= 0 or NaN.  L == 32, 16, 8: exact max
+// by REDUX on the high then the low words of the IEEE bit pattern (non-negative doubles order like
+// their bits; a NaN lane yields a NaN result, which every caller treats like a failure; one REDUX
+// per segment and pass for 16 and 8 lanes); L < 8: butterfly of fmax (NaN ignored).
 template <int L>
 __device__ __forceinline__ double seg_max(double v) {
-  if constexpr (L == 32) {
+  if constexpr ((L == 16 || L == 8) && HCB_SEG16_REDUX) {   // per-segment REDUX (as for 32 lanes)
+    const unsigned long long bits = (unsigned long long)__double_as_longlong(v);
+    const unsigned mhi = seg_redux_max<L>((unsigned)(bits >> 32));
+    const unsigned mlo = seg_redux_max<L>(((unsigned)(bits >> 32) == mhi) ? (unsigned)bits : 0u);
+    return __longlong_as_double((long long)(((unsigned long long)mhi << 32) | mlo));
+  } else if constexpr (L == 32) {
     const unsigned long long bits = (unsigned long long)__double_as_longlong(v);
     const unsigned mhi = __reduce_max_sync(FULL, (unsigned)(bits >> 32));
     const unsigned mlo = __reduce_max_sync(FULL, ((unsigned)(bits >> 32) == mhi) ? (unsigned)bits : 0u);
@@ -173,22 +195,19 @@ __device__ __forceinline__ int seg_argmax_thr(double v, int r, double thr, bool 
     const int idx = seg_argmax<L>(v, r, vmax);
     sing |= !(vmax > thr);
     return idx;
-  } else if constexpr (L == 16 && HCB_SEG16_REDUX) {
-    // two 16-lane tracks per warp: the high-word maximum of each segment by one full-warp REDUX
-    // each (the other segment contributes 0), then the same unique-maximum test as for 32 lanes;
-    // the fast path is taken only when both segments pass it (warp-uniform), else the exact
-    // butterfly of seg_argmax
-    const int sg = (threadIdx.x & 31) >> 4;
+  } else if constexpr ((L == 16 || L == 8) && HCB_SEG16_REDUX) {
+    // 32/L tracks per warp: the high-word maximum of each segment by one full-warp REDUX each (the
+    // other segments contribute 0), then the same unique-maximum test as for 32 lanes; the fast
+    // path is taken only when every segment passes it (warp-uniform), else the exact butterfly
     const unsigned long long bits = (unsigned long long)__double_as_longlong(v);
     const unsigned hi = (v >= 0.0) ? (unsigned)(bits >> 32) + 1u : 0u;
-    const unsigned m0 = __reduce_max_sync(FULL, sg == 0 ? hi : 0u);
-    const unsigned m1 = __reduce_max_sync(FULL, sg == 1 ? hi : 0u);
-    const unsigned mhi = sg ? m1 : m0;
-    const unsigned b1 = __ballot_sync(FULL, hi == mhi) & (0xFFFFu << (16 * sg));
+    const unsigned mhi = seg_redux_max<L>(hi);
+    const int sg = (threadIdx.x & 31) / L;
+    const unsigned b1 = __ballot_sync(FULL, hi == mhi) & (seg_mask<L>() << (L * sg));
     const unsigned thr_hi1 = (unsigned)((unsigned long long)__double_as_longlong(thr) >> 32) + 1u;
     if (__all_sync(FULL, __popc(b1) == 1 && mhi != thr_hi1 && mhi != 0u)) {
       sing |= (mhi < thr_hi1);
-      return __ffs(b1) - 1 - 16 * sg;
+      return __ffs(b1) - 1 - L * sg;
     }
     double vmax;
     const int idx = seg_argmax<L>(v, r, vmax);
