@@ -110,6 +110,38 @@ def test_batched_zgesv_singular_and_pivoting(hc):
     assert np.allclose(x.cpu().numpy()[1], [1, 1, 1])
 
 
+@pytest.mark.parametrize("n", [3, 4, 6, 8, 11, 16, 18, 24, 32])
+def test_batched_zgesv_tied_pivots(hc, n):
+    """Exact ties in the pivot search (reading R13: ties -> lowest row): entries in {+-1, +-i} from a
+    row/column selection of the 32 x 32 Sylvester-Hadamard matrix times random unit phases make every
+    |a_ik|^2 equal in the first column, so the arg-max takes its exact tie path (the single-REDUX fast
+    path of 8-, 16- and 32-lane tracks only applies to a unique maximum); tied and random systems
+    alternate in the batch so a warp holding several tracks mixes both paths."""
+    import torch
+    g = rng.gen(700 + n)
+    H = np.array([[1.0]])
+    while H.shape[0] < 32:
+        H = np.block([[H, H], [H, -H]])
+    units = np.array([1, -1, 1j, -1j])
+    mats = []
+    while len(mats) < 64:
+        M = H[np.ix_(g.permutation(32)[:n], g.permutation(32)[:n])] * units[g.integers(0, 4, n)][None, :]
+        if np.linalg.cond(M) < 1e3:
+            mats.append(M)
+    B = 2 * len(mats) + 3
+    A = g.standard_normal((B, n, n)) + 1j * g.standard_normal((B, n, n)) + 2 * np.eye(n)
+    A[0:2 * len(mats):2] = np.array(mats)
+    b = g.standard_normal((B, n)) + 1j * g.standard_normal((B, n))
+    x, info = hc.batched_zgesv(_cuda(A), _cuda(b))
+    torch.cuda.synchronize()
+    x = x.cpu().numpy()
+    assert np.all(info.cpu().numpy() == 0)
+    ref = np.linalg.solve(A, b[..., None])[..., 0]
+    err = np.max(np.abs(x - ref), axis=1) / np.maximum(1, np.max(np.abs(ref), axis=1))
+    cond = np.linalg.cond(A)
+    assert np.all(err <= 1e-13 * cond), (err / cond).max()
+
+
 # ------------------------------------------------------------------ whole tracker
 
 def test_univariate_vs_companion(hc, orc):
