@@ -107,6 +107,7 @@ def lib():
         L.orc_newton.argtypes = [C.POINTER(_Hom), C.POINTER(_Settings), C.c_void_p, C.c_double, C.c_int,
                                  C.c_double]
         L.orc_newton.restype = C.c_int
+        L.orc_endpoint_residual.argtypes = [C.POINTER(_Hom), C.c_void_p, C.c_void_p, C.c_void_p]
         _lib = L
     return _lib
 
@@ -180,6 +181,14 @@ def newton(hom: "Homotopy", x, t: float, iters: int, tol: float, settings: "Sett
     x = _c128(x).copy()
     r = lib().orc_newton(C.byref(hom.h), C.byref(st), _ptr(x), float(t), int(iters), float(tol))
     return x, r
+
+
+def endpoint_residual(hom: "Homotopy", x):
+    """Reading R10 at t = 1: (r = ||F||_inf, r_rel = max_i |F_i| / sum_k |c_ik| |m_k(x)|)."""
+    x = _c128(x)
+    r, rr = C.c_double(), C.c_double()
+    lib().orc_endpoint_residual(C.byref(hom.h), _ptr(x), C.byref(r), C.byref(rr))
+    return r.value, rr.value
 
 
 def td_homotopy(desc, gamma: complex) -> Homotopy:

@@ -584,6 +584,21 @@ int orc_predict(const orc_homotopy *h, const orc_settings *cfg, const double *x,
   return r;
 }
 
+/* The endpoint residuals of reading R10 at x (t = 1) -- the same endpoint_residual() the tracker
+ * classifies with; exported so the pins can check r and r_rel against hand-computed values. */
+void orc_endpoint_residual(const orc_homotopy *h, const double *x, double *r, double *r_rel) {
+  tracker T;
+  orc_settings cfg;
+  int n = h->sys->n;
+  orc_settings_default(&cfg);
+  tracker_init(&T, h, h->p1, &cfg);
+  cplx *xx = malloc(sizeof(cplx) * n);
+  load_vec(x, n, xx);
+  endpoint_residual(&T, xx, r, r_rel);
+  free(xx);
+  tracker_free(&T);
+}
+
 int orc_newton(const orc_homotopy *h, const orc_settings *cfg, double *x, double t, int iters, double tol) {
   tracker T;
   int n = h->sys->n, sing;

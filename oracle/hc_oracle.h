@@ -82,6 +82,8 @@ void orc_track(const orc_homotopy *h, const double *p1s, int64_t B,
 /* One predictor step from (x, t) with step dt (RK4 or Euler per st->predictor); 0 on success. */
 int orc_predict(const orc_homotopy *h, const orc_settings *st, const double *x, double t, double dt, double *xp);
 /* Newton at fixed t (Eq. 6), in place; returns 1 converged, 0 not converged, -1 singular. */
+/* Endpoint residuals at x, t = 1 (reading R10): r = ||F||_inf, r_rel = max_i |F_i| / sum_k |c_ik||m_k(x)|. */
+void orc_endpoint_residual(const orc_homotopy *h, const double *x, double *r, double *r_rel);
 int orc_newton(const orc_homotopy *h, const orc_settings *st, double *x, double t, int iters, double tol);
 
 #ifdef __cplusplus

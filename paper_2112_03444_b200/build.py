@@ -3,11 +3,13 @@
 nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo, one object per translation unit
 (the tracker is instantiated once per N = 1..32 in its own unit so they compile in parallel),
 static cudart, output paper_2112_03444_b200/lib/libhc.so.  Incremental: an object is rebuilt
-when its source or any header is newer.
+when its source or any header is newer; objects live in a directory keyed by a hash of the
+compiler flags (variant defines included), so changing HCB_DEFINES never reuses a stale object.
 """
 from __future__ import annotations
 
 import glob
+import hashlib
 import os
 import subprocess
 import sys
@@ -21,7 +23,6 @@ INCLUDE = os.path.join(ROOT, "include")
 # into lib_timing/, HCB_VARIANT=hybrid one with the hybrid 16-lane layout for N = 17, 18 into
 # lib_hybrid/ (load either with HC_LIB_PATH); the product library is the default variant.
 VARIANT = os.environ.get("HCB_VARIANT", "")
-BUILD = os.path.join(PKG, "build" + ("_" + VARIANT if VARIANT else ""))
 LIBDIR = os.path.join(PKG, "lib" + ("_" + VARIANT if VARIANT else ""))
 LIB = os.path.join(LIBDIR, "libhc.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
@@ -34,6 +35,8 @@ elif VARIANT == "hybrid":   # experiment: 16-lane hybrid layout for N = 17, 18 (
 # any variant may add preprocessor switches for A/B experiments, e.g.
 # HCB_VARIANT=w16 HCB_DEFINES="HCB_MAXW_MID=16" (see the #ifndef switches in kernels/tracker.cuh)
 FLAGS = FLAGS + ["-D" + d for d in os.environ.get("HCB_DEFINES", "").split()] if VARIANT else FLAGS
+BUILD = os.path.join(PKG, "build" + ("_" + VARIANT if VARIANT else ""),
+                     hashlib.sha1(" ".join(ARCH + [f for f in FLAGS if not f.startswith("-I")]).encode()).hexdigest()[:10])
 
 
 def sources():

@@ -112,4 +112,27 @@ __host__ __device__ constexpr int lanes_for(int N) {
   return hy_layout(N) ? 16 : (N <= 1) ? 1 : (N <= 2) ? 2 : (N <= 4) ? 4 : (N <= 8) ? 8 : (N <= 16) ? 16 : 32;
 }
 
+// CTA shape of the tracker kernel (warps per CTA, minimum resident CTAs per SM), shared by the
+// kernel's __launch_bounds__ and the host's layout policy (hc_track_batch).
+#ifndef HCB_MAXW_MID   // warps per CTA for 17 <= N <= 20 (A/B experiments override it)
+#define HCB_MAXW_MID 12
+#endif
+#ifndef HCB_MAXW_MID16   // warps per CTA for N = 15, 16 (16-lane tracks; A/B experiments override it)
+#define HCB_MAXW_MID16 16
+#endif
+#ifndef HCB_MAXW_LOW   // warps per CTA and CTAs per SM for N <= 14 (A/B experiments override them)
+#define HCB_MAXW_LOW 4
+#endif
+#ifndef HCB_MINB_LOW
+#define HCB_MINB_LOW 4
+#endif
+__host__ __device__ constexpr int tracker_maxw(int N, int LW) {
+  return (hy_layout(N) && LW == lanes_for(N)) ? 8
+         : (N == 15 || N == 16)               ? HCB_MAXW_MID16
+         : (N >= 17 && N <= 20)               ? HCB_MAXW_MID
+         : (N <= 14)                          ? HCB_MAXW_LOW
+                                              : 4;
+}
+__host__ __device__ constexpr int tracker_minb(int N) { return (N <= 14) ? HCB_MINB_LOW : (N <= 20) ? 1 : 2; }
+
 }  // namespace hcb

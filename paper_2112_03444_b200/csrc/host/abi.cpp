@@ -430,7 +430,8 @@ static hc_status check_settings(const hc_tracker_settings &s) {
 static bool aligned16(const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
 
 // Wide latency layout when the throughput layout would leave the GPU mostly idle: at most ~2.5
-// waves of one-track-per-warp slots (16 resident warps per SM for N <= 14, 12 for N = 15, 16), i.e.
+// waves of one-track-per-warp slots (the wide kernel's resident warps per SM, from the same CTA
+// shape as its __launch_bounds__: 16 for N <= 16), i.e.
 // small single-instance solves (katsura-6: 64 tracks, cyclic-7: 5040), where the makespan is one
 // track's chain of solves and spreading its op list over 32 lanes shortens every solve.
 static bool wide_layout(int device, int N, int64_t tracks) {
@@ -440,7 +441,7 @@ static bool wide_layout(int device, int N, int64_t tracks) {
   }
   int sms = 148;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
-  const int64_t slots = (int64_t)sms * (N <= 14 ? 16 : 12);
+  const int64_t slots = (int64_t)sms * tracker_maxw(N, 32) * tracker_minb(N);
   return tracks * 2 <= slots * 5;
 }
 

@@ -49,18 +49,6 @@ constexpr unsigned FULL = 0xffffffffu;
 //   not fit.
 //   Hybrid layout (hy_layout(N), 16-lane tracks with column-distributed extra rows): one 8-warp CTA
 //   (16 tracks; shared memory bound).
-#ifndef HCB_MAXW_MID   // warps per CTA for 17 <= N <= 20 (A/B experiments override it)
-#define HCB_MAXW_MID 12
-#endif
-#ifndef HCB_MAXW_MID16   // warps per CTA for N = 15, 16 (16-lane tracks; A/B experiments override it)
-#define HCB_MAXW_MID16 16
-#endif
-#ifndef HCB_MAXW_LOW   // warps per CTA and CTAs per SM for N <= 14 (A/B experiments override them)
-#define HCB_MAXW_LOW 4
-#endif
-#ifndef HCB_MINB_LOW
-#define HCB_MINB_LOW 4
-#endif
 // LW: lanes per track -- lanes_for(N) (throughput layout, 32/LW tracks per warp) or 32 (the wide
 // latency layout for N <= 16: one track per warp, its op list and monomial program spread over 32
 // lanes and REDUX-based reductions; chosen by the host for batches that under-fill the GPU).
@@ -70,12 +58,8 @@ struct TrackerShape {
   static constexpr int L = LW;
   static constexpr int E = HY ? N - 16 : 0;   // extra rows (hybrid layout)
   static constexpr int NC = HY ? 2 : 1;       // unknown components per lane
-  static constexpr int MAXW = HY                          ? 8
-                              : (N == 15 || N == 16)      ? HCB_MAXW_MID16
-                              : (N >= 17 && N <= 20)      ? HCB_MAXW_MID
-                              : (N <= 14)                 ? HCB_MAXW_LOW
-                                                          : 4;
-  static constexpr int MINB = (N <= 14) ? HCB_MINB_LOW : (N <= 20) ? 1 : 2;
+  static constexpr int MAXW = tracker_maxw(N, LW);
+  static constexpr int MINB = tracker_minb(N);
 };
 
 __device__ __forceinline__ double2 cmul(double2 a, double2 b) {
@@ -134,7 +118,8 @@ __device__ __forceinline__ unsigned seg_redux_max(unsigned x) {
 // Maximum over the L lanes of a segment of a value that is >= 0 or NaN.  L == 32, 16, 8: exact max
 // by REDUX on the high then the low words of the IEEE bit pattern (non-negative doubles order like
 // their bits; a NaN lane yields a NaN result, which every caller treats like a failure; one REDUX
-// per segment and pass for 16 and 8 lanes); L < 8: butterfly of fmax (NaN ignored).
+// per segment and pass for 16 and 8 lanes); L < 8: butterfly of the NaN-propagating nmax (a NaN residual or step norm
+// classifies the same way for every lane width, as the oracle's max does).
 template <int L>
 __device__ __forceinline__ double seg_max(double v) {
   if constexpr ((L == 16 || L == 8) && HCB_SEG16_REDUX) {   // per-segment REDUX (as for 32 lanes)
@@ -149,7 +134,7 @@ __device__ __forceinline__ double seg_max(double v) {
     return __longlong_as_double((long long)(((unsigned long long)mhi << 32) | mlo));
   } else {
 #pragma unroll
-    for (int off = L / 2; off >= 1; off >>= 1) v = fmax(v, __shfl_xor_sync(FULL, v, off));
+    for (int off = L / 2; off >= 1; off >>= 1) v = nmax(v, __shfl_xor_sync(FULL, v, off));
     return v;
   }
 }

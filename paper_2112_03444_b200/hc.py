@@ -194,6 +194,14 @@ def track_batch(system: System, start_x, p0=None, p1=None, st: L.hc_tracker_sett
         resid = torch.empty((B, S, 2), dtype=torch.float64, device=dev)
     else:
         x, status, ctr, resid = out
+        # the kernel writes B*S*N values through raw pointers: a wrong buffer would be an
+        # out-of-bounds device write, so every output is checked before the launch
+        for name, tns, shape, dtype in (("x", x, (B, S, N), torch.complex128), ("status", status, (B, S), torch.int32),
+                                        ("counters", ctr, (B, S, 4), torch.int32),
+                                        ("resid", resid, (B, S, 2), torch.float64)):
+            if (tuple(tns.shape) != shape or tns.dtype != dtype or not tns.is_contiguous() or tns.device != dev):
+                raise ValueError(f"out[{name}] must be a contiguous {dtype} tensor of shape {shape} on {dev}, "
+                                 f"got {tns.dtype} {tuple(tns.shape)} on {tns.device}")
     if stream is None:
         stream = torch.cuda.current_stream(dev)
     b = L.hc_batch(B, S, start_x.data_ptr(), p0.data_ptr() if system.P else None,
@@ -227,7 +235,11 @@ def track_batch_host(system: System, start_x, p0=None, p1=None, st: L.hc_tracker
         resid = np.empty((B, S, 2), np.float64)
     else:
         x, status, ctr, resid = out
-        assert x.shape == (B, S, N) and x.dtype == np.complex128 and x.flags.c_contiguous
+        for name, a, shape, dtype in (("x", x, (B, S, N), np.complex128), ("status", status, (B, S), np.int32),
+                                      ("counters", ctr, (B, S, 4), np.int32), ("resid", resid, (B, S, 2), np.float64)):
+            if a.shape != shape or a.dtype != dtype or not a.flags.c_contiguous:
+                raise ValueError(f"out[{name}] must be a C-contiguous {np.dtype(dtype).name} array of shape {shape}, "
+                                 f"got {a.dtype} {a.shape}")
     sp = stream.cuda_stream if stream is not None else None
     b = L.hc_batch(B, S, _ptr(start_x), _ptr(p0) if system.P else None, _ptr(p1) if system.P else None, _ptr(x),
                    _ptr(status), _ptr(ctr), _ptr(resid), HC_MEM_HOST, sp)

@@ -126,6 +126,23 @@ ECO12_GAMMA_SEED = 2
 P3P_TD_GAMMA_SEED = 3
 
 
+def make_eco12():
+    """The oracle's finite solution set of eco-12 (Table 1: 1024 solutions, reading R25),
+    the expected set of tests/test_gpu_parity.py::test_eco12_table1_count (the oracle needs
+    minutes for the 118,098 total-degree tracks, so the set is stored)."""
+    d = systems.eco(12)
+    t0 = time.time()
+    res = oracle.track(oracle.td_homotopy(d, rng.gamma(ECO12_GAMMA_SEED)), oracle.td_start(d.degrees()))
+    U, mult = oracle.dedup(oracle.finite_solutions(res))
+    st = np.bincount(res.status.reshape(-1), minlength=6)
+    print(f"eco-12 TD: {len(U)} distinct finite of {res.status.size} tracks (statuses {st.tolist()}), "
+          f"max mult {mult.max()}, {time.time() - t0:.1f} s", flush=True)
+    hdr = (f"eco-12 finite solutions (PAPER.md Table 1 P:469: 1024), reading R25 (standard eco-n).\n"
+           f"Written by scripts/make_fixtures.py (oracle only): TD homotopy, gamma seed {ECO12_GAMMA_SEED},\n"
+           f"{res.status.size} tracks -> {len(U)} distinct finite solutions; statuses {st.tolist()}.")
+    fixtures.write_solutions(fixtures.fixture_path("eco12_solutions.sols"), U, hdr)
+
+
 def make_p3p():
     """P3P depth form (Eq. P3PafterElim): total-degree solve (2^3 = 8 tracks) at the
     generic complex p0 = rng.p3p_p0() -> the 8 start solutions (Table 2: 8)."""

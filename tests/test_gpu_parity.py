@@ -250,10 +250,10 @@ def test_eco_parity(hc, orc, n):
     assert_same_set(orc, A, B, f"eco-{n}")
 
 
-@pytest.mark.skipif(not fixtures.have_fixture("eco12_solutions.sols"), reason="eco-12 fixture missing")
 def test_eco12_table1_count(hc, orc):
     """Table 1: eco-12 has 1024 solutions.  GPU TD solve (118,098 tracks) vs the oracle's set
     (fixture written by scripts/make_fixtures.py, oracle only; the same gamma seed)."""
+    assert fixtures.have_fixture("eco12_solutions.sols"), "run: python scripts/make_fixtures.py eco12"
     d = systems.eco(12)
     res, _ = run_td(hc, d, rng.gamma(2))
     B = gpu_set(orc, res)
@@ -530,22 +530,51 @@ def test_fourview_config3_full_batch_sampled(hc, orc):
                         f"4-view instance {b}")
 
 
-def test_trifocal_config4_full_batch_sampled(hc, orc):
-    """Config 4 at full size (1024 instances x 5328 tracks, the bench workload): sampled tracks
-    from spread-out instances agree with the oracle one by one; planted ground truth recovered."""
+@pytest.fixture(scope="module")
+def trifocal_config4(hc):
+    """Config 4 at full size (1024 instances x 5328 tracks), the bench workload and launch
+    configuration, run once for the tests below."""
     d = systems.trifocal_unknown_f()
     start, p0 = fixtures.trifocal_start()
     p1s, xg = rng.trifocal_batch(1024)
     res = run_ph(hc, d, start, p0, p1s)
-    st = res.status.cpu().numpy()
-    X = res.x.cpu().numpy()
+    return d, start, p0, p1s, xg, res.status.cpu().numpy(), res.x.cpu().numpy()
+
+
+def _planted_found(d, X, xg):
+    imgs = np.array(systems.trifocal_symmetry(xg))
+    return min(np.min(np.max(np.abs(X - y), axis=1), initial=np.inf) for y in imgs) < 1e-8
+
+
+def test_trifocal_config4_set_parity(hc, orc, trifocal_config4):
+    """R21 set parity at the paper's trifocal workload (Table 2) in the bench launch: for
+    instances 0 and 777 of the 1024-instance batch the oracle tracks all 5328 starts, and the GPU's
+    CONVERGED distinct set equals the oracle's (equal counts, nearest neighbour within 1e-8
+    relative per coordinate)."""
+    d, start, p0, p1s, xg, st, X = trifocal_config4
+    for b in (0, 777):
+        ref = orc.track(orc.ph_homotopy(d, p0), start, p1s=p1s[b:b + 1])
+        A = orc.dedup(ref.x[0][ref.status[0] == 0])[0]
+        B = orc.dedup(X[b][st[b] == 0])[0]
+        assert len(A) > 0.9 * start.shape[0] / 2
+        assert_same_set_r21(orc, d, p1s[b], A, B, f"trifocal instance {b}")
+
+
+def test_trifocal_config4_full_batch_sampled(hc, orc, trifocal_config4):
+    """Config 4 at full size: the planted ground truth (up to the Z2^3 images) is recovered in every
+    sampled instance where the oracle recovers it -- each GPU miss is re-run through the oracle on
+    all 5328 starts, which must miss it too and give the same solution set (a path failure of the
+    method, R7, not of the kernel); sampled tracks from spread-out instances agree one by one."""
+    d, start, p0, p1s, xg, st, X = trifocal_config4
     assert (st == 0).mean() > 0.9
-    found = 0
-    for b in range(0, 1024, 16):
-        imgs = np.array(systems.trifocal_symmetry(xg[b]))
-        G = X[b][st[b] == 0]
-        found += min(np.min(np.max(np.abs(G - y), axis=1)) for y in imgs) < 1e-8
-    assert found >= 62   # of 64 sampled instances (path failures are shared with the oracle)
+    missed = [b for b in range(0, 1024, 16) if not _planted_found(d, X[b][st[b] == 0], xg[b])]
+    assert len(missed) <= 4, missed
+    for b in missed:
+        ref = orc.track(orc.ph_homotopy(d, p0), start, p1s=p1s[b:b + 1])
+        G = ref.x[0][ref.status[0] == 0]
+        assert not _planted_found(d, G, xg[b]), f"instance {b}: the oracle finds the planted root, the GPU not"
+        assert_same_set_r21(orc, d, p1s[b], orc.dedup(G)[0], orc.dedup(X[b][st[b] == 0])[0],
+                            f"trifocal instance {b}")
     g = rng.gen(77)
     agree = tot = 0
     for b in (0, 300, 777, 1023):

@@ -160,6 +160,87 @@ def test_predictor_exact_on_linear_path(orc):
         assert not fail and xp[0] == 1.5
 
 
+def _quintic_path_homotopy(orc):
+    """F(x; p) = x - p^5 with p0 = 1, p1 = 2: p(t) = 1 + t, exact path x(t) = (1 + t)^5, Davidenko
+    rhs dx/dt = 5 (1 + t)^4 depends on t only."""
+    from hc_inputs.poly import var_p, var_x
+    f = var_x(1, 1, 0) - var_p(1, 1, 0) ** 5
+    d = systems.from_polys([f], "quintic-path")
+    return orc.ph_homotopy(d, np.array([1.0]), np.array([2.0]))
+
+
+def test_rk4_is_simpson_on_t_only_ode(orc):
+    """Closed form pinning RK4's stage times and weights (classical RK4): when dx/dt = f(t),
+    one RK4 step is Simpson's rule h/6 (f(t) + 4 f(t + h/2) + f(t + h)), whose error for the quartic
+    f = 5 (1+t)^4 is exactly h^5 f''''/2880 = h^5 / 24 (f'''' = 120).  Euler (Eq. 4) gives
+    x + 5h, error (1+h)^5 - 1 - 5h = 10h^2 + 10h^3 + 5h^4 + h^5.  A wrong stage time (e.g. k2 at t)
+    or weight breaks the h^5/24 identity at the first digit."""
+    hom = _quintic_path_homotopy(orc)
+    for h in (0.2, 0.1, 0.05):
+        st = orc.default_settings()
+        xp, fail = orc.predict(hom, np.array([1.0 + 0j]), 0.0, h, st)
+        assert not fail
+        err = xp[0].real - (1 + h) ** 5
+        assert abs(xp[0].imag) == 0.0
+        assert abs(err - h ** 5 / 24) <= 1e-6 * h ** 5 / 24 + 1e-14, (h, err, h ** 5 / 24)   # + rounding of (1+h)^5
+        st.predictor = 1
+        xe, fail = orc.predict(hom, np.array([1.0 + 0j]), 0.0, h, st)
+        assert not fail and abs(xe[0].real - (1 + 5 * h)) <= 1e-15
+    # from t0 = 0.3 (the stage times are t0 + {0, h/2, h/2, h}): error h^5/24 again
+    xp, _ = orc.predict(hom, np.array([1.3 ** 5 + 0j]), 0.3, 0.1)
+    assert abs((xp[0].real - 1.4 ** 5) - 1e-5 / 24) <= 1e-6 * 1e-5 / 24 + 1e-14
+
+
+def test_rk4_fourth_order_on_x_dependent_ode(orc):
+    """Order pin for the x-dependent stages: H = x^2 - (1 + t) (univariate_param(2), p0 = (-1, 0, 1),
+    p1 = (-2, 0, 1)); the exact path from x(0) = 1 is sqrt(1 + t) and dx/dt = 1/(2x).  A one-step
+    method of order q has local error C h^(q+1), so halving h divides the error by ~2^(q+1): RK4
+    (q = 4) -> ~32, Euler (q = 1) -> ~4.  Wrong stage points (x + h/2 k1 etc.) or weights drop the
+    order and fail the ratio window."""
+    d = systems.univariate_param(2)
+    hom = orc.ph_homotopy(d, np.array([-1.0, 0, 1]), np.array([-2.0, 0, 1]))
+
+    def err(h, pred):
+        st = orc.default_settings()
+        st.predictor = pred
+        xp, fail = orc.predict(hom, np.array([1.0 + 0j]), 0.0, h, st)
+        assert not fail
+        return abs(xp[0] - np.sqrt(1 + h))
+    for pred, lo, hi in ((0, 25.0, 40.0), (1, 3.5, 4.5)):
+        e = [err(h, pred) for h in (0.2, 0.1, 0.05)]
+        for a, b in zip(e, e[1:]):
+            assert lo <= a / b <= hi, (pred, e)
+
+
+def test_endpoint_residuals_by_hand(orc):
+    """Reading R10 pinned by hand.  F1 = 2x^2 - 3y + 1, F2 = (1+i)xy - 4 at (x, y) = (1+i, 2):
+    x^2 = 2i, so F1 = -5 + 4i, |F1| = sqrt(41), sum |c||m| = 2*2 + 3*2 + 1 = 11;
+    F2 = (1+i)(1+i)2 - 4 = -4 + 4i, |F2| = 4 sqrt(2), sum |c||m| = sqrt(2)*2sqrt(2) + 4 = 8.
+    r = max(sqrt(41), 4 sqrt(2)) = sqrt(41); r_rel = max(sqrt(41)/11, sqrt(2)/2) = sqrt(2)/2.
+    Checked for the total-degree target (F alone) and for a parameter homotopy whose t = 1
+    coefficients are p1 (p0 random: it must not enter)."""
+    from hc_inputs.poly import const, var_p, var_x
+    x, y = var_x(2, 0, 0), var_x(2, 0, 1)
+    d = systems.from_polys([2 * x * x - 3 * y + 1, (1 + 1j) * x * y - 4], "resid-2x2")
+    pt = np.array([1 + 1j, 2])
+    for hom in (orc.td_homotopy(d, rng.gamma(0)),):
+        r, rr = orc.endpoint_residual(hom, pt)
+        assert abs(r - np.sqrt(41)) <= 1e-14 and abs(rr - np.sqrt(2) / 2) <= 1e-15
+    P = 5
+    xp, yp = var_x(2, P, 0), var_x(2, P, 1)
+    pp = [var_p(2, P, q) for q in range(P)]
+    dp = systems.from_polys([pp[0] * xp * xp + pp[1] * yp + pp[2], pp[3] * xp * yp + pp[4]], "resid-2x2-p")
+    p1 = np.array([2, -3, 1, 1 + 1j, -4], complex)
+    p0 = crandn(rng.gen(3), P)
+    r, rr = orc.endpoint_residual(orc.ph_homotopy(dp, p0, p1), pt)
+    assert abs(r - np.sqrt(41)) <= 1e-14 and abs(rr - np.sqrt(2) / 2) <= 1e-15
+    # a row whose terms all vanish: r_rel = 0 when F_i = 0, and the zero-denominator rule
+    r, rr = orc.endpoint_residual(orc.td_homotopy(d, rng.gamma(0)), np.array([0.5 + 0.5j, 0]))
+    # F2 = -4 (its monomial vanishes): |F2| / |−4| = 1
+    assert abs(rr - 1.0) <= 1e-15
+    del const
+
+
 def test_newton_quadratic_contraction(orc):
     """Closed form: Newton on x^2 - 4 from 2 + 1e-3: one step error ~ e^2/(2*2) = 2.5e-7 < 1e-5 (S:246)."""
     d = systems.univariate([-4, 0, 1])
