@@ -2,6 +2,7 @@
 
 HC_LIB_PATH=paper_2112_03444_b200/lib_timing/libhc.so python scripts/phase_timing.py [config] [instances]
 Prints, per warp-iteration (one eval + solve per slot), the average cycles of each phase.
+python scripts/phase_timing.py --print a.json b.json   summarises saved outputs.
 """
 import ctypes as C
 import json
@@ -14,6 +15,16 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import bench  # noqa: E402
 from paper_2112_03444_b200 import _lib, hc  # noqa: E402
 
+if len(sys.argv) > 1 and sys.argv[1] == "--print":
+    for f in sys.argv[2:]:
+        try:
+            d = json.load(open(f))
+        except Exception:
+            continue
+        print(f, round(d["cycles_per_iteration"]), d["launch"], d["tracker_ms"])
+        for k, v in d["phases"].items():
+            print("   %-28s %8.0f %5.1f%%" % (k, v["cycles_per_iter"], 100 * v["share"]))
+    sys.exit(0)
 cfg = sys.argv[1] if len(sys.argv) > 1 else "trifocal"
 B = int(sys.argv[2]) if len(sys.argv) > 2 else 64
 d, start, p0, p1s, _, _ = bench.make_workload(cfg, B, 0)
