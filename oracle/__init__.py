@@ -21,8 +21,8 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 _SO = os.path.join(_HERE, "liboracle.so")
 _SRC = [os.path.join(_HERE, "hc_oracle.c"), os.path.join(_HERE, "hc_oracle.h")]
 
-CONVERGED, DIVERGED, STEP_UNDERFLOW, MAX_STEPS, SINGULAR, NONFINITE = range(6)
-STATUS_NAMES = ["CONVERGED", "DIVERGED", "STEP_UNDERFLOW", "MAX_STEPS", "SINGULAR", "NONFINITE"]
+CONVERGED, DIVERGED, STEP_UNDERFLOW, MAX_STEPS, SINGULAR, NONFINITE, AT_INFINITY = range(7)
+STATUS_NAMES = ["CONVERGED", "DIVERGED", "STEP_UNDERFLOW", "MAX_STEPS", "SINGULAR", "NONFINITE", "AT_INFINITY"]
 
 
 def build(force: bool = False) -> str:
@@ -52,7 +52,9 @@ class _Settings(C.Structure):
                 ("shrink", C.c_double), ("max_newton", C.c_int32), ("newton_tol", C.c_double),
                 ("max_steps", C.c_int32), ("inf_norm", C.c_double), ("end_newton", C.c_int32),
                 ("end_tol", C.c_double), ("res_abs", C.c_double), ("res_rel", C.c_double),
-                ("pivot_rel", C.c_double)]
+                ("pivot_rel", C.c_double), ("eg_start", C.c_double), ("eg_inf_mu", C.c_double),
+                ("eg_sing_mu", C.c_double), ("eg_stab", C.c_double), ("eg_inf_s", C.c_double), ("eg_inf_norm", C.c_double), ("eg_samples", C.c_int32), ("eg_max_winding", C.c_int32),
+                ("eg_max_radii", C.c_int32), ("eg_tol", C.c_double)]
 
 
 @dataclass
@@ -74,6 +76,16 @@ class Settings:
     res_abs: float = 1e-10
     res_rel: float = 1e-12
     pivot_rel: float = 1e-14
+    eg_start: float = 0.1          # endgame (reading R26); 0 disables it
+    eg_inf_mu: float = -0.05
+    eg_sing_mu: float = 0.75
+    eg_stab: float = 0.02
+    eg_inf_s: float = 1e-12
+    eg_inf_norm: float = 1e5
+    eg_samples: int = 16
+    eg_max_winding: int = 8
+    eg_max_radii: int = 12
+    eg_tol: float = 1e-10
 
     def _c(self) -> _Settings:
         s = _Settings()
@@ -100,7 +112,8 @@ def lib():
         L.orc_td_start.argtypes = [C.c_int, C.c_void_p, C.c_void_p]
         L.orc_td_start.restype = C.c_int64
         L.orc_track.argtypes = [C.POINTER(_Hom), C.c_void_p, C.c_int64, C.c_void_p, C.c_int64,
-                                C.POINTER(_Settings), C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
+                                C.POINTER(_Settings), C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                                C.c_void_p]
         L.orc_predict.argtypes = [C.POINTER(_Hom), C.POINTER(_Settings), C.c_void_p, C.c_double, C.c_double,
                                   C.c_void_p]
         L.orc_predict.restype = C.c_int
@@ -246,6 +259,7 @@ class TrackResult:
     status: np.ndarray    # [B, S] int32
     counters: np.ndarray  # [B, S, 4] int32: steps, rejections, newton iterations, linear solves
     resid: np.ndarray     # [B, S, 2] float64: ||F||_inf, relative (backward-error) residual
+    winding: np.ndarray   # [B, S] int32: Cauchy endgame winding number (0: not used)
 
 
 def nthreads_default() -> int:
@@ -267,9 +281,10 @@ def track(hom: Homotopy, start_x, p1s=None, settings: Settings | None = None, nt
     status = np.zeros((B, S), np.int32)
     ctr = np.zeros((B, S, 4), np.int32)
     resid = np.zeros((B, S, 2), np.float64)
+    wind = np.zeros((B, S), np.int32)
     lib().orc_track(C.byref(hom.h), _ptr(p1s) if hom.kind == "ph" else None, B, _ptr(start_x), S, C.byref(st),
-                    int(nthreads or nthreads_default()), _ptr(x), _ptr(status), _ptr(ctr), _ptr(resid))
-    return TrackResult(x, status, ctr, resid)
+                    int(nthreads or nthreads_default()), _ptr(x), _ptr(status), _ptr(ctr), _ptr(resid), _ptr(wind))
+    return TrackResult(x, status, ctr, resid, wind)
 
 
 # ---------------------------------------------------------------------------------------

@@ -48,6 +48,17 @@ void orc_settings_default(orc_settings *s) {
   s->res_abs = 1e-10;
   s->res_rel = 1e-12;
   s->pivot_rel = 1e-14;
+  /* endgame: reading R26 (the paper: "extra verification steps are needed") */
+  s->eg_start = 0.1;
+  s->eg_inf_mu = -0.05;
+  s->eg_sing_mu = 0.75;
+  s->eg_stab = 0.02;
+  s->eg_inf_s = 1e-12;
+  s->eg_inf_norm = 1e5;
+  s->eg_samples = 16;
+  s->eg_max_winding = 8;
+  s->eg_max_radii = 12;
+  s->eg_tol = 1e-10;
 }
 
 /* ---------------------------------------------------------------------------------------
@@ -161,11 +172,13 @@ typedef struct {
   cplx *c_one;           /* coefficient values at t = 1 (target) [ncoef] */
   cplx *p_t, *dp;        /* scratch [P] */
   cplx *F, *G, *J;       /* scratch */
-  double t_cached;
+  cplx t_cached;
   int cached;
 } hctx;
 
-static void ctx_coefs(hctx *cx, double t) {
+/* t may be complex (the Cauchy endgame, R26, tracks around |1 - t| = s); p(t) and c(p(t)) are
+ * polynomials, so the same formulas hold. */
+static void ctx_coefs(hctx *cx, cplx t) {
   const orc_sys *s = cx->h->sys;
   if (cx->cached && cx->t_cached == t) return;
   if (cx->h->kind == 1) {
@@ -190,7 +203,7 @@ static void ctx_coefs(hctx *cx, double t) {
 }
 
 /* H, ∂H/∂x, ∂H/∂t at (x, t); any output may be NULL. */
-static void eval_H(hctx *cx, const cplx *x, double t, cplx *H, cplx *Hx, cplx *Ht) {
+static void eval_H(hctx *cx, const cplx *x, cplx t, cplx *H, cplx *Hx, cplx *Ht) {
   const orc_homotopy *h = cx->h;
   const orc_sys *s = h->sys;
   int n = s->n;
@@ -380,7 +393,7 @@ typedef struct {
 } tracker;
 
 /* dx/dt = -(∂H/∂x)^{-1} ∂H/∂t  (Eq. 3).  Returns 0 on success. */
-static int davidenko(tracker *T, const cplx *x, double t, cplx *dxdt) {
+static int davidenko(tracker *T, const cplx *x, cplx t, cplx *dxdt) {
   int n = T->n;
   eval_H(&T->cx, x, t, NULL, T->Hx, T->rhs);
   T->solves++;
@@ -389,15 +402,14 @@ static int davidenko(tracker *T, const cplx *x, double t, cplx *dxdt) {
   return 0;
 }
 
-/* RK4 (P:175) or Euler (Eq. 4): x* from (x, t) with step h.  Returns 0 on success. */
-static int predict(tracker *T, const cplx *x, double t, double h, cplx *xp) {
+/* RK4 or Euler (Eq. 4): x* from (x, t) with step h, given k1 = dx/dt at (x, t) in T->k1.
+ * Returns 0 on success. */
+static int predict_from_k1(tracker *T, const cplx *x, double t, double h, cplx *xp) {
   int n = T->n;
   if (T->st->predictor == 1) {
-    if (davidenko(T, x, t, T->k1)) return 1;
     for (int i = 0; i < n; i++) xp[i] = x[i] + h * T->k1[i];
     return 0;
   }
-  if (davidenko(T, x, t, T->k1)) return 1;
   for (int i = 0; i < n; i++) T->xs[i] = x[i] + 0.5 * h * T->k1[i];
   if (davidenko(T, T->xs, t + 0.5 * h, T->k2)) return 1;
   for (int i = 0; i < n; i++) T->xs[i] = x[i] + 0.5 * h * T->k2[i];
@@ -409,9 +421,15 @@ static int predict(tracker *T, const cplx *x, double t, double h, cplx *xp) {
   return 0;
 }
 
+/* RK4 (P:175) or Euler (Eq. 4): x* from (x, t) with step h.  Returns 0 on success. */
+static int predict(tracker *T, const cplx *x, double t, double h, cplx *xp) {
+  if (davidenko(T, x, t, T->k1)) return 1;
+  return predict_from_k1(T, x, t, h, xp);
+}
+
 /* Newton (Eq. 6): x <- x - (∂H/∂x)^{-1} H at fixed t, <= iters iterations, converged when
  * ||Δ||_inf <= tol * max(1, ||x||_inf).  Returns 1 if converged. */
-static int newton(tracker *T, cplx *x, double t, int iters, double tol, int32_t *count, int *singular) {
+static int newton(tracker *T, cplx *x, cplx t, int iters, double tol, int32_t *count, int *singular) {
   int n = T->n;
   *singular = 0;
   for (int it = 0; it < iters; it++) {
@@ -452,21 +470,205 @@ static void endpoint_residual(tracker *T, const cplx *x, double *r, double *r_re
   free(F); free(den);
 }
 
-static void track_one(tracker *T, const cplx *x0, cplx *x_out, int32_t *status, int32_t *ctr, double *resid) {
+/* ---------------------------------------------------------------------------------------
+ * Endgame (reading R26).  The paper tracks to t = 1 and notes that "the cardinality of the output
+ * is not always correct, and extra verification steps are needed"; a path that ends
+ * at a singular root or at infinity makes the step size collapse near t = 1.  Standard HC
+ * endgames (Morgan, Sommese and Wampler's Cauchy endgame) handle both; this is the plain form:
+ *
+ *  sampling: with s = 1 - t, once s <= eg_start, the first step attempt at s <= s_next records,
+ *    right after the predictor's first stage (k1 = dx/dt at that point, so no extra solve),
+ *    log ||x||_inf and log (s ||dx/dt||_inf), and s_next = s / 2.  Between consecutive samples
+ *    v  = d log ||x|| / d log s          (x ~ s^v: v < 0 means ||x|| grows as s -> 0)
+ *    mu = d log (s ||dx/dt||) / d log s  (x = x* + c s^{1/m}: mu -> 1/m; x ~ s^{-q/m}: mu -> -q/m)
+ *  An estimate is "stable" when mu changed by less than eg_stab since the previous sample (the
+ *  Puiseux regime has been reached: before it a path may look divergent and turn back).
+ *  at infinity: stable, mu < eg_inf_mu and |v - mu| < eg_stab (||x|| ~ s^mu) at three
+ *               consecutive samples                                              -> AT_INFINITY;
+ *  singular:    stable and 0 < mu < eg_sing_mu at three consecutive samples     -> Cauchy endgame;
+ *  otherwise the path is tracked to t = 1 as before (a non-singular endpoint has mu -> 1).
+ *
+ *  Cauchy endgame at radius s: x is tracked around the circle t(theta) = 1 - s e^{i theta}
+ *    (Davidenko in theta: dx/dtheta = dx/dt * dt/dtheta, dt/dtheta = -i s e^{i theta}) in
+ *    eg_samples equal arcs per loop; the loop is repeated until x returns to its start (the
+ *    winding number m = loops, <= eg_max_winding); the endpoint estimate is the mean of the
+ *    m * eg_samples samples (the trapezoidal rule for the Cauchy integral
+ *    x(1) = (1 / 2 pi m) int_0^{2 pi m} x(theta) dtheta, exact for the Puiseux terms below order
+ *    m * eg_samples).  The path then moves radially to s / 2 (ordinary tracking in real t) and the
+ *    loop is repeated; the endgame succeeds when two consecutive estimates agree within
+ *    eg_tol * max(1, ||x||_inf), and the endpoint is classified by its residuals (R10).
+ * --------------------------------------------------------------------------------------- */
+
+/* One RK4 (or Euler) step along the circle t(theta) = 1 - s e^{i theta} from theta to theta + h. */
+static int predict_circle(tracker *T, const cplx *x, double s, double th, double h, cplx *xp) {
+  int n = T->n;
+  cplx *k[4] = {T->k1, T->k2, T->k3, T->k4};
+  const double cst[4] = {0.0, 0.5, 0.5, 1.0};
+  int stages = T->st->predictor == 1 ? 1 : 4;
+  for (int q = 0; q < stages; q++) {
+    double thq = th + cst[q] * h;
+    cplx tq = 1.0 - s * cexp(I * thq), dtdth = -I * s * cexp(I * thq);
+    for (int i = 0; i < n; i++) T->xs[i] = q == 0 ? x[i] : x[i] + cst[q] * h * k[q - 1][i];
+    if (davidenko(T, T->xs, tq, k[q])) return 1;
+    for (int i = 0; i < n; i++) k[q][i] *= dtdth;
+  }
+  for (int i = 0; i < n; i++)
+    xp[i] = stages == 1 ? x[i] + h * k[0][i]
+                        : x[i] + (h / 6.0) * (k[0][i] + 2.0 * k[1][i] + 2.0 * k[2][i] + k[3][i]);
+  return 0;
+}
+
+typedef struct { int32_t steps, rej, newt; } eg_ctr;
+
+/* Track x along the circle of radius s from theta0 to theta1 (landing exactly on theta1) with
+ * the corrector at every step and the step policy R7 in theta.  Returns 0 on success. */
+static int circle_arc(tracker *T, cplx *x, double s, double th0, double th1, eg_ctr *c) {
+  const orc_settings *st = T->st;
+  int n = T->n, sing;
+  cplx *xp = malloc(sizeof(cplx) * n);
+  double th = th0, h = th1 - th0;
+  int fail = 0;
+  while (th < th1) {
+    if (c->steps >= st->max_steps) { fail = 1; break; }
+    c->steps++;
+    double hh = h, tn = th + h;
+    if (tn >= th1) { tn = th1; hh = th1 - th; }
+    int ok = predict_circle(T, x, s, th, hh, xp) == 0;
+    if (ok) ok = newton(T, xp, 1.0 - s * cexp(I * tn), st->max_newton, st->newton_tol, &c->newt, &sing);
+    if (ok) {
+      memcpy(x, xp, sizeof(cplx) * n);
+      th = tn;
+    } else {
+      c->rej++;
+      h *= st->shrink;
+      if (h < st->dt_min) { fail = 1; break; }
+    }
+  }
+  free(xp);
+  return fail;
+}
+
+/* Ordinary tracking in real t from t0 to t1 < 1 (the radial move between Cauchy radii). */
+static int radial(tracker *T, cplx *x, double t0, double t1, eg_ctr *c) {
+  const orc_settings *st = T->st;
+  int n = T->n, sing;
+  cplx *xp = malloc(sizeof(cplx) * n);
+  double t = t0, dt = t1 - t0;
+  int fail = 0;
+  while (t < t1) {
+    if (c->steps >= st->max_steps) { fail = 1; break; }
+    c->steps++;
+    double h = dt, tn = t + dt;
+    if (tn >= t1) { tn = t1; h = t1 - t; }
+    int ok = predict(T, x, t, h, xp) == 0;
+    if (ok) ok = newton(T, xp, tn, st->max_newton, st->newton_tol, &c->newt, &sing);
+    if (ok) {
+      memcpy(x, xp, sizeof(cplx) * n);
+      t = tn;
+    } else {
+      c->rej++;
+      dt *= st->shrink;
+      if (dt < st->dt_min) { fail = 1; break; }
+    }
+  }
+  free(xp);
+  return fail;
+}
+
+/* Cauchy endgame from x at t = 1 - s (real).  On success x holds the endpoint estimate and *m the
+ * winding number; returns 0.  On failure x holds the last tracked point; returns 1. */
+static int cauchy_endgame(tracker *T, cplx *x, double s, eg_ctr *c, int *m) {
+  const orc_settings *st = T->st;
+  int n = T->n, K = st->eg_samples;
+  cplx *xr = malloc(sizeof(cplx) * n), *sum = malloc(sizeof(cplx) * n), *est = malloc(sizeof(cplx) * n);
+  int have_est = 0, fail = 1;
+  for (int r = 0; r < st->eg_max_radii; r++) {
+    memcpy(xr, x, sizeof(cplx) * n);
+    for (int i = 0; i < n; i++) sum[i] = 0;
+    int loops = 0, closed = 0, arc_fail = 0;
+    while (loops < st->eg_max_winding && !closed && !arc_fail) {
+      for (int j = 0; j < K && !arc_fail; j++) {
+        for (int i = 0; i < n; i++) sum[i] += x[i];   /* sample at theta = 2 pi j / K of this loop */
+        arc_fail = circle_arc(T, x, s, 2.0 * M_PI * j / K, 2.0 * M_PI * (j + 1) / K, c);
+      }
+      loops++;
+      if (!arc_fail) {
+        double dmax = 0, xm = vec_norm_inf(n, xr);
+        for (int i = 0; i < n; i++) {
+          double d = cabs(x[i] - xr[i]);
+          if (!(d <= dmax)) dmax = d;
+        }
+        closed = dmax <= 1e-6 * (xm > 1.0 ? xm : 1.0);   /* back on the starting branch */
+      }
+    }
+    if (arc_fail || !closed) break;
+    /* the loop ended where it started: continue from the exact start point (the closed loop only
+     * adds tracking error) */
+    memcpy(x, xr, sizeof(cplx) * n);
+    double scale = 0;
+    int agree = have_est;
+    for (int i = 0; i < n; i++) {
+      cplx e = sum[i] / (double)(loops * K);
+      if (have_est) {
+        double em = cabs(e);
+        if (!(cabs(e - est[i]) <= st->eg_tol * (em > 1.0 ? em : 1.0))) agree = 0;
+      }
+      est[i] = e;
+      if (cabs(e) > scale) scale = cabs(e);
+    }
+    have_est = 1;
+    *m = loops;
+    if (agree) { fail = 0; break; }
+    if (r + 1 < st->eg_max_radii && radial(T, x, 1.0 - s, 1.0 - 0.5 * s, c)) break;
+    s *= 0.5;
+    (void)scale;
+  }
+  if (!fail) memcpy(x, est, sizeof(cplx) * n);
+  free(xr); free(sum); free(est);
+  return fail;
+}
+
+static void track_one(tracker *T, const cplx *x0, cplx *x_out, int32_t *status, int32_t *ctr, double *resid,
+                      int32_t *winding) {
   const orc_settings *st = T->st;
   int n = T->n;
   cplx *x = malloc(sizeof(cplx) * n), *xp = malloc(sizeof(cplx) * n);
   memcpy(x, x0, sizeof(cplx) * n);
   double t = 0.0, dt = st->dt_init;
   int32_t steps = 0, rej = 0, newt = 0, acc = 0;
-  int stat = -1, sing;
+  int stat = -1, sing, wind = 0;
+  /* endgame sampling state (R26) */
+  const int eg_on = st->eg_start > 0.0 && st->eg_start < 1.0;
+  double s_next = st->eg_start, pls = 0, plx = 0, pld = 0, mu_prev = 0;
+  int nsamp = 0, cauchy = 0, inf_run = 0, sing_run = 0;
   T->solves = 0;
   while (t < 1.0) {
     if (steps >= st->max_steps) { stat = ORC_MAX_STEPS; break; }
     steps++;
     double h = dt, t1 = t + dt;
     if (t1 >= 1.0) { t1 = 1.0; h = 1.0 - t; }
-    int ok = predict(T, x, t, h, xp) == 0;
+    /* predictor stage 1: k1 = dx/dt at (x, t) */
+    int ok = davidenko(T, x, t, T->k1) == 0;
+    if (eg_on && ok && 1.0 - t <= s_next) {
+      /* endgame sample at s = 1 - t with k1 = dx/dt at (x, t) */
+      double s = 1.0 - t, ls = log(s), lx = log(vec_norm_inf(n, x)), ldv = log(s * vec_norm_inf(n, T->k1));
+      if (nsamp > 0) {
+        double v = (lx - plx) / (ls - pls), mu = (ldv - pld) / (ls - pls);
+        int stable = nsamp > 1 && fabs(mu - mu_prev) < st->eg_stab;
+        /* at infinity: ||x|| ~ s^v with v = mu < eg_inf_mu, converged (R26) */
+        inf_run = (stable && mu < st->eg_inf_mu && fabs(v - mu) < st->eg_stab) ? inf_run + 1 : 0;
+        if (s > st->eg_inf_s && exp(lx) < st->eg_inf_norm) inf_run = 0;   /* see eg_inf_s, eg_inf_norm */
+        /* finite singular endpoint: mu -> 1/m, 0 < 1/m < eg_sing_mu, converged */
+        sing_run = (stable && mu > 0.0 && mu < st->eg_sing_mu) ? sing_run + 1 : 0;
+        if (inf_run >= 3) { stat = ORC_AT_INFINITY; break; }
+        if (sing_run >= 3) { cauchy = 1; break; }
+        mu_prev = mu;
+      }
+      pls = ls; plx = lx; pld = ldv;
+      nsamp++;
+      s_next = 0.5 * s;
+    }
+    if (ok) ok = predict_from_k1(T, x, t, h, xp) == 0;
     if (ok) ok = newton(T, xp, t1, st->max_newton, st->newton_tol, &newt, &sing);
     if (ok) {
       memcpy(x, xp, sizeof(cplx) * n);
@@ -481,7 +683,20 @@ static void track_one(tracker *T, const cplx *x0, cplx *x_out, int32_t *status, 
     }
   }
   double r = INFINITY, r_rel = INFINITY;
-  if (stat < 0) {
+  if (cauchy) {
+    /* the step attempt that took the sample is abandoned after its first stage */
+    eg_ctr c = {steps, rej, newt};
+    int m = 0;
+    int fail = cauchy_endgame(T, x, 1.0 - t, &c, &m);
+    steps = c.steps; rej = c.rej; newt = c.newt;
+    if (fail) stat = c.steps >= st->max_steps ? ORC_MAX_STEPS : ORC_STEP_UNDERFLOW;
+    else if (!all_finite(n, x)) stat = ORC_NONFINITE;
+    else {
+      wind = m;
+      endpoint_residual(T, x, &r, &r_rel);
+      stat = (r <= st->res_abs || r_rel <= st->res_rel) ? ORC_CONVERGED : ORC_SINGULAR;
+    }
+  } else if (stat < 0) {
     /* endpoint polish on F(.; p1) = H(., 1) */
     int32_t pol = 0;
     newton(T, x, 1.0, st->end_newton, st->end_tol, &pol, &sing);
@@ -496,6 +711,7 @@ static void track_one(tracker *T, const cplx *x0, cplx *x_out, int32_t *status, 
   *status = stat;
   ctr[0] = steps; ctr[1] = rej; ctr[2] = newt; ctr[3] = T->solves;
   resid[0] = r; resid[1] = r_rel;
+  if (winding) *winding = wind;
   free(x); free(xp);
 }
 
@@ -526,6 +742,7 @@ typedef struct {
   double *x_out;
   int32_t *status, *counters;
   double *resid;
+  int32_t *winding;
   int64_t next;   /* dynamic chunking over track ids */
 } job;
 
@@ -548,7 +765,7 @@ static void *worker(void *arg) {
       cur_b = b;
     }
     load_vec(J->start_x + 2 * s * n, n, x0);
-    track_one(&T, x0, xo, J->status + g, J->counters + 4 * g, J->resid + 2 * g);
+    track_one(&T, x0, xo, J->status + g, J->counters + 4 * g, J->resid + 2 * g, J->winding ? J->winding + g : NULL);
     for (int i = 0; i < n; i++) st(J->x_out, g * n + i, xo[i]);
   }
   if (have) tracker_free(&T);
@@ -558,8 +775,8 @@ static void *worker(void *arg) {
 
 void orc_track(const orc_homotopy *h, const double *p1s, int64_t B, const double *start_x, int64_t S,
                const orc_settings *st, int nthreads, double *x_out, int32_t *status, int32_t *counters,
-               double *resid) {
-  job J = {h, p1s, B, S, start_x, st, x_out, status, counters, resid, 0};
+               double *resid, int32_t *winding) {
+  job J = {h, p1s, B, S, start_x, st, x_out, status, counters, resid, winding, 0};
   if (nthreads < 1) nthreads = 1;
   if (nthreads == 1) { worker(&J); return; }
   pthread_t *th = malloc(sizeof(pthread_t) * nthreads);

@@ -53,10 +53,21 @@ typedef struct {
   double end_tol;
   double res_abs, res_rel;
   double pivot_rel;
+  /* endgame (reading R26): 0 < eg_start < 1 enables it (s = 1 - t at which sampling starts) */
+  double eg_start;
+  double eg_inf_mu;      /* at infinity: converged mu = v < eg_inf_mu (three consecutive samples) */
+  double eg_sing_mu;     /* Cauchy endgame: converged 0 < mu < eg_sing_mu (three consecutive samples) */
+  double eg_stab;        /* converged: |mu - mu_prev| < eg_stab (and |v - mu| < eg_stab at infinity) */
+  double eg_inf_s;       /* at infinity is decided only at s <= eg_inf_s or once ||x||_inf >= eg_inf_norm */
+  double eg_inf_norm;
+  int32_t eg_samples;    /* Cauchy: sample points per loop around |1 - t| = s */
+  int32_t eg_max_winding;
+  int32_t eg_max_radii;  /* Cauchy: radii s, s/2, s/4, ... tried */
+  double eg_tol;         /* Cauchy: consecutive estimates agree within eg_tol * max(1, |x|) */
 } orc_settings;
 
 enum { ORC_CONVERGED = 0, ORC_DIVERGED = 1, ORC_STEP_UNDERFLOW = 2, ORC_MAX_STEPS = 3,
-       ORC_SINGULAR = 4, ORC_NONFINITE = 5 };
+       ORC_SINGULAR = 4, ORC_NONFINITE = 5, ORC_AT_INFINITY = 6 };
 
 void orc_settings_default(orc_settings *s);
 
@@ -74,10 +85,11 @@ int64_t orc_td_start(int n, const int32_t *deg, double *x /*[prod*n*2] or NULL*/
 
 /* Track S start points through H for each of B instances (PH: p1 = p1s + b*P*2; TD: B = 1).
  * Outputs per track g = b*S + s: x[g*n*2], status[g], counters[g*4] = (steps, rejections,
- * newton iterations, linear solves), resid[g*2] = (abs, rel).  Multithreaded, deterministic. */
+ * newton iterations, linear solves), resid[g*2] = (abs, rel), winding[g] (0: no Cauchy endgame, else
+ * the winding number it found; may be NULL).  Multithreaded, deterministic. */
 void orc_track(const orc_homotopy *h, const double *p1s, int64_t B,
                const double *start_x, int64_t S, const orc_settings *st, int nthreads,
-               double *x_out, int32_t *status, int32_t *counters, double *resid);
+               double *x_out, int32_t *status, int32_t *counters, double *resid, int32_t *winding);
 
 /* One predictor step from (x, t) with step dt (RK4 or Euler per st->predictor); 0 on success. */
 int orc_predict(const orc_homotopy *h, const orc_settings *st, const double *x, double t, double dt, double *xp);

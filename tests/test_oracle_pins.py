@@ -416,6 +416,67 @@ def test_eco_counts(orc, n, count):
         assert max(abs(eval_poly(f, x)) for f in d.polys) < 1e-10
 
 
+# ---------------------------------------------------------------- endgame (reading R26)
+
+@pytest.mark.parametrize("m", [2, 3, 4])
+def test_cauchy_endgame_winding_and_endpoint(orc, m):
+    """Closed form: F = (x - 2)^m by total degree (G = x^m - 1, which does not vanish at 2).  Near
+    t = 1, (x - 2)^m ~ -s gamma (2^m - 1), so the m paths are the m branches of a Puiseux series in
+    s^{1/m} permuted cyclically around t = 1: the Cauchy endgame must report winding number m for
+    every track and the endpoint 2 to 1e-8 (the plain tracker's Newton polish converges only
+    linearly at a root of multiplicity m)."""
+    from hc_inputs.poly import var_x
+    X = var_x(1, 0, 0)
+    d = systems.from_polys([(X - 2) ** m], f"(x-2)^{m}")
+    res = orc.track(orc.td_homotopy(d, rng.gamma(1)), orc.td_start([m]))
+    assert np.all(res.status == orc.CONVERGED), res.status
+    assert np.all(res.winding == m), res.winding
+    assert np.max(np.abs(res.x[0, :, 0] - 2)) <= 1e-8
+
+
+def test_cauchy_endgame_double_root_2x2(orc):
+    """Closed form: F = ((x - 2)^2 + y - 1, y - 1) has the double root (2, 1) (substitute y = 1);
+    both total-degree paths reach it with winding number 2 and 1e-8 accuracy."""
+    from hc_inputs.poly import var_x
+    x, y = var_x(2, 0, 0), var_x(2, 0, 1)
+    d = systems.from_polys([(x - 2) ** 2 + y - 1, y - 1], "double-root")
+    for g in (1, 2):
+        res = orc.track(orc.td_homotopy(d, rng.gamma(g)), orc.td_start(d.degrees()))
+        assert np.all(res.status == orc.CONVERGED) and np.all(res.winding == 2)
+        assert np.max(np.abs(res.x[0] - np.array([2, 1]))) <= 1e-8
+
+
+def test_endgame_at_infinity_cyclic5(orc):
+    """Textbook count: cyclic-5 has 70 isolated roots of total degree 120, so 50 paths go to
+    infinity.  With the endgame the 70 are found (no root classified at infinity), at least 30 of
+    the other 50 are classified AT_INFINITY by their converged valuation, every AT_INFINITY track
+    fails to converge without the endgame too, and the endgame saves solves."""
+    d = systems.cyclic(5)
+    hom, X0 = orc.td_homotopy(d, rng.gamma(1)), orc.td_start(d.degrees())
+    res = orc.track(hom, X0)
+    U, mult = orc.dedup(orc.finite_solutions(res))
+    assert len(U) == 70 and mult.max() == 1
+    inf = res.status[0] == orc.AT_INFINITY
+    assert 30 <= inf.sum() <= 50
+    st = orc.default_settings()
+    st.eg_start = 0
+    plain = orc.track(hom, X0, settings=st)
+    assert np.all(plain.status[0][inf] != orc.CONVERGED)
+    assert res.counters[0][:, 3].sum() < plain.counters[0][:, 3].sum()
+
+
+def test_endgame_keeps_near_infinity_roots_cyclic7(orc):
+    """cyclic-7 has roots of norm up to 9.41 whose paths look exactly like paths to infinity
+    (||x|| ~ s^{-1/7}) down to s ~ 1e-7 before turning back (SURVEY [X3]); the endgame's
+    eg_inf_s / eg_inf_norm guard must keep all 924 (Table 1) and classify most of the 4116
+    diverging paths AT_INFINITY."""
+    d = systems.cyclic(7)
+    res = orc.track(orc.td_homotopy(d, rng.gamma(CYCLIC7_GAMMA_SEED)), orc.td_start(d.degrees()))
+    U, mult = orc.dedup(orc.finite_solutions(res))
+    assert len(U) == 924 and mult.max() == 1
+    assert (res.status[0] == orc.AT_INFINITY).sum() >= 2000
+
+
 def test_determinism_across_thread_counts(orc):
     """bit-identical results for 1 and 8 threads."""
     d = systems.cyclic(5)
