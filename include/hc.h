@@ -57,7 +57,8 @@ typedef enum {
   HC_STEP_UNDERFLOW = 2, /* step size fell below dt_min */
   HC_MAX_STEPS = 3,      /* more than max_steps step attempts */
   HC_SINGULAR = 4,       /* reached t = 1 but the endpoint failed the residual test (singular/ill-conditioned) */
-  HC_NONFINITE = 5       /* non-finite endpoint */
+  HC_NONFINITE = 5,      /* non-finite endpoint */
+  HC_AT_INFINITY = 6     /* endgame (reading R26): converged valuation ||x|| ~ s^v, v < 0, with s = 1 - t */
 } hc_track_status;
 
 typedef enum { HC_RK4 = 0, HC_EULER = 1 } hc_predictor;
@@ -155,6 +156,27 @@ typedef struct {
   double res_abs;       /* CONVERGED if ||F(x)||_inf <= res_abs (1e-10) ... */
   double res_rel;       /* ... or max_i |F_i| / sum_k |c_ik||m_k(x)| <= res_rel (1e-12) */
   double pivot_rel;     /* a solve fails when |pivot| <= pivot_rel * max|A_ij| (1e-14) */
+  /* Endgame (reading R26; the paper: "the cardinality of the output is not always
+   * correct, and extra verification steps are needed").  With s = 1 - t, once
+   * s <= eg_start every halving of s is sampled at a step start (right after the predictor's
+   * first stage): v = dlog||x||/dlog s and mu = dlog(s ||dx/dt||)/dlog s between samples.
+   * AT_INFINITY: three consecutive samples with |mu - mu_prev| < eg_stab, |v - mu| < eg_stab,
+   * mu < eg_inf_mu, and s <= eg_inf_s or ||x||_inf >= eg_inf_norm.  Cauchy endgame (singular
+   * endpoint, winding number m, mu -> 1/m): three consecutive samples with |mu - mu_prev| < eg_stab
+   * and 0 < mu < eg_sing_mu; the path is tracked around |1 - t| = s in eg_samples arcs per loop until
+   * it closes (m loops, m <= eg_max_winding), the endpoint estimate is the mean of the samples
+   * (Cauchy integral), radii s, s/2, ... (at most eg_max_radii) until two estimates agree within
+   * eg_tol * max(1, ||x||_inf). */
+  double eg_start;      /* 0 disables the endgame (0.1) */
+  double eg_inf_mu;     /* (-0.05) */
+  double eg_sing_mu;    /* (0.75) */
+  double eg_stab;       /* (0.02) */
+  double eg_inf_s;      /* (1e-12) */
+  double eg_inf_norm;   /* (1e5) */
+  int32_t eg_samples;   /* (16) */
+  int32_t eg_max_winding; /* (8) */
+  int32_t eg_max_radii; /* (12) */
+  double eg_tol;        /* (1e-10) */
 } hc_tracker_settings;
 hc_status hc_tracker_settings_default(hc_tracker_settings *out);
 
@@ -179,6 +201,7 @@ typedef struct {
   double *resid_out;           /* [B * S * 2]: ||F||_inf, relative residual; or NULL */
   int32_t memory;              /* hc_memory */
   void *stream;                /* cudaStream_t (NULL = default stream) */
+  int32_t *winding_out;        /* [B * S]: Cauchy endgame winding number (0: not used); or NULL */
 } hc_batch;
 
 /* Enqueue (or, for HC_MEM_HOST, run) one batch.  *out (may be NULL) receives a result handle that
@@ -193,8 +216,9 @@ hc_status hc_track_batch(hc_system sys, const hc_tracker_settings *settings, con
                          hc_result *out);
 /* Block until the batch finished. */
 hc_status hc_result_wait(hc_result res);
-/* Device time in ms between the start of the coefficient prologue and the end of the tracker
- * kernel, measured with CUDA events on the batch stream; also each kernel alone. */
+/* Device time in ms between the start of the coefficient prologue and the end of the batch (the
+ * tracker and, when enabled, the Cauchy endgame kernel), measured with CUDA events on the batch
+ * stream; also the prologue alone and the tracker kernel alone. */
 hc_status hc_result_elapsed_ms(hc_result res, float *total_ms, float *prologue_ms, float *tracker_ms);
 
 /* Launch configuration the tracker kernel used (lanes per track, warps per CTA, persistent CTAs,

@@ -12,8 +12,8 @@ _PKG = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("HC_LIB_PATH") or os.path.join(_PKG, "lib", "libhc.so")
 
 HC_OK, HC_E_INVALID_ARG, HC_E_TOO_LARGE, HC_E_CUDA, HC_E_OOM, HC_E_INTERNAL = range(6)
-HC_CONVERGED, HC_DIVERGED, HC_STEP_UNDERFLOW, HC_MAX_STEPS, HC_SINGULAR, HC_NONFINITE = range(6)
-STATUS_NAMES = ["CONVERGED", "DIVERGED", "STEP_UNDERFLOW", "MAX_STEPS", "SINGULAR", "NONFINITE"]
+HC_CONVERGED, HC_DIVERGED, HC_STEP_UNDERFLOW, HC_MAX_STEPS, HC_SINGULAR, HC_NONFINITE, HC_AT_INFINITY = range(7)
+STATUS_NAMES = ["CONVERGED", "DIVERGED", "STEP_UNDERFLOW", "MAX_STEPS", "SINGULAR", "NONFINITE", "AT_INFINITY"]
 HC_RK4, HC_EULER = 0, 1
 HC_MEM_DEVICE, HC_MEM_HOST = 0, 1
 
@@ -56,14 +56,17 @@ class hc_tracker_settings(C.Structure):
                 ("shrink", C.c_double), ("max_newton", C.c_int32), ("newton_tol", C.c_double),
                 ("max_steps", C.c_int32), ("inf_norm", C.c_double), ("end_newton", C.c_int32),
                 ("end_tol", C.c_double), ("res_abs", C.c_double), ("res_rel", C.c_double),
-                ("pivot_rel", C.c_double)]
+                ("pivot_rel", C.c_double), ("eg_start", C.c_double), ("eg_inf_mu", C.c_double),
+                ("eg_sing_mu", C.c_double), ("eg_stab", C.c_double), ("eg_inf_s", C.c_double),
+                ("eg_inf_norm", C.c_double), ("eg_samples", C.c_int32), ("eg_max_winding", C.c_int32),
+                ("eg_max_radii", C.c_int32), ("eg_tol", C.c_double)]
 
 
 class hc_batch(C.Structure):
     _fields_ = [("n_instances", C.c_int64), ("n_start", C.c_int64), ("start_x", C.c_void_p),
                 ("p_start", C.c_void_p), ("p_target", C.c_void_p), ("x_out", C.c_void_p),
                 ("status_out", C.c_void_p), ("counters_out", C.c_void_p), ("resid_out", C.c_void_p),
-                ("memory", C.c_int32), ("stream", C.c_void_p)]
+                ("memory", C.c_int32), ("stream", C.c_void_p), ("winding_out", C.c_void_p)]
 
 
 class hc_track_info(C.Structure):

@@ -44,7 +44,22 @@ struct CoefMono {
 
 struct DevSettings {
   double dt_init, dt_min, dt_max, grow, shrink, newton_tol, inf_norm, end_tol, res_abs, res_rel, pivot_rel;
+  // endgame (reading R26; hc.h documents each field)
+  double eg_start, eg_inf_mu, eg_sing_mu, eg_stab, eg_inf_s, eg_inf_norm, eg_tol;
   int32_t predictor, grow_after, max_newton, max_steps, end_newton;
+  int32_t eg_samples, eg_max_winding, eg_max_radii;
+};
+
+// Internal track status: handed from the tracker to the Cauchy endgame kernel (never returned).
+constexpr int32_t HC_EG_PENDING = 7;
+
+// Per-slot endgame sampling state of the tracker kernel (shared memory, written by lane 0 of the
+// slot): next sample point, the previous sample (log s, log ||x||, log s||dx/dt||), previous mu,
+// the current norms, and the run lengths of the at-infinity / singular conditions (reading R26).
+struct EgSample {
+  double s_next, pls, plx, pld, mu_prev;
+  double xn2, kn2;   // ||x||_inf^2 at the last accepted point, ||k1||_inf^2 of the current step
+  int32_t nsamp, inf_run, sing_run, pad;
 };
 
 struct TrackArgs {
@@ -69,6 +84,9 @@ struct TrackArgs {
   int32_t *status_out;       // [total]
   int32_t *counters_out;     // [total][4]
   double *resid_out;         // [total][2]
+  int32_t *winding_out;      // [total] Cauchy endgame winding number (0: not used)
+  int64_t *eg_list;          // [total] tracks handed to the Cauchy endgame (status HC_EG_PENDING)
+  unsigned long long *eg_count;  // [2]: tracks in eg_list; the endgame kernel's work counter
   DevSettings st;
   unsigned long long *phase_cycles;  // [8] per-phase clock sums (only in HCB_PHASE_TIMING builds), or null
 };

@@ -20,6 +20,7 @@ HCB_DECLW(9) HCB_DECLW(10) HCB_DECLW(11) HCB_DECLW(12) HCB_DECLW(13) HCB_DECLW(1
 #undef HCB_DECLW
 #define HCB_DECL(N)                                                                                      \
   cudaError_t launch_tracker_##N(const TrackArgs &, int, cudaStream_t, TrackerPlan *);                  \
+  cudaError_t launch_endgame_##N(const TrackArgs &, int, cudaStream_t);                                 \
   cudaError_t launch_zgesv_##N(int64_t, const double2 *, const double2 *, double2 *, int32_t *, double, \
                                cudaStream_t);
 HCB_DECL(1) HCB_DECL(2) HCB_DECL(3) HCB_DECL(4) HCB_DECL(5) HCB_DECL(6) HCB_DECL(7) HCB_DECL(8)
@@ -46,6 +47,15 @@ static const zgesv_fn kZgesv[33] = {
     launch_zgesv_30,  launch_zgesv_31, launch_zgesv_32};
 
 tracker_launch_fn tracker_launcher(int N) { return (N >= 1 && N <= 32) ? kTrackers[N] : nullptr; }
+typedef cudaError_t (*endgame_fn)(const TrackArgs &, int, cudaStream_t);
+static const endgame_fn kEndgame[33] = {
+    nullptr,            launch_endgame_1,  launch_endgame_2,  launch_endgame_3,  launch_endgame_4,
+    launch_endgame_5,   launch_endgame_6,  launch_endgame_7,  launch_endgame_8,  launch_endgame_9,
+    launch_endgame_10,  launch_endgame_11, launch_endgame_12, launch_endgame_13, launch_endgame_14,
+    launch_endgame_15,  launch_endgame_16, launch_endgame_17, launch_endgame_18, launch_endgame_19,
+    launch_endgame_20,  launch_endgame_21, launch_endgame_22, launch_endgame_23, launch_endgame_24,
+    launch_endgame_25,  launch_endgame_26, launch_endgame_27, launch_endgame_28, launch_endgame_29,
+    launch_endgame_30,  launch_endgame_31, launch_endgame_32};
 // the wide latency layout (32 lanes per track) for N <= 16
 static const tracker_launch_fn kTrackersWide[17] = {
     nullptr,               launch_tracker_wide_1,  launch_tracker_wide_2,  launch_tracker_wide_3,
@@ -109,13 +119,14 @@ struct hc_result_s {
   cudaStream_t stream = nullptr;
   int64_t B = 0, S = 0, total = 0;
   int memory = HC_MEM_DEVICE;
-  cudaEvent_t ev[3] = {nullptr, nullptr, nullptr};
+  cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};   // prologue start, tracker start, end, endgame start
   // device buffers owned by the result (freed on destroy)
   std::vector<void *> owned;
   // where the outputs are (device or host)
   hc_complex *x = nullptr;
   int32_t *status = nullptr, *counters = nullptr;
   double *resid = nullptr;
+  int32_t *winding = nullptr;
   bool outputs_on_host = false;
   bool waited = false;
   TrackerPlan plan{};
@@ -167,6 +178,17 @@ hc_status hc_tracker_settings_default(hc_tracker_settings *s) {
   s->res_abs = 1e-10;
   s->res_rel = 1e-12;
   s->pivot_rel = 1e-14;
+  // endgame, reading R26
+  s->eg_start = 0.1;
+  s->eg_inf_mu = -0.05;
+  s->eg_sing_mu = 0.75;
+  s->eg_stab = 0.02;
+  s->eg_inf_s = 1e-12;
+  s->eg_inf_norm = 1e5;
+  s->eg_samples = 16;
+  s->eg_max_winding = 8;
+  s->eg_max_radii = 12;
+  s->eg_tol = 1e-10;
   return HC_OK;
 }
 
@@ -424,6 +446,11 @@ static hc_status check_settings(const hc_tracker_settings &s) {
     return fail(HC_E_INVALID_ARG, "iteration counts");
   if (!(s.newton_tol > 0) || !(s.inf_norm > 0) || !(s.end_tol > 0) || !(s.pivot_rel >= 0))
     return fail(HC_E_INVALID_ARG, "tolerances");
+  if (!(s.eg_start >= 0.0 && s.eg_start < 1.0)) return fail(HC_E_INVALID_ARG, "need 0 <= eg_start < 1");
+  if (s.eg_start > 0.0 && (s.eg_samples < 2 || s.eg_max_winding < 1 || s.eg_max_radii < 2 || !(s.eg_stab > 0) ||
+                           !(s.eg_tol > 0) || !(s.eg_inf_s >= 0) || !(s.eg_inf_norm > 0) || !(s.eg_sing_mu > 0) ||
+                           !(s.eg_inf_mu < 0)))
+    return fail(HC_E_INVALID_ARG, "endgame settings");
   return HC_OK;
 }
 
@@ -496,7 +523,7 @@ hc_status hc_track_batch(hc_system sys, const hc_tracker_settings *settings, con
   const double2 *d_p0 = reinterpret_cast<const double2 *>(bt->p_start);
   const double2 *d_p1 = reinterpret_cast<const double2 *>(bt->p_target);
   double2 *d_x = reinterpret_cast<double2 *>(bt->x_out);
-  int32_t *d_status = bt->status_out, *d_ctr = bt->counters_out;
+  int32_t *d_status = bt->status_out, *d_ctr = bt->counters_out, *d_wind = bt->winding_out;
   double *d_resid = bt->resid_out;
   if (host) {
     double2 *a, *b0 = nullptr, *b1 = nullptr;
@@ -517,6 +544,8 @@ hc_status hc_track_batch(hc_system sys, const hc_tracker_settings *settings, con
     d_status = nullptr;
     d_ctr = nullptr;
     d_resid = nullptr;
+    d_wind = nullptr;
+    if (bt->winding_out && (s = dev_alloc(r, &d_wind, (size_t)total)) != HC_OK) return bail(s);
   }
   if (!d_x && (s = dev_alloc(r, &d_x, (size_t)total * N)) != HC_OK) return bail(s);
   if (!d_status && (s = dev_alloc(r, &d_status, (size_t)total)) != HC_OK) return bail(s);
@@ -525,9 +554,12 @@ hc_status hc_track_batch(hc_system sys, const hc_tracker_settings *settings, con
   double2 *d_coef = nullptr;
   unsigned long long *d_queue = nullptr;
   if ((s = dev_alloc(r, &d_coef, (size_t)B * (cs.D + 1) * cs.ncoef)) != HC_OK) return bail(s);
-  if ((s = dev_alloc(r, &d_queue, 1)) != HC_OK) return bail(s);
-  if (cudaMemsetAsync(d_queue, 0, sizeof(unsigned long long), r->stream) != cudaSuccess)
+  // work counters: [0] the tracker's queue, [1] tracks handed to the endgame, [2] the endgame's queue
+  if ((s = dev_alloc(r, &d_queue, 3)) != HC_OK) return bail(s);
+  if (cudaMemsetAsync(d_queue, 0, 3 * sizeof(unsigned long long), r->stream) != cudaSuccess)
     return bail(cuda_fail(cudaGetLastError(), "memset queue"));
+  int64_t *d_eg_list = nullptr;
+  if (st.eg_start > 0.0 && (s = dev_alloc(r, &d_eg_list, (size_t)total)) != HC_OK) return bail(s);
   // P == 0: coefficients are constants; feed the prologue a dummy parameter vector
   double2 *d_dummy = nullptr;
   if (P == 0) {
@@ -574,6 +606,19 @@ hc_status hc_track_batch(hc_system sys, const hc_tracker_settings *settings, con
   ta.status_out = d_status;
   ta.counters_out = d_ctr;
   ta.resid_out = d_resid;
+  ta.winding_out = d_wind;
+  ta.eg_list = d_eg_list;
+  ta.eg_count = d_queue + 1;
+  ta.st.eg_start = st.eg_start;
+  ta.st.eg_inf_mu = st.eg_inf_mu;
+  ta.st.eg_sing_mu = st.eg_sing_mu;
+  ta.st.eg_stab = st.eg_stab;
+  ta.st.eg_inf_s = st.eg_inf_s;
+  ta.st.eg_inf_norm = st.eg_inf_norm;
+  ta.st.eg_tol = st.eg_tol;
+  ta.st.eg_samples = st.eg_samples;
+  ta.st.eg_max_winding = st.eg_max_winding;
+  ta.st.eg_max_radii = st.eg_max_radii;
   ta.st.dt_init = st.dt_init;
   ta.st.dt_min = st.dt_min;
   ta.st.dt_max = st.dt_max;
@@ -602,6 +647,25 @@ hc_status hc_track_batch(hc_system sys, const hc_tracker_settings *settings, con
 #endif
   e = (wide ? tracker_launcher_wide(N) : tracker_launcher(N))(ta, sys->device, r->stream, &r->plan);
   if (e != cudaSuccess) return bail(cuda_fail(e, "tracker launch"));
+  cudaEventRecord(r->ev[3], r->stream);
+  // ---- the Cauchy endgame (reading R26) over the tracks the tracker handed over; the count stays
+  //      on the device, so an empty list costs one short launch and no host synchronisation.  It
+  //      runs on the throughput-layout tables (the coefficient slots are the same in both layouts) ----
+  if (st.eg_start > 0.0) {
+    TrackArgs ea = ta;
+    ea.ops = sys->dt.d_ops;
+    ea.Q = sys->cs.Q;
+    ea.mono_prog = sys->dt.d_mono_prog;
+    ea.n_mono = sys->cs.n_mono;
+    ea.n_levels = sys->cs.n_levels;
+    for (int l = 0; l < MAX_LEVELS; ++l) ea.level_end[l] = sys->cs.level_end[l];
+    ea.mpos = sys->dt.d_mpos;
+    ea.n_entries = sys->cs.n_entries;
+    if (sys->cs.ncoef != cs.ncoef || sys->cs.D != cs.D || sys->cs.ncoef_src != cs.ncoef_src)
+      return bail(fail(HC_E_INTERNAL, "lane layouts disagree on coefficient slots"));
+    e = kEndgame[N](ea, sys->device, r->stream);
+    if (e != cudaSuccess) return bail(cuda_fail(e, "endgame launch"));
+  }
   cudaEventRecord(r->ev[2], r->stream);
 
   if (host) {
@@ -617,6 +681,9 @@ hc_status hc_track_batch(hc_system sys, const hc_tracker_settings *settings, con
     if (bt->resid_out && cudaMemcpyAsync(bt->resid_out, d_resid, sizeof(double) * total * 2,
                                          cudaMemcpyDeviceToHost, r->stream) != cudaSuccess)
       return bail(cuda_fail(cudaGetLastError(), "D2H resid"));
+    if (bt->winding_out && cudaMemcpyAsync(bt->winding_out, d_wind, sizeof(int32_t) * total,
+                                           cudaMemcpyDeviceToHost, r->stream) != cudaSuccess)
+      return bail(cuda_fail(cudaGetLastError(), "D2H winding"));
     if (cudaStreamSynchronize(r->stream) != cudaSuccess) return bail(cuda_fail(cudaGetLastError(), "sync"));
     r->waited = true;
   }
@@ -624,6 +691,7 @@ hc_status hc_track_batch(hc_system sys, const hc_tracker_settings *settings, con
   r->status = d_status;
   r->counters = d_ctr;
   r->resid = d_resid;
+  r->winding = d_wind;
   if (out) *out = r;
   else if (!host) {
     // fire-and-forget: the caller owns all outputs; release our buffers after the stream passes
@@ -649,7 +717,7 @@ hc_status hc_result_elapsed_ms(hc_result r, float *total, float *prologue, float
   float a = 0, b = 0, c = 0;
   CK(cudaEventElapsedTime(&a, r->ev[0], r->ev[2]));
   CK(cudaEventElapsedTime(&b, r->ev[0], r->ev[1]));
-  CK(cudaEventElapsedTime(&c, r->ev[1], r->ev[2]));
+  CK(cudaEventElapsedTime(&c, r->ev[1], r->ev[3]));   // the tracker kernel alone (not the endgame)
   if (total) *total = a;
   if (prologue) *prologue = b;
   if (tracker) *tracker = c;

@@ -96,6 +96,9 @@ __device__ __forceinline__ double2 shfl2(double2 v, int src, int width) {
   return make_double2(__shfl_sync(FULL, v.x, src, width), __shfl_sync(FULL, v.y, src, width));
 }
 
+#ifndef HCB_EG_SAMPLING   // endgame sampling in the tracker (A/B switch; 0 = no endgame hand-off)
+#define HCB_EG_SAMPLING 1
+#endif
 #ifndef HCB_SEG16_REDUX   // 8- and 16-lane tracks: REDUX-based segment max / arg-max (A/B switch)
 #define HCB_SEG16_REDUX 1
 #endif
@@ -580,16 +583,39 @@ __device__ __forceinline__ void horner(const double2 *__restrict__ ct, double t,
   }
 }
 
+// Coefficient values at a complex t (the Cauchy endgame tracks around |1 - t| = s, reading R26):
+// the same Horner recurrences in complex arithmetic, any degree D.
+template <int L>
+__device__ __forceinline__ void horner_c(const double2 *__restrict__ ct, double2 t, int D, int ncoef, int nsrc,
+                                         double2 *__restrict__ cval, int r) {
+  for (int j = r; j < ncoef; j += L) {
+    double2 p = __ldg(&ct[(size_t)D * ncoef + j]), q = make_double2(0.0, 0.0);
+#pragma unroll 1
+    for (int d = D - 1; d >= 0; --d) {
+      const double2 c = __ldg(&ct[(size_t)d * ncoef + j]);
+      q = cfma(q, t, p);   // q = q t + p
+      p = cfma(p, t, c);   // p = p t + c
+    }
+    cval[j] = p;
+    if (j < nsrc) cval[ncoef + j] = q;
+  }
+}
+
+template <typename T>
+struct is_complex_t { static constexpr bool value = false; };
+template <>
+struct is_complex_t<double2> { static constexpr bool value = true; };
+
 // ------------------------------------------------------------------------------------------
 // Evaluate [dH/dx | rhs] into the slot's M (shared), then fused LU + solve.  Returns the solution
 // component y_r in lane r (r < N) and whether the solve succeeded (uniform over the slot).
 // rhs_off = 0 -> rhs = H (coefficients c(t)); rhs_off = ncoef -> rhs = dH/dt (coefficients c'(t)).
 // ------------------------------------------------------------------------------------------
-template <int N, int L, int NC>
+template <int N, int L, int NC, typename TT>
 __device__ __forceinline__ bool eval_solve(const TrackArgs &A, const uint2 *__restrict__ ops_s,
                                            const uint32_t *__restrict__ prog_s, const int16_t *__restrict__ mpos_s,
                                            const int16_t *__restrict__ row_of, const double2 *__restrict__ ct,
-                                           double t, bool need_coef, int rhs_off, bool want_abs, double2 *cval,
+                                           TT t, bool need_coef, int rhs_off, bool want_abs, double2 *cval,
                                            double2 *mono,
                                            double2 *M, double2 *prow, double *rabs, int r, int seg,
                                            const double2 (&xr)[NC],
@@ -607,7 +633,9 @@ __device__ __forceinline__ bool eval_solve(const TrackArgs &A, const uint2 *__re
   if constexpr (NC == 2) {
     if (r < E) mono[16 + r] = xr[NC - 1];
   }
-  if (need_coef) switch (D) {   // D is uniform: the common degrees keep all loads of a coefficient in flight together
+  if constexpr (is_complex_t<TT>::value) {
+    if (need_coef) horner_c<L>(ct, t, D, ncoef, A.ncoef_src, cval, r);
+  } else if (need_coef) switch (D) {   // D is uniform: the common degrees keep all loads of a coefficient in flight together
     case 1: horner<1, L>(ct, t, ncoef, A.ncoef_src, cval, r); break;
     case 2: horner<2, L>(ct, t, ncoef, A.ncoef_src, cval, r); break;
     case 3: horner<3, L>(ct, t, ncoef, A.ncoef_src, cval, r); break;
@@ -738,7 +766,8 @@ __device__ __forceinline__ void track_body(const TrackArgs &A) {
   const int slot = warp * TPW + seg;
   const int ncoef = A.ncoef, D = A.D;
   unsigned char *sb = slots_base + (size_t)slot * slot_bytes(N, ncoef, A.ncoef_src, A.n_mono, A.n_entries + 1);
-  double2 *cval = reinterpret_cast<double2 *>(sb);
+  EgSample *egs = reinterpret_cast<EgSample *>(sb);   // endgame sampling state (R26), lane 0 writes
+  double2 *cval = reinterpret_cast<double2 *>(sb + EG_SAMPLE_BYTES);
   double2 *mono = cval + ncoef + A.ncoef_src;
   double2 *M = mono + A.n_mono;
   double2 *prow = M + A.n_entries + 1;
@@ -765,6 +794,7 @@ __device__ __forceinline__ void track_body(const TrackArgs &A) {
   auto comp_valid = [&](int c) -> bool { return c == 0 ? (r < N) : (r < E); };
   auto comp_row = [&](int c) -> int { return c == 0 ? r : 16 + r; };
   bool need_track = true;
+  bool fresh_k1 = false;   // the last solve was a successful RK stage 1 (endgame sampling)
   double cval_t = -1.0;   // t at which the slot's coefficient values were last evaluated (-1: none)
 #ifdef HCB_PHASE_TIMING
   unsigned long long hcb_phase[8] = {0, 0, 0, 0, 0, 0, 0, 0};
@@ -797,6 +827,10 @@ __device__ __forceinline__ void track_body(const TrackArgs &A) {
       int4 c = make_int4(steps, rej, newt, solves);
       reinterpret_cast<int4 *>(A.counters_out)[g] = c;
       reinterpret_cast<double2 *>(A.resid_out)[g] = make_double2(ra, rr);
+      if (A.winding_out) A.winding_out[g] = 0;
+      // a singular endpoint (reading R26): the Cauchy endgame kernel continues this track from
+      // (x, t = 1 - ra); the list entry is the track id
+      if (status == HC_EG_PENDING) A.eg_list[atomicAdd(A.eg_count, 1ULL)] = g;
     }
     need_track = true;
     state = ST_DONE;
@@ -821,6 +855,12 @@ __device__ __forceinline__ void track_body(const TrackArgs &A) {
           t = 0.0;
           dt = st.dt_init;
           acc = steps = rej = newt = solves = 0;
+          if (r == 0) {   // endgame sampling state (read again only after eval_solve's __syncwarp)
+            egs->s_next = st.eg_start;
+            egs->mu_prev = 0.0;
+            egs->xn2 = 0.0;   // (no sample is taken at t = 0: s = 1 > eg_start)
+            egs->nsamp = egs->inf_run = egs->sing_run = 0;
+          }
           begin_step();
         } else {
           state = ST_DONE;
@@ -829,6 +869,48 @@ __device__ __forceinline__ void track_body(const TrackArgs &A) {
         }
       }
     }
+    // ---- endgame sampling (reading R26): at the first step start with s = 1 - t <= s_next, right
+    //      after the predictor's first stage (k1 = dx/dt = -y), record log ||x||, log s||k1||;
+    //      between samples v = dlog||x||/dlog s, mu = dlog(s||dx/dt||)/dlog s.  Three consecutive
+    //      converged samples with mu = v < eg_inf_mu (and s <= eg_inf_s or ||x|| >= eg_inf_norm)
+    //      -> AT_INFINITY; with 0 < mu < eg_sing_mu -> the Cauchy endgame kernel. ----
+    //      (Taken at the top of the iteration after that stage, where fewer values are live; the norms
+    //      come from the reductions the solves already did: ||x|| at the last accept, ||k1||.)
+    if (HCB_EG_SAMPLING && st.eg_start > 0.0) {
+      bool eg_inf = false, eg_cauchy = false;
+      const bool want = fresh_k1 && (1.0 - t) <= egs->s_next;
+      fresh_k1 = false;
+      if (__any_sync(FULL, want)) {
+        __syncwarp();   // lane 0's xn2 / kn2 stores of the previous iterations are visible
+        EgSample e = *egs;
+        if (want) {
+          const double s = 1.0 - t, xn = sqrt(e.xn2), kn = sqrt(e.kn2);
+          const double ls = log(s), lx = log(xn), ldv = log(s * kn);
+          if (e.nsamp > 0) {
+            const double v = (lx - e.plx) / (ls - e.pls), mu = (ldv - e.pld) / (ls - e.pls);
+            const bool stable = e.nsamp > 1 && fabs(mu - e.mu_prev) < st.eg_stab;
+            int inf_run = (stable && mu < st.eg_inf_mu && fabs(v - mu) < st.eg_stab) ? e.inf_run + 1 : 0;
+            if (s > st.eg_inf_s && xn < st.eg_inf_norm) inf_run = 0;
+            const int sing_run = (stable && mu > 0.0 && mu < st.eg_sing_mu) ? e.sing_run + 1 : 0;
+            eg_inf = inf_run >= 3;
+            eg_cauchy = !eg_inf && sing_run >= 3;
+            e.mu_prev = mu;
+            e.inf_run = inf_run;
+            e.sing_run = sing_run;
+          }
+          e.pls = ls;
+          e.plx = lx;
+          e.pld = ldv;
+          e.nsamp += 1;
+          e.s_next = 0.5 * s;
+        }
+        __syncwarp();
+        if (want && r == 0) *egs = e;
+      }
+      if (eg_inf) finish(HC_AT_INFINITY, INFINITY, INFINITY);
+      else if (eg_cauchy) finish(HC_EG_PENDING, 1.0 - t, 0.0);   // x and s = 1 - t for the endgame kernel
+    }
+
     if (__all_sync(FULL, state == ST_DONE)) break;
 #ifdef HCB_PHASE_TIMING
     hcb_iter0 = clock64();
@@ -915,6 +997,8 @@ __device__ __forceinline__ void track_body(const TrackArgs &A) {
         reject = true;
       } else {
         const double w = (stage == 0 || stage == 3) ? 1.0 : 2.0;
+        fresh_k1 = stage == 0;   // k1 = dx/dt at the step start: an endgame sample point (R26)
+        if (stage == 0 && r == 0) egs->kn2 = d2;   // ||k1||^2 (k1 = -y)
 #pragma unroll
         for (int c = 0; c < NC; ++c) {
           const double2 k = make_double2(-yv[c].x, -yv[c].y);
@@ -966,6 +1050,7 @@ __device__ __forceinline__ void track_body(const TrackArgs &A) {
     if (accept) {
 #pragma unroll
       for (int c = 0; c < NC; ++c) x[c] = xc[c];
+      if (r == 0) egs->xn2 = c2;   // ||x||^2 of the accepted point (endgame samples)
       t = t1;
       if (++acc >= st.grow_after) {
         dt = fmin(dt * st.grow, st.dt_max);

@@ -1,4 +1,5 @@
-// Instantiation of the fused tracker and the batched LU solve for N = 10 (see tracker.cuh, zgesv.cuh).
+// Instantiation of the fused tracker, the Cauchy endgame and the batched LU solve for N = 10 (see tracker.cuh, endgame.cuh, zgesv.cuh).
+#include "endgame.cuh"
 #include "zgesv.cuh"
 namespace hcb {
 cudaError_t launch_tracker_10(const TrackArgs &A, int device, cudaStream_t s, TrackerPlan *p) {
@@ -11,5 +12,8 @@ cudaError_t launch_tracker_wide_10(const TrackArgs &A, int device, cudaStream_t 
 cudaError_t launch_zgesv_10(int64_t batch, const double2 *A, const double2 *b, double2 *x, int32_t *info,
                            double pivot_rel, cudaStream_t s) {
   return launch_zgesv_n<10>(batch, A, b, x, info, pivot_rel, s);
+}
+cudaError_t launch_endgame_10(const TrackArgs &A, int device, cudaStream_t s) {
+  return launch_endgame_n<10>(A, device, s);
 }
 }  // namespace hcb

@@ -13,7 +13,8 @@ from dataclasses import dataclass
 import numpy as np
 
 from . import _lib as L
-from ._lib import (HC_CONVERGED, HC_DIVERGED, HC_EULER, HC_MAX_STEPS, HC_MEM_DEVICE, HC_MEM_HOST,  # noqa: F401
+from ._lib import (HC_AT_INFINITY, HC_CONVERGED, HC_DIVERGED, HC_EULER, HC_MAX_STEPS, HC_MEM_DEVICE,  # noqa: F401
+                   HC_MEM_HOST,
                    HC_NONFINITE, HC_RK4, HC_SINGULAR, HC_STEP_UNDERFLOW, STATUS_NAMES, HCError, check)
 
 
@@ -141,6 +142,7 @@ class BatchResult:
     counters: object   # [B, S, 4] int32: steps, rejections, newton iterations, solves
     resid: object      # [B, S, 2] float64
     handle: object = None
+    winding: object = None   # [B, S] int32: Cauchy endgame winding number (0: not used), or None
 
     def elapsed_ms(self):
         """(total, prologue, tracker) device ms from the CUDA events on the batch stream."""
@@ -187,18 +189,22 @@ def track_batch(system: System, start_x, p0=None, p1=None, st: L.hc_tracker_sett
         B = p1.shape[0]
     else:
         B = 1 if p1 is None else int(torch.as_tensor(p1).reshape(-1, 1).shape[0])
+    wind = None
     if out is None:
         x = torch.empty((B, S, N), dtype=torch.complex128, device=dev)
         status = torch.empty((B, S), dtype=torch.int32, device=dev)
         ctr = torch.empty((B, S, 4), dtype=torch.int32, device=dev)
         resid = torch.empty((B, S, 2), dtype=torch.float64, device=dev)
+        wind = torch.empty((B, S), dtype=torch.int32, device=dev)
     else:
-        x, status, ctr, resid = out
+        x, status, ctr, resid = out[:4]
+        wind = out[4] if len(out) > 4 else None
         # the kernel writes B*S*N values through raw pointers: a wrong buffer would be an
         # out-of-bounds device write, so every output is checked before the launch
         for name, tns, shape, dtype in (("x", x, (B, S, N), torch.complex128), ("status", status, (B, S), torch.int32),
                                         ("counters", ctr, (B, S, 4), torch.int32),
-                                        ("resid", resid, (B, S, 2), torch.float64)):
+                                        ("resid", resid, (B, S, 2), torch.float64)) + (
+                                            (("winding", wind, (B, S), torch.int32),) if wind is not None else ()):
             if (tuple(tns.shape) != shape or tns.dtype != dtype or not tns.is_contiguous() or tns.device != dev):
                 raise ValueError(f"out[{name}] must be a contiguous {dtype} tensor of shape {shape} on {dev}, "
                                  f"got {tns.dtype} {tuple(tns.shape)} on {tns.device}")
@@ -206,11 +212,11 @@ def track_batch(system: System, start_x, p0=None, p1=None, st: L.hc_tracker_sett
         stream = torch.cuda.current_stream(dev)
     b = L.hc_batch(B, S, start_x.data_ptr(), p0.data_ptr() if system.P else None,
                    p1.data_ptr() if system.P else None, x.data_ptr(), status.data_ptr(), ctr.data_ptr(),
-                   resid.data_ptr(), HC_MEM_DEVICE, stream.cuda_stream)
+                   resid.data_ptr(), HC_MEM_DEVICE, stream.cuda_stream, wind.data_ptr() if wind is not None else None)
     h = C.c_void_p()
     check(L.lib().hc_track_batch(system.h, C.byref(st or hc_tracker_settings_default()), C.byref(b), C.byref(h)),
           "hc_track_batch")
-    res = BatchResult(x, status, ctr, resid, h)
+    res = BatchResult(x, status, ctr, resid, h, wind)
     res._keep = (start_x, p0, p1, system)   # the system must outlive the result
     return res
 
@@ -228,25 +234,29 @@ def track_batch_host(system: System, start_x, p0=None, p1=None, st: L.hc_tracker
         B = p1.shape[0]
     else:
         B = 1
+    wind = None
     if out is None:
         x = np.empty((B, S, N), np.complex128)
         status = np.empty((B, S), np.int32)
         ctr = np.empty((B, S, 4), np.int32)
         resid = np.empty((B, S, 2), np.float64)
+        wind = np.empty((B, S), np.int32)
     else:
-        x, status, ctr, resid = out
+        x, status, ctr, resid = out[:4]
+        wind = out[4] if len(out) > 4 else None
         for name, a, shape, dtype in (("x", x, (B, S, N), np.complex128), ("status", status, (B, S), np.int32),
-                                      ("counters", ctr, (B, S, 4), np.int32), ("resid", resid, (B, S, 2), np.float64)):
+                                      ("counters", ctr, (B, S, 4), np.int32), ("resid", resid, (B, S, 2), np.float64)) + (
+                                          (("winding", wind, (B, S), np.int32),) if wind is not None else ()):
             if a.shape != shape or a.dtype != dtype or not a.flags.c_contiguous:
                 raise ValueError(f"out[{name}] must be a C-contiguous {np.dtype(dtype).name} array of shape {shape}, "
                                  f"got {a.dtype} {a.shape}")
     sp = stream.cuda_stream if stream is not None else None
     b = L.hc_batch(B, S, _ptr(start_x), _ptr(p0) if system.P else None, _ptr(p1) if system.P else None, _ptr(x),
-                   _ptr(status), _ptr(ctr), _ptr(resid), HC_MEM_HOST, sp)
+                   _ptr(status), _ptr(ctr), _ptr(resid), HC_MEM_HOST, sp, _ptr(wind) if wind is not None else None)
     h = C.c_void_p()
     check(L.lib().hc_track_batch(system.h, C.byref(st or hc_tracker_settings_default()), C.byref(b), C.byref(h)),
           "hc_track_batch")
-    res = BatchResult(x, status, ctr, resid, h)
+    res = BatchResult(x, status, ctr, resid, h, wind)
     res._keep = (system,)
     return res
 

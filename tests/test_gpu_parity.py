@@ -70,6 +70,37 @@ def assert_same_set_r21(orc, desc, p, A, B, what, tol=TOL):
             assert (cond > 1e8 or np.max(np.abs(a)) > 1e6) and dd <= 1e-5, (what, dd, cond)
 
 
+def assert_same_set_modulo_path_failures(orc, desc, p0, p1, ref_x, ref_st, gpu_x, gpu_st, what, max_frac=0.01):
+    """R21 for workloads whose paths can fail (vision systems at real data, R7): the CONVERGED sets
+    are compared as in R21 except that a solution found by one side only is accepted when every
+    track that reached it on that side failed (did not converge) on the other side from the same
+    start -- a path failure, not a wrong endpoint -- and it is a root by the oracle's residual
+    (R10).  Such one-sided solutions are bounded by max_frac of the tracks."""
+    A = orc.dedup(ref_x[ref_st == 0])[0]
+    B = orc.dedup(gpu_x[gpu_st == 0])[0]
+
+    def member(P, y):
+        return np.all(np.abs(P - y) <= TOL * np.maximum(1.0, np.abs(y)), axis=1)
+    hom = orc.ph_homotopy(desc, p0, p1)
+    extra = 0
+    for P, Q, X_own, st_own, st_other, side in ((A, B, ref_x, ref_st, gpu_st, "oracle"),
+                                                (B, A, gpu_x, gpu_st, ref_st, "gpu")):
+        for a in P:
+            if np.any(member(Q, a)):
+                continue
+            dd = np.min(np.max(np.abs(Q - a) / np.maximum(1, np.abs(a)), axis=1), initial=np.inf)
+            if dd <= 1e-5 and (np.max(np.abs(a)) > 1e6 or np.linalg.cond(orc.eval_JF(desc, p1, a), np.inf) > 1e8):
+                continue   # R21: ill-conditioned endpoints are only determined to ~cond * eps
+            tracks = np.nonzero((st_own == 0) & np.all(np.abs(X_own - a) <= 1e-6 * np.maximum(1.0, np.abs(a)), axis=1))[0]
+            assert len(tracks) > 0, (what, side)
+            assert np.all(st_other[tracks] != 0), (what, side, "both sides converged from the same start to different points")
+            r, rr = orc.endpoint_residual(hom, a)
+            assert r <= 1e-10 or rr <= 1e-12, (what, side, r, rr)
+            extra += len(tracks)
+    assert extra <= max_frac * len(ref_st), (what, extra)
+    return extra
+
+
 def assert_same_set(orc, A, B, what):
     ok, ua, ub = orc.match_sets(A, B, tol=TOL)
     assert ok, f"{what}: oracle {len(A)} vs gpu {len(B)} solutions, unmatched {ua}/{ub}"
@@ -333,6 +364,16 @@ def test_host_memory_path_matches_device_path(hc):
     h = hc.track_batch_host(s, X0, p0, p1[None])
     assert np.array_equal(a.x.cpu().numpy().view(np.float64), h.x.view(np.float64))
     assert np.array_equal(a.status.cpu().numpy(), h.status)
+    # the endgame's winding output through the host path as well
+    from hc_inputs.poly import var_x
+    X = var_x(1, 0, 0)
+    s3 = hc.System.total_degree_homotopy(systems.from_polys([(X - 2) ** 3], "(x-2)^3"), device=0)
+    q0, q1 = s3.td_params(rng.gamma(1))
+    Y0 = s3.td_start()
+    a3 = hc.track_batch(s3, _cuda(Y0), _cuda(q0), _cuda(q1)[None])
+    a3.wait()
+    h3 = hc.track_batch_host(s3, Y0, q0, q1[None])
+    assert np.all(h3.winding == 3) and np.array_equal(a3.winding.cpu().numpy(), h3.winding)
 
 
 def test_fourview_ph_parity(hc, orc):
@@ -423,6 +464,65 @@ def test_monodromy_cyclic7_family_924(hc, orc):
     assert_same_set_r21(orc, d, p0, fix, res.solutions, "cyclic-7 family monodromy")
 
 
+# ------------------------------------------------------------------ endgame (reading R26)
+
+@pytest.mark.parametrize("m", [2, 3, 4])
+def test_cauchy_endgame_gpu(hc, orc, m):
+    """(x - 2)^m by total degree: the tracker hands every track to the Cauchy endgame kernel, which
+    finds winding number m and the endpoint 2 to 1e-8 -- the oracle's closed-form pin, on the GPU."""
+    from hc_inputs.poly import var_x
+    X = var_x(1, 0, 0)
+    d = systems.from_polys([(X - 2) ** m], f"(x-2)^{m}")
+    res, _ = run_td(hc, d, rng.gamma(1))
+    st = res.status.cpu().numpy()[0]
+    assert np.all(st == 0), st
+    assert np.all(res.winding.cpu().numpy()[0] == m)
+    assert np.max(np.abs(res.x.cpu().numpy()[0][:, 0] - 2)) <= 1e-8
+    ref = orc.track(orc.td_homotopy(d, rng.gamma(1)), orc.td_start([m]))
+    assert np.array_equal(ref.winding[0], res.winding.cpu().numpy()[0])
+
+
+def test_cauchy_endgame_double_root_gpu(hc, orc):
+    """The oracle's 2x2 double-root pin (2, 1) with winding 2, on the GPU, both lane layouts' tables."""
+    from hc_inputs.poly import var_x
+    x, y = var_x(2, 0, 0), var_x(2, 0, 1)
+    d = systems.from_polys([(x - 2) ** 2 + y - 1, y - 1], "double-root")
+    res, _ = run_td(hc, d, rng.gamma(2))
+    assert np.all(res.status.cpu().numpy() == 0) and np.all(res.winding.cpu().numpy() == 2)
+    assert np.max(np.abs(res.x.cpu().numpy()[0] - np.array([2, 1]))) <= 1e-8
+
+
+def test_endgame_at_infinity_cyclic5_gpu(hc, orc):
+    """cyclic-5 (textbook: 70 finite of 120): the GPU set equals the oracle's and at least 30 of the
+    50 diverging paths end AT_INFINITY, each of them a path the oracle does not converge either."""
+    d = systems.cyclic(5)
+    gam = rng.gamma(1)
+    res, _ = run_td(hc, d, gam)
+    ref = orc.track(orc.td_homotopy(d, gam), orc.td_start(d.degrees()))
+    A = orc.dedup(orc.finite_solutions(ref))[0]
+    B = gpu_set(orc, res)
+    assert len(A) == 70
+    assert_same_set(orc, A, B, "cyclic-5 with endgame")
+    st = res.status.cpu().numpy()[0]
+    inf = st == hc.HC_AT_INFINITY
+    assert 30 <= inf.sum() <= 50
+    assert np.all(ref.status[0][inf] != orc.CONVERGED)
+    assert abs(int(inf.sum()) - int((ref.status[0] == orc.AT_INFINITY).sum())) <= 5
+
+
+def test_endgame_off_matches_plain_tracking(hc, orc):
+    """eg_start = 0 disables the endgame on both sides: no AT_INFINITY, no winding, same sets."""
+    d = systems.cyclic(5)
+    gam = rng.gamma(1)
+    res, _ = run_td(hc, d, gam, st=hc.settings(eg_start=0.0))
+    st = res.status.cpu().numpy()[0]
+    assert not np.any(st == hc.HC_AT_INFINITY) and np.all(res.winding.cpu().numpy() == 0)
+    ost = orc.default_settings()
+    ost.eg_start = 0
+    ref = orc.track(orc.td_homotopy(d, gam), orc.td_start(d.degrees()), settings=ost)
+    assert_same_set(orc, orc.dedup(orc.finite_solutions(ref))[0], gpu_set(orc, res), "cyclic-5 plain")
+
+
 # ------------------------------------------------------------------ edge cases
 
 def _linear_plus_quadratic(n, nq, seed):
@@ -490,6 +590,10 @@ def test_invalid_batches_rejected(hc):
     assert e.value.code == HC_E_INVALID_ARG
     with pytest.raises(hc.HCError):
         s.td_params(0.0)
+    for bad in (dict(eg_start=1.5), dict(eg_samples=1), dict(eg_inf_mu=0.1), dict(eg_tol=0.0)):
+        with pytest.raises(hc.HCError) as e:
+            hc.track_batch(s, _cuda(X0), _cuda(p0), _cuda(p1)[None], st=hc.settings(**bad))
+        assert e.value.code == HC_E_INVALID_ARG, bad
 
 
 def test_euler_predictor_setting(hc, orc):
@@ -547,24 +651,28 @@ def _planted_found(d, X, xg):
 
 
 def test_trifocal_config4_set_parity(hc, orc, trifocal_config4):
-    """R21 set parity at the paper's trifocal workload (Table 2) in the bench launch: for
-    instances 0 and 777 of the 1024-instance batch the oracle tracks all 5328 starts, and the GPU's
-    CONVERGED distinct set equals the oracle's (equal counts, nearest neighbour within 1e-8
-    relative per coordinate)."""
+    """Set parity at the paper's trifocal workload (Table 2) in the bench launch: for
+    instances 0 and 777 of the 1024-instance batch the oracle tracks all 5328 starts; the GPU's
+    CONVERGED distinct set equals the oracle's within 1e-8 relative per coordinate, except for
+    solutions one side reached on tracks where the other side's path failed (~4 % of trifocal
+    tracks end in STEP_UNDERFLOW on both sides; which near-singular paths fail is rounding
+    dependent), each verified a root by the oracle's residual and bounded by 1 % of the tracks."""
     d, start, p0, p1s, xg, st, X = trifocal_config4
     for b in (0, 777):
         ref = orc.track(orc.ph_homotopy(d, p0), start, p1s=p1s[b:b + 1])
-        A = orc.dedup(ref.x[0][ref.status[0] == 0])[0]
-        B = orc.dedup(X[b][st[b] == 0])[0]
-        assert len(A) > 0.9 * start.shape[0] / 2
-        assert_same_set_r21(orc, d, p1s[b], A, B, f"trifocal instance {b}")
+        assert (ref.status[0] == 0).sum() > 0.9 * start.shape[0]
+        extra = assert_same_set_modulo_path_failures(orc, d, p0, p1s[b], ref.x[0], ref.status[0], X[b], st[b],
+                                                     f"trifocal instance {b}")
+        print(f"trifocal instance {b}: oracle {(ref.status[0] == 0).sum()} converged, gpu {(st[b] == 0).sum()}, "
+              f"one-sided (path failures of the other side) {extra}")
 
 
 def test_trifocal_config4_full_batch_sampled(hc, orc, trifocal_config4):
     """Config 4 at full size: the planted ground truth (up to the Z2^3 images) is recovered in every
     sampled instance where the oracle recovers it -- each GPU miss is re-run through the oracle on
     all 5328 starts, which must miss it too and give the same solution set (a path failure of the
-    method, R7, not of the kernel); sampled tracks from spread-out instances agree one by one."""
+    method, R7, not of the kernel) and the sets agree modulo path failures; sampled tracks from
+    spread-out instances agree one by one."""
     d, start, p0, p1s, xg, st, X = trifocal_config4
     assert (st == 0).mean() > 0.9
     missed = [b for b in range(0, 1024, 16) if not _planted_found(d, X[b][st[b] == 0], xg[b])]
@@ -573,8 +681,8 @@ def test_trifocal_config4_full_batch_sampled(hc, orc, trifocal_config4):
         ref = orc.track(orc.ph_homotopy(d, p0), start, p1s=p1s[b:b + 1])
         G = ref.x[0][ref.status[0] == 0]
         assert not _planted_found(d, G, xg[b]), f"instance {b}: the oracle finds the planted root, the GPU not"
-        assert_same_set_r21(orc, d, p1s[b], orc.dedup(G)[0], orc.dedup(X[b][st[b] == 0])[0],
-                            f"trifocal instance {b}")
+        assert_same_set_modulo_path_failures(orc, d, p0, p1s[b], ref.x[0], ref.status[0], X[b], st[b],
+                                             f"trifocal instance {b}")
     g = rng.gen(77)
     agree = tot = 0
     for b in (0, 300, 777, 1023):
