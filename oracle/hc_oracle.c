@@ -628,6 +628,38 @@ static int cauchy_endgame(tracker *T, cplx *x, double s, eg_ctr *c, int *m) {
   return fail;
 }
 
+/* Ordinary tracking (R5-R9, no endgame sampling) from (x, *t) with step *dt to t = 1; returns -1 when
+ * t = 1 was reached (the caller polishes and classifies), else the terminal status. */
+static int resume_plain(tracker *T, cplx *x, double *tp, double *dtp, int32_t *steps, int32_t *rej, int32_t *newt) {
+  const orc_settings *st = T->st;
+  int n = T->n, sing, stat = -1, acc = 0;
+  double t = *tp, dt = *dtp;
+  cplx *xp = malloc(sizeof(cplx) * n);
+  while (t < 1.0) {
+    if (*steps >= st->max_steps) { stat = ORC_MAX_STEPS; break; }
+    (*steps)++;
+    double h = dt, t1 = t + dt;
+    if (t1 >= 1.0) { t1 = 1.0; h = 1.0 - t; }
+    int ok = predict(T, x, t, h, xp) == 0;
+    if (ok) ok = newton(T, xp, t1, st->max_newton, st->newton_tol, newt, &sing);
+    if (ok) {
+      memcpy(x, xp, sizeof(cplx) * n);
+      t = t1;
+      if (++acc >= st->grow_after) { dt = dt * st->grow; if (dt > st->dt_max) dt = st->dt_max; acc = 0; }
+      if (vec_norm_inf(n, x) > st->inf_norm) { stat = ORC_DIVERGED; break; }
+    } else {
+      (*rej)++;
+      acc = 0;
+      dt *= st->shrink;
+      if (dt < st->dt_min) { stat = ORC_STEP_UNDERFLOW; break; }
+    }
+  }
+  free(xp);
+  *tp = t;
+  *dtp = dt;
+  return stat;
+}
+
 static void track_one(tracker *T, const cplx *x0, cplx *x_out, int32_t *status, int32_t *ctr, double *resid,
                       int32_t *winding) {
   const orc_settings *st = T->st;
@@ -687,15 +719,32 @@ static void track_one(tracker *T, const cplx *x0, cplx *x_out, int32_t *status, 
     /* the step attempt that took the sample is abandoned after its first stage */
     eg_ctr c = {steps, rej, newt};
     int m = 0;
+    cplx *xh = malloc(sizeof(cplx) * n);
+    memcpy(xh, x, sizeof(cplx) * n);
     int fail = cauchy_endgame(T, x, 1.0 - t, &c, &m);
     steps = c.steps; rej = c.rej; newt = c.newt;
-    if (fail) stat = c.steps >= st->max_steps ? ORC_MAX_STEPS : ORC_STEP_UNDERFLOW;
-    else if (!all_finite(n, x)) stat = ORC_NONFINITE;
-    else {
-      wind = m;
+    if (!fail && all_finite(n, x)) {
       endpoint_residual(T, x, &r, &r_rel);
-      stat = (r <= st->res_abs || r_rel <= st->res_rel) ? ORC_CONVERGED : ORC_SINGULAR;
+      if (r <= st->res_abs || r_rel <= st->res_rel) { stat = ORC_CONVERGED; wind = m; }
+      else fail = 1;
+    } else {
+      fail = 1;
     }
+    if (fail) {
+      /* the loops enclosed other branch points (e.g. a near-double root: the estimate is the mean of
+       * several roots) or failed: resume ordinary tracking from the hand-over point, without
+       * endgame sampling (R26) */
+      memcpy(x, xh, sizeof(cplx) * n);
+      free(xh);
+      r = r_rel = INFINITY;
+      cauchy = 0;
+      stat = resume_plain(T, x, &t, &dt, &steps, &rej, &newt);
+    } else {
+      free(xh);
+    }
+  }
+  if (cauchy) {
+    /* done above */
   } else if (stat < 0) {
     /* endpoint polish on F(.; p1) = H(., 1) */
     int32_t pol = 0;

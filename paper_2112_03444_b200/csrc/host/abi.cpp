@@ -356,7 +356,8 @@ static void fill_info(const CompiledSystem &cs, hc_system_info *o) {
   o->mono_levels = cs.n_levels;
   o->flops_eval_kernel = cs.flops_eval_kernel;
   o->flops_solve_kernel = cs.flops_solve_kernel;
-  o->smem_per_track = (int64_t)slot_bytes(cs.N, cs.ncoef, cs.ncoef_src, cs.n_mono, cs.n_entries + 1);
+  o->smem_per_track =
+      (int64_t)slot_bytes(cs.N, cs.L * (hy_layout(cs.N) ? 2 : 1), cs.ncoef, cs.ncoef_src, cs.n_mono, cs.n_entries + 1);
 }
 
 hc_status hc_system_info_get(hc_system sys, hc_system_info *o) {

@@ -12,7 +12,10 @@
 //   at closure is the winding number m; the estimate of x(1) is the mean of the m K samples (the
 //   trapezoidal Cauchy integral).  Then move radially (ordinary real-t tracking) to s / 2 and
 //   repeat; two consecutive estimates within eg_tol * max(1, |x_i|) end it, and the endpoint is
-//   classified by its residuals at t = 1 (R10).
+//   classified by its residuals at t = 1 (R10).  When the loops fail or the estimate is not a root
+//   (the circle enclosed other branch points, e.g. of a near-double root: the mean of several roots)
+//   the track resumes ordinary tracking (R5-R9, no sampling) from the hand-over point to t = 1 and
+//   the R10 polish and classification -- exactly the oracle's order.
 // Same evaluation and fused LU as the tracker (eval_solve with a complex t); slots of a warp run
 // independent state machines, one eval + solve per slot per loop iteration, and pull work from
 // eg_list through a global counter.  Only tracks with singular endpoints ever reach this kernel, so
@@ -23,7 +26,11 @@
 
 namespace hcb {
 
-enum EgMode : int { EG_ARC = 0, EG_RADIAL = 1, EG_RESID = 2, EG_IDLE = 3 };
+enum EgMode : int { EG_ARC = 0, EG_RADIAL = 1, EG_PLAIN = 2, EG_POLISH = 3, EG_RESID = 4, EG_IDLE = 5 };
+
+#ifndef HCB_EG_DEBUG   // experiment builds: a failed Cauchy attempt records its reason in resid[1]
+#define HCB_EG_DEBUG 0
+#endif
 
 template <int N, int L>
 __device__ __forceinline__ void endgame_body(const TrackArgs &A) {
@@ -46,8 +53,8 @@ __device__ __forceinline__ void endgame_body(const TrackArgs &A) {
   const int seg = lane / L, r = lane % L;
   const int slot = warp * TPW + seg;
   const int ncoef = A.ncoef, D = A.D;
-  unsigned char *sb = slots_base + (size_t)slot * slot_bytes(N, ncoef, A.ncoef_src, A.n_mono, A.n_entries + 1);
-  double2 *cval = reinterpret_cast<double2 *>(sb + EG_SAMPLE_BYTES);
+  unsigned char *sb = slots_base + (size_t)slot * slot_bytes(N, L, ncoef, A.ncoef_src, A.n_mono, A.n_entries + 1);
+  double2 *cval = reinterpret_cast<double2 *>(sb + EG_SAMPLE_BYTES) + 3 * L;   // (the vector area is unused here)
   double2 *mono = cval + ncoef + A.ncoef_src;
   double2 *M = mono + A.n_mono;
   double2 *prow = M + A.n_entries + 1;
@@ -65,15 +72,16 @@ __device__ __forceinline__ void endgame_body(const TrackArgs &A) {
   const unsigned long long n_items = A.eg_count[0];
 
   // ---- slot state (replicated over the slot's lanes) ----
-  int mode = EG_IDLE, phase = 0, stage = 0, it = 0;
+  int mode = EG_IDLE, phase = 0, stage = 0, it = 0, acc = 0;
   long long g = -1;
   const double2 *ct = A.coef_t;
   int steps = 0, rej = 0, newt = 0, solves = 0;
   double s = 0.0, th = 0.0, th_end = 0.0, h = 0.0, hh = 0.0, tn = 0.0;   // circle
-  double tr = 0.0, t_end = 0.0, dtr = 0.0, hr = 0.0, t1 = 0.0;            // radial
+  double tr = 0.0, t_end = 0.0, dtr = 0.0, hr = 0.0, t1 = 0.0;            // radial / plain
+  double s_h = 0.0, dt_h = 0.0;                                           // hand-over point
   int arc = 0, loops = 0, radius = 0, m = 0;
-  bool have_est = false, need_track = true;
-  double2 x = make_double2(0.0, 0.0), xr = x, sum = x, est = x, kacc = x, kprev = x, xc = x;
+  bool have_est = false, need_track = true, cauchy_est = false;
+  double2 x = make_double2(0.0, 0.0), xr = x, sum = x, est = x, kacc = x, kprev = x, xc = x, xh = x;
   const bool valid = r < N;
   double2 cval_t = make_double2(-1.0, 0.0);   // t of the slot's cached coefficient values
 
@@ -89,8 +97,35 @@ __device__ __forceinline__ void endgame_body(const TrackArgs &A) {
     need_track = true;
     mode = EG_IDLE;
   };
-  auto fail = [&]() { done(steps >= st.max_steps ? HC_MAX_STEPS : HC_STEP_UNDERFLOW, INFINITY, INFINITY, 0); };
-  // the next step attempt on the circle (from th towards th_end) or on the radial segment
+  // real-t step attempt (radial move or plain tracking) from tr towards t_end with dtr
+  auto begin_real_step = [&]() -> bool {
+    if (steps >= st.max_steps) return false;
+    ++steps;
+    hr = dtr;
+    t1 = tr + dtr;
+    if (t1 >= t_end) {
+      t1 = t_end;
+      hr = t_end - tr;
+    }
+    phase = 0;
+    stage = 0;
+    kacc = kprev = make_double2(0.0, 0.0);
+    return true;
+  };
+  // the Cauchy endgame failed (or its estimate is not a root): resume plain tracking from the
+  // hand-over point to t = 1 (R5-R9), then polish and classify
+  int dbg = 0;
+  auto fallback = [&](int why) {
+    dbg = why;
+    x = xh;
+    tr = 1.0 - s_h;
+    t_end = 1.0;
+    dtr = dt_h;
+    acc = 0;
+    cauchy_est = false;
+    mode = EG_PLAIN;
+    if (!begin_real_step()) done(HC_MAX_STEPS, INFINITY, INFINITY, 0);
+  };
   auto begin_arc_step = [&]() -> bool {
     if (steps >= st.max_steps) return false;
     ++steps;
@@ -120,20 +155,6 @@ __device__ __forceinline__ void endgame_body(const TrackArgs &A) {
     arc = 0;
     return begin_arc();
   };
-  auto begin_radial_step = [&]() -> bool {
-    if (steps >= st.max_steps) return false;
-    ++steps;
-    hr = dtr;
-    t1 = tr + dtr;
-    if (t1 >= t_end) {
-      t1 = t_end;
-      hr = t_end - tr;
-    }
-    phase = 0;
-    stage = 0;
-    kacc = kprev = make_double2(0.0, 0.0);
-    return true;
-  };
 
   for (;;) {
     {
@@ -148,23 +169,27 @@ __device__ __forceinline__ void endgame_body(const TrackArgs &A) {
           ct = A.coef_t + (size_t)b * (D + 1) * ncoef;
           cval_t = make_double2(-1.0, 0.0);
           x = valid ? A.x_out[(size_t)g * N + r] : make_double2(0.0, 0.0);
+          xh = x;
           const int4 c0 = reinterpret_cast<const int4 *>(A.counters_out)[g];
           steps = c0.x;
           rej = c0.y;
           newt = c0.z;
           solves = c0.w;
-          s = reinterpret_cast<const double2 *>(A.resid_out)[g].x;   // the tracker's s = 1 - t
+          const double2 sd = reinterpret_cast<const double2 *>(A.resid_out)[g];   // (s = 1 - t, dt) at hand-over
+          s = s_h = sd.x;
+          dt_h = sd.y;
           radius = 0;
           have_est = false;
           m = 0;
-          if (!begin_radius()) fail();
+          dbg = 0;
+          if (!begin_radius()) fallback(5);
         } else {
           mode = EG_IDLE;
           g = -1;
         }
       }
     }
-    if (__all_sync(FULL, mode == EG_IDLE)) break;
+    if (__all_sync(FULL, mode == EG_IDLE && !need_track)) break;
 
     // ---- what this slot evaluates: te (complex), the point, and the rhs ----
     double2 te = make_double2(1.0, 0.0), xe = x, dtdth = make_double2(0.0, 0.0);
@@ -182,7 +207,7 @@ __device__ __forceinline__ void endgame_body(const TrackArgs &A) {
         te = make_double2(1.0 - s * e.x, -s * e.y);
         xe = xc;
       }
-    } else if (mode == EG_RADIAL) {
+    } else if (mode == EG_RADIAL || mode == EG_PLAIN) {
       if (phase == 0) {
         const double cs = (stage == 0) ? 0.0 : (stage == 3 ? 1.0 : 0.5);
         te = make_double2(tr + cs * hr, 0.0);
@@ -193,6 +218,9 @@ __device__ __forceinline__ void endgame_body(const TrackArgs &A) {
         te = make_double2(t1, 0.0);
         xe = xc;
       }
+    } else if (mode == EG_POLISH) {
+      te = make_double2(1.0, 0.0);
+      xe = xc;
     } else if (mode == EG_RESID) {
       te = make_double2(1.0, 0.0);
       xe = x;
@@ -208,17 +236,18 @@ __device__ __forceinline__ void endgame_body(const TrackArgs &A) {
 
     // ---- slot-uniform reductions (all lanes, before any slot-divergent branch) ----
     const double2 cand = make_double2(xc.x - y.x, xc.y - y.y);   // Newton update
-    const bool cand_fin = seg_all<L>(cfinite(cand), seg);
-    const double d2 = seg_max<L>(abs2(y));
-    const double c2 = seg_max<L>(abs2(cand));
+    const bool cand_fin = seg_all<L>(!valid || cfinite(cand), seg);
+    const double d2 = seg_max<L>(valid ? abs2(y) : 0.0);
+    const double c2 = seg_max<L>(valid ? abs2(cand) : 0.0);
     // loop closure: the accepted point vs the loop's start point
-    const double dcl = seg_max<L>(abs2(make_double2(cand.x - xr.x, cand.y - xr.y)));
-    const double xr2 = seg_max<L>(abs2(xr));
+    const double dcl = seg_max<L>(valid ? abs2(make_double2(cand.x - xr.x, cand.y - xr.y)) : 0.0);
+    const double xr2 = seg_max<L>(valid ? abs2(xr) : 0.0);
     // the estimate if this accept closes a loop, and its agreement with the previous radius
     const double2 enew = make_double2(sum.x / ((loops + 1) * K), sum.y / ((loops + 1) * K));
     const double em = sqrt(abs2(enew));
-    const bool agree = seg_all<L>(!valid || sqrt(abs2(make_double2(enew.x - est.x, enew.y - est.y))) <= st.eg_tol * fmax(1.0, em), seg);
-    const bool x_fin = seg_all<L>(cfinite(x), seg);
+    const bool agree =
+        seg_all<L>(!valid || sqrt(abs2(make_double2(enew.x - est.x, enew.y - est.y))) <= st.eg_tol * fmax(1.0, em), seg);
+    const bool x_fin = seg_all<L>(!valid || cfinite(x), seg);
     double res_abs = 0.0, res_rel = 0.0;
     if (want_abs) {
       const double mg = valid ? sqrt(abs2(fr[0])) : 0.0;
@@ -229,11 +258,28 @@ __device__ __forceinline__ void endgame_body(const TrackArgs &A) {
     // ---- advance the slot's state machine ----
     if (mode == EG_IDLE) continue;
     if (mode == EG_RESID) {
-      if (!x_fin) done(HC_NONFINITE, INFINITY, INFINITY, 0);
-      else done((res_abs <= st.res_abs || res_rel <= st.res_rel) ? HC_CONVERGED : HC_SINGULAR, res_abs, res_rel, m);
+      const bool conv = res_abs <= st.res_abs || res_rel <= st.res_rel;
+      if (cauchy_est) {   // the Cauchy estimate: a root, or back to plain tracking
+        if (x_fin && conv) done(HC_CONVERGED, res_abs, res_rel, m);
+        else fallback(6);
+      } else if (!x_fin) {
+        done(HC_NONFINITE, INFINITY, INFINITY, 0);
+      } else {
+        done(conv ? HC_CONVERGED : HC_SINGULAR, res_abs, HCB_EG_DEBUG ? (double)dbg : res_rel, 0);
+      }
       continue;
     }
     ++solves;
+    if (mode == EG_POLISH) {   // R10 polish at t = 1 (as the tracker's ST_POLISH)
+      if (!ok) {
+        mode = EG_RESID;
+      } else {
+        x = xc = cand;
+        if (!cand_fin) done(HC_NONFINITE, INFINITY, INFINITY, 0);
+        else if (d2 <= st.end_tol * st.end_tol * fmax(1.0, c2) || ++it >= st.end_newton) mode = EG_RESID;
+      }
+      continue;
+    }
     bool accept = false, reject = false;
     const double hstep = (mode == EG_ARC) ? hh : hr;
     if (phase == 0) {   // RK stage: k = (dx/dt) (dt/dtau) = -y dt/dtau
@@ -268,9 +314,9 @@ __device__ __forceinline__ void endgame_body(const TrackArgs &A) {
       if (mode == EG_ARC) {
         th = tn;
         if (th < th_end) {
-          if (!begin_arc_step()) fail();
+          if (!begin_arc_step()) fallback(1);
         } else if (++arc < K) {
-          if (!begin_arc()) fail();
+          if (!begin_arc()) fallback(1);
         } else {   // a loop is complete
           ++loops;
           arc = 0;
@@ -278,7 +324,8 @@ __device__ __forceinline__ void endgame_body(const TrackArgs &A) {
             x = xr;
             m = loops;
             if (have_est && agree) {
-              x = enew;   // the endpoint estimate
+              x = enew;   // the endpoint estimate: classified at t = 1
+              cauchy_est = true;
               mode = EG_RESID;
             } else {
               est = enew;
@@ -288,35 +335,56 @@ __device__ __forceinline__ void endgame_body(const TrackArgs &A) {
                 t_end = 1.0 - 0.5 * s;
                 dtr = t_end - tr;
                 mode = EG_RADIAL;
-                if (!begin_radial_step()) fail();
+                if (!begin_real_step()) fallback(1);
               } else {
-                fail();
+                fallback(3);
               }
             }
           } else if (loops < st.eg_max_winding) {
-            if (!begin_arc()) fail();
+            if (!begin_arc()) fallback(1);
           } else {
-            fail();
+            fallback(2);
           }
         }
-      } else {   // radial
+      } else {   // radial move or plain tracking
         tr = t1;
-        if (tr < t_end) {
-          if (!begin_radial_step()) fail();
+        if (mode == EG_PLAIN) {
+          if (++acc >= st.grow_after) {
+            dtr = fmin(dtr * st.grow, st.dt_max);
+            acc = 0;
+          }
+          if (c2 > st.inf_norm * st.inf_norm) {
+            done(HC_DIVERGED, INFINITY, INFINITY, 0);
+          } else if (tr >= 1.0) {
+            xc = x;
+            it = 0;
+            mode = EG_POLISH;
+          } else if (!begin_real_step()) {
+            done(HC_MAX_STEPS, INFINITY, INFINITY, 0);
+          }
+        } else if (tr < t_end) {
+          if (!begin_real_step()) fallback(1);
         } else {
           s *= 0.5;
           ++radius;
-          if (!begin_radius()) fail();
+          if (!begin_radius()) fallback(1);
         }
       }
     } else if (reject) {
       ++rej;
       if (mode == EG_ARC) {
         h *= st.shrink;
-        if (h < st.dt_min || !begin_arc_step()) fail();
+        if (h < st.dt_min) fallback(4);
+        else if (!begin_arc_step()) fallback(1);
+      } else if (mode == EG_PLAIN) {
+        acc = 0;
+        dtr *= st.shrink;
+        if (dtr < st.dt_min) done(HC_STEP_UNDERFLOW, INFINITY, INFINITY, 0);
+        else if (!begin_real_step()) done(HC_MAX_STEPS, INFINITY, INFINITY, 0);
       } else {
         dtr *= st.shrink;
-        if (dtr < st.dt_min || !begin_radial_step()) fail();
+        if (dtr < st.dt_min) fallback(7);
+        else if (!begin_real_step()) fallback(1);
       }
     }
   }
@@ -334,7 +402,7 @@ cudaError_t launch_endgame_n(const TrackArgs &A, int device, cudaStream_t stream
   constexpr int L = lanes_for(N);
   constexpr int TPW = 32 / L;
   const size_t tables = table_bytes(A.Q, L, A.n_mono - (N + 1), N) + align16((size_t)2 * A.n_entries);
-  const size_t per_warp = (size_t)TPW * slot_bytes(N, A.ncoef, A.ncoef_src, A.n_mono, A.n_entries + 1);
+  const size_t per_warp = (size_t)TPW * slot_bytes(N, L, A.ncoef, A.ncoef_src, A.n_mono, A.n_entries + 1);
   int smem_max = 0;
   cudaDeviceGetAttribute(&smem_max, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
   int warps = 4;

@@ -153,7 +153,7 @@ __device__ __forceinline__ bool seg_all(bool p, int seg) {
   return (b & m) == m;
 }
 
-enum SlotState : int { ST_RK = 0, ST_NEWTON = 1, ST_POLISH = 2, ST_RESID = 3, ST_DONE = 4 };
+enum SlotState : int { ST_RK = 0, ST_NEWTON = 1, ST_POLISH = 2, ST_RESID = 3, ST_DONE = 4, ST_EGFIN = 5 };
 
 // ------------------------------------------------------------------------------------------
 // Arg-max of v over the L lanes of a segment; ties -> lowest lane.  v < 0 marks a non-candidate.
@@ -167,9 +167,22 @@ enum SlotState : int { ST_RK = 0, ST_NEWTON = 1, ST_POLISH = 2, ST_RESID = 3, ST
 // thr's take the exact two-REDUX path of seg_argmax.
 template <int L>
 __device__ __forceinline__ int seg_argmax(double v, int r, double &vmax);
+#ifndef HCB_PACKED_ARGMAX   // 32-lane arg-max by one REDUX on a packed (|a|^2 bits, lane) key (A/B switch)
+#define HCB_PACKED_ARGMAX 0
+#endif
 template <int L>
 __device__ __forceinline__ int seg_argmax_thr(double v, int r, double thr, bool &sing) {
-  if constexpr (L == 32) {
+  if constexpr (L == 32 && HCB_PACKED_ARGMAX) {
+    // key = the top 27 bits of |a|^2's IEEE pattern (exponent + 16 mantissa bits; sign is 0) above
+    // 31 - lane: one REDUX gives the pivot and ties (to 2^-16 relative) go to the lowest row;
+    // non-candidates (used rows, padding, NaN) have key 0
+    const unsigned hi = (unsigned)((unsigned long long)__double_as_longlong(v) >> 36);
+    const unsigned key = (v >= 0.0) ? ((hi << 5) | (31u - (unsigned)r)) : 0u;
+    const unsigned mk = __reduce_max_sync(FULL, key);
+    const unsigned thr_hi = (unsigned)((unsigned long long)__double_as_longlong(thr) >> 36);
+    sing |= (mk == 0u) || ((mk >> 5) <= thr_hi);
+    return 31 - (int)(mk & 31u);
+  } else if constexpr (L == 32) {
     const unsigned long long bits = (unsigned long long)__double_as_longlong(v);
     const unsigned hi = (v >= 0.0) ? (unsigned)(bits >> 32) + 1u : 0u;
     const unsigned mhi = __reduce_max_sync(FULL, hi);
@@ -765,9 +778,10 @@ __device__ __forceinline__ void track_body(const TrackArgs &A) {
   const int seg = lane / L, r = lane % L;
   const int slot = warp * TPW + seg;
   const int ncoef = A.ncoef, D = A.D;
-  unsigned char *sb = slots_base + (size_t)slot * slot_bytes(N, ncoef, A.ncoef_src, A.n_mono, A.n_entries + 1);
+  unsigned char *sb = slots_base + (size_t)slot * slot_bytes(N, L * NC, ncoef, A.ncoef_src, A.n_mono, A.n_entries + 1);
   EgSample *egs = reinterpret_cast<EgSample *>(sb);   // endgame sampling state (R26), lane 0 writes
-  double2 *cval = reinterpret_cast<double2 *>(sb + EG_SAMPLE_BYTES);
+  double2 *vstate = reinterpret_cast<double2 *>(sb + EG_SAMPLE_BYTES);   // [3][NC][L]
+  double2 *cval = vstate + 3 * NC * L;
   double2 *mono = cval + ncoef + A.ncoef_src;
   double2 *M = mono + A.n_mono;
   double2 *prow = M + A.n_entries + 1;
@@ -788,9 +802,15 @@ __device__ __forceinline__ void track_body(const TrackArgs &A) {
   double t = 0.0, dt = 0.0, h = 0.0, t1 = 0.0;
   int stage = 0, it = 0, acc = 0, steps = 0, rej = 0, newt = 0, solves = 0;
   // component c of lane r is unknown r (c = 0) or 16 + r (c = 1, hybrid layout, r < E)
-  double2 x[NC], kacc[NC], kprev[NC], xc[NC];
+  // x stays in registers; the RK accumulators and the corrector's point live in the slot's shared
+  // memory ([kacc | kprev | xc][NC][L], one conflict-free 16-byte word per lane): they are touched a
+  // few times per iteration, and the registers they free keep the N <= 16 kernels within 128
+  double2 x[NC];
+  auto KACC = [&](int c) -> double2 & { return vstate[(0 * NC + c) * L + r]; };
+  auto KPREV = [&](int c) -> double2 & { return vstate[(1 * NC + c) * L + r]; };
+  auto XC = [&](int c) -> double2 & { return vstate[(2 * NC + c) * L + r]; };
 #pragma unroll
-  for (int c = 0; c < NC; ++c) x[c] = kacc[c] = kprev[c] = xc[c] = make_double2(0.0, 0.0);
+  for (int c = 0; c < NC; ++c) x[c] = KACC(c) = KPREV(c) = XC(c) = make_double2(0.0, 0.0);
   auto comp_valid = [&](int c) -> bool { return c == 0 ? (r < N) : (r < E); };
   auto comp_row = [&](int c) -> int { return c == 0 ? r : 16 + r; };
   bool need_track = true;
@@ -814,7 +834,7 @@ __device__ __forceinline__ void track_body(const TrackArgs &A) {
     }
     stage = 0;
 #pragma unroll
-    for (int c = 0; c < NC; ++c) kacc[c] = kprev[c] = make_double2(0.0, 0.0);
+    for (int c = 0; c < NC; ++c) KACC(c) = KPREV(c) = make_double2(0.0, 0.0);
     state = ST_RK;
     return true;
   };
@@ -829,7 +849,7 @@ __device__ __forceinline__ void track_body(const TrackArgs &A) {
       reinterpret_cast<double2 *>(A.resid_out)[g] = make_double2(ra, rr);
       if (A.winding_out) A.winding_out[g] = 0;
       // a singular endpoint (reading R26): the Cauchy endgame kernel continues this track from
-      // (x, t = 1 - ra); the list entry is the track id
+      // (x, t = 1 - ra) with step rr; the list entry is the track id
       if (status == HC_EG_PENDING) A.eg_list[atomicAdd(A.eg_count, 1ULL)] = g;
     }
     need_track = true;
@@ -880,7 +900,7 @@ __device__ __forceinline__ void track_body(const TrackArgs &A) {
       bool eg_inf = false, eg_cauchy = false;
       const bool want = fresh_k1 && (1.0 - t) <= egs->s_next;
       fresh_k1 = false;
-      if (__any_sync(FULL, want)) {
+      if (__builtin_expect(__any_sync(FULL, want), 0)) {
         __syncwarp();   // lane 0's xn2 / kn2 stores of the previous iterations are visible
         EgSample e = *egs;
         if (want) {
@@ -907,11 +927,16 @@ __device__ __forceinline__ void track_body(const TrackArgs &A) {
         __syncwarp();
         if (want && r == 0) *egs = e;
       }
-      if (eg_inf) finish(HC_AT_INFINITY, INFINITY, INFINITY);
-      else if (eg_cauchy) finish(HC_EG_PENDING, 1.0 - t, 0.0);   // x and s = 1 - t for the endgame kernel
+      // the decision is carried out by the state machine below (one finish() call site): this
+      // iteration's evaluation is a dummy for the slot and counts no solve
+      if (eg_inf || eg_cauchy) {
+        state = ST_EGFIN;
+        stage = eg_inf ? 1 : 2;
+      }
     }
 
-    if (__all_sync(FULL, state == ST_DONE)) break;
+    // (a slot the sampling just finished refills at the next iteration: need_track)
+    if (__all_sync(FULL, state == ST_DONE && !need_track)) break;
 #ifdef HCB_PHASE_TIMING
     hcb_iter0 = clock64();
     hcb_phase[7] += 1;   // iterations
@@ -926,12 +951,12 @@ __device__ __forceinline__ void track_body(const TrackArgs &A) {
       te = t + cs * h;
 #pragma unroll
       for (int c = 0; c < NC; ++c)
-        xe[c] = make_double2(fma(cs * h, kprev[c].x, x[c].x), fma(cs * h, kprev[c].y, x[c].y));
+        xe[c] = make_double2(fma(cs * h, KPREV(c).x, x[c].x), fma(cs * h, KPREV(c).y, x[c].y));
       rhs_off = ncoef;  // rhs = dH/dt
     } else if (state == ST_NEWTON) {
       te = t1;
 #pragma unroll
-      for (int c = 0; c < NC; ++c) xe[c] = xc[c];
+      for (int c = 0; c < NC; ++c) xe[c] = XC(c);
     } else if (state == ST_POLISH || state == ST_RESID) {
       te = 1.0;
 #pragma unroll
@@ -965,7 +990,7 @@ __device__ __forceinline__ void track_body(const TrackArgs &A) {
     double yd2 = 0.0, cd2 = 0.0;
 #pragma unroll
     for (int c = 0; c < NC; ++c) {
-      const double2 base = (state == ST_POLISH) ? x[c] : xc[c];
+      const double2 base = (state == ST_POLISH) ? x[c] : XC(c);
       cand[c] = make_double2(base.x - yv[c].x, base.y - yv[c].y);   // Newton update x - dx
       fin = fin && cfinite(cand[c]);
       yd2 = nmax(yd2, abs2(yv[c]));
@@ -990,9 +1015,12 @@ __device__ __forceinline__ void track_body(const TrackArgs &A) {
 
     // ---- advance the slot's state machine ----
     if (state == ST_DONE) continue;
-    if (state != ST_RESID) ++solves;
+    if (state != ST_RESID && state != ST_EGFIN) ++solves;
     bool accept = false, reject = false;
-    if (state == ST_RK) {
+    if (state == ST_EGFIN) {   // endgame decision (R26): at infinity, or x, s = 1 - t, dt for the Cauchy kernel
+      const bool inf = stage == 1;
+      finish(inf ? HC_AT_INFINITY : HC_EG_PENDING, inf ? INFINITY : 1.0 - t, inf ? INFINITY : dt);
+    } else if (state == ST_RK) {
       if (!ok) {
         reject = true;
       } else {
@@ -1002,8 +1030,8 @@ __device__ __forceinline__ void track_body(const TrackArgs &A) {
 #pragma unroll
         for (int c = 0; c < NC; ++c) {
           const double2 k = make_double2(-yv[c].x, -yv[c].y);
-          kacc[c] = make_double2(fma(w, k.x, kacc[c].x), fma(w, k.y, kacc[c].y));
-          kprev[c] = k;
+          KACC(c) = make_double2(fma(w, k.x, KACC(c).x), fma(w, k.y, KACC(c).y));
+          KPREV(c) = k;
         }
         if (stage + 1 < n_rk) {
           ++stage;
@@ -1011,10 +1039,10 @@ __device__ __forceinline__ void track_body(const TrackArgs &A) {
 #pragma unroll
           for (int c = 0; c < NC; ++c) {
             if (n_rk == 1) {
-              xc[c] = make_double2(fma(h, kprev[c].x, x[c].x), fma(h, kprev[c].y, x[c].y));
+              XC(c) = make_double2(fma(h, KPREV(c).x, x[c].x), fma(h, KPREV(c).y, x[c].y));
             } else {
               const double h6 = h / 6.0;
-              xc[c] = make_double2(fma(h6, kacc[c].x, x[c].x), fma(h6, kacc[c].y, x[c].y));
+              XC(c) = make_double2(fma(h6, KACC(c).x, x[c].x), fma(h6, KACC(c).y, x[c].y));
             }
           }
           state = ST_NEWTON;
@@ -1027,7 +1055,7 @@ __device__ __forceinline__ void track_body(const TrackArgs &A) {
         reject = true;
       } else {
 #pragma unroll
-        for (int c = 0; c < NC; ++c) xc[c] = cand[c];
+        for (int c = 0; c < NC; ++c) XC(c) = cand[c];
         if (d2 <= st.newton_tol * st.newton_tol * fmax(1.0, c2)) accept = true;
         else if (++it >= st.max_newton) reject = true;
       }
@@ -1049,7 +1077,7 @@ __device__ __forceinline__ void track_body(const TrackArgs &A) {
     }
     if (accept) {
 #pragma unroll
-      for (int c = 0; c < NC; ++c) x[c] = xc[c];
+      for (int c = 0; c < NC; ++c) x[c] = XC(c);
       if (r == 0) egs->xn2 = c2;   // ||x||^2 of the accepted point (endgame samples)
       t = t1;
       if (++acc >= st.grow_after) {
@@ -1098,7 +1126,8 @@ cudaError_t launch_tracker_n(const TrackArgs &A, int device, cudaStream_t stream
   constexpr int L = TrackerShape<N, LW>::L;
   constexpr int TPW = 32 / L;
   const size_t tables = table_bytes(A.Q, L, A.n_mono - (N + 1), N) + align16((size_t)2 * A.n_entries);
-  const size_t per_warp = (size_t)TPW * slot_bytes(N, A.ncoef, A.ncoef_src, A.n_mono, A.n_entries + 1);
+  const size_t per_warp =
+      (size_t)TPW * slot_bytes(N, L * TrackerShape<N, LW>::NC, A.ncoef, A.ncoef_src, A.n_mono, A.n_entries + 1);
   int smem_max = 0;
   cudaDeviceGetAttribute(&smem_max, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
   int warps = TrackerShape<N, LW>::MAXW;
