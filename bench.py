@@ -38,13 +38,25 @@ FP64_DFMA_PER_CLK_PER_SM = 64   # B200 FP64 vector: 64 DFMA/clk/SM (DESIGN.md "r
 
 # ------------------------------------------------------------------------------ workloads
 
-def make_workload(name: str, B: int, rank: int):
-    """Seeded synthetic inputs (hc_inputs) for this rank: (desc, start_x, p0, p1s, settings overrides, meta)."""
+def instance_range(args, rank: int, world: int) -> tuple[int, int]:
+    """Global instance block [lo, hi) of this rank (paper_2112_03444_b200.distributed.shard_range):
+    weak scaling gives every rank --instances instances (the job grows with the GPU count), strong
+    scaling splits --total-instances (configs[4]: 8192) into balanced contiguous blocks."""
+    from paper_2112_03444_b200.distributed import shard_range
+    if args.total_instances:
+        return shard_range(args.total_instances, rank, world)
+    return shard_range(args.instances * world, rank, world)
+
+
+def make_workload(name: str, lo: int, hi: int):
+    """Seeded synthetic inputs (hc_inputs) for the global instances [lo, hi): (desc, start_x, p0, p1s,
+    settings overrides, meta); instance b is generated from seed base + b whichever rank owns it."""
     from hc_inputs import fixtures, rng, systems
+    B = hi - lo
     if name == "trifocal":
         d = systems.trifocal_unknown_f()
         start, p0 = fixtures.trifocal_start()
-        p1s = np.stack([rng.trifocal_instance(rng.SEED_TRIFOCAL_INSTANCE + rank * B + b)[0] for b in range(B)])
+        p1s = np.stack([rng.trifocal_instance(rng.SEED_TRIFOCAL_INSTANCE + b)[0] for b in range(lo, hi)])
         meta = {"workload": f"trifocal rel. pose unknown f (18x18, Table 2 P:488) PH, S={start.shape[0]} starts "
                             f"(oracle monodromy fixture) x {B} planted instances per GPU (configs[3]; "
                             f"configs[4] = 8192 instances at 8 GPUs)"}
@@ -53,7 +65,7 @@ def make_workload(name: str, B: int, rank: int):
         d = systems.nview_triangulation(4)
         start = fixtures.read_solutions(fixtures.fixture_path("fourview_start.sols"))
         p0 = fixtures.read_params(fixtures.fixture_path("fourview_p0.params"))
-        p1s = np.stack([rng.fourview_instance(rng.SEED_FOURVIEW_INSTANCE + rank * B + b)[0] for b in range(B)])
+        p1s = np.stack([rng.fourview_instance(rng.SEED_FOURVIEW_INSTANCE + b)[0] for b in range(lo, hi)])
         meta = {"workload": f"4-view triangulation (14x14, Table 2 P:490) PH, S=296 x {B} planted instances "
                             f"per GPU (configs[2])"}
         return d, start, p0, p1s, {}, meta
@@ -61,7 +73,7 @@ def make_workload(name: str, B: int, rank: int):
         d = systems.fivepoint_relpose_depth()
         start = fixtures.read_solutions(fixtures.fixture_path("fivepoint_start.sols"))
         p0 = fixtures.read_params(fixtures.fixture_path("fivepoint_p0.params"))
-        p1s = np.stack([rng.fivepoint_instance(rng.SEED_FIVEPOINT_INSTANCE + rank * B + b)[0] for b in range(B)])
+        p1s = np.stack([rng.fivepoint_instance(rng.SEED_FIVEPOINT_INSTANCE + b)[0] for b in range(lo, hi)])
         meta = {"workload": f"5-point rel. pose + depth (16x16, Table 2 P:492; reading R24) PH, S=40 x {B} "
                             f"planted instances per GPU (SURVEY N2)"}
         return d, start, p0, p1s, {}, meta
@@ -69,7 +81,7 @@ def make_workload(name: str, B: int, rank: int):
         d = systems.p3p_depth()
         start = fixtures.read_solutions(fixtures.fixture_path("p3p_start.sols"))
         p0 = fixtures.read_params(fixtures.fixture_path("p3p_p0.params"))
-        p1s = np.stack([rng.p3p_instance(rng.SEED_P3P_INSTANCE + rank * B + b)[0] for b in range(B)])
+        p1s = np.stack([rng.p3p_instance(rng.SEED_P3P_INSTANCE + b)[0] for b in range(lo, hi)])
         meta = {"workload": f"P3P absolute pose, depth form (3x3, Eq. P3PafterElim P:260-273, Table 2 P:512) PH, "
                             f"S={start.shape[0]} x {B} planted instances per GPU (SURVEY N2)"}
         return d, start, p0, p1s, {}, meta
@@ -136,45 +148,65 @@ class ClockSampler:
 
 # ------------------------------------------------------------------------------ oracle (cpu)
 
-def oracle_sample(name: str, budget_s: float, rank: int = 0, B: int = 1, nthreads: int | None = None):
-    """Time the CPU oracle (as it stands) on a bounded sample of the workload, sized to ~budget_s:
-    the first tracks of instance 0, or -- when one instance takes less than that (4-view, 5-point)
-    -- all tracks of the first instances of the batch.  Returns (tracks/s, cores, sample description)."""
+def oracle_sample(name: str, budget_s: float, nthreads: int | None = None):
+    """Time the CPU oracle (as it stands) on a bounded, unbiased sample of the workload, sized to
+    ~budget_s.  Parameter homotopies: the same number of start solutions, drawn without replacement
+    by a seeded permutation, from each of up to 64 instances spread evenly over the 1024-instance
+    batch (the trifocal start set is ordered by symmetry orbit and instances differ in difficulty,
+    so neither a prefix of one instance nor the first instances is representative); single-instance
+    workloads: the whole solve, repeated to fill the budget.  Returns (tracks/s, cores, description)."""
     import oracle
-    max_inst = 256
-    d, start, p0, p1s, _, _ = make_workload(name, 1 if name in ("trifocal", "cyclic7ph") else max_inst, rank)
     nthreads = nthreads or oracle.nthreads_default()
-    if start is None:   # TD single instance
+    if name in ("cyclic7", "katsura6", "eco12"):
+        d, _, _, _, _, _ = make_workload(name, 0, 1)
         from hc_inputs import rng
         hom = oracle.td_homotopy(d, rng.gamma(2))
         start = oracle.td_start(d.degrees())
-        run = lambda X, k=1: oracle.track(hom, X, nthreads=nthreads)   # noqa: E731
-    else:
-        hom = oracle.ph_homotopy(d, p0)
-        run = lambda X, k=1: oracle.track(hom, X, p1s=p1s[:k], nthreads=nthreads)   # noqa: E731
-    S = start.shape[0]
-    n = min(S, max(nthreads * 2, 16))
-    t = time.perf_counter()
-    run(start[:n])
-    dt = time.perf_counter() - t
-    m = int(min(S, max(n, n * budget_s / max(dt, 1e-3))))
-    k = 1
-    if m == S and p1s is not None and p1s.shape[0] > 1:   # a whole instance fits: take more instances
-        k = int(min(p1s.shape[0], max(1, budget_s / max(dt * S / n, 1e-3))))
-    reps = 1
-    if m == S:   # the whole sample is shorter than the budget: repeat it
         t = time.perf_counter()
-        run(start[:m], k)
+        oracle.track(hom, start, nthreads=nthreads)
         d1 = time.perf_counter() - t
         reps = int(min(1000, max(1, budget_s / max(d1, 1e-4))))
+        if d1 > budget_s:   # eco-12 (118,098 tracks): a strided subset
+            m = max(nthreads * 4, int(start.shape[0] * budget_s / d1))
+            idx = np.linspace(0, start.shape[0] - 1, m).astype(np.int64)
+            t = time.perf_counter()
+            oracle.track(hom, start[idx], nthreads=nthreads)
+            dt = time.perf_counter() - t
+            return m / dt, nthreads, f"{m} of {start.shape[0]} tracks, evenly strided ({dt:.1f} s, {nthreads} threads)"
+        t = time.perf_counter()
+        for _ in range(reps):
+            oracle.track(hom, start, nthreads=nthreads)
+        dt = time.perf_counter() - t
+        return start.shape[0] * reps / dt, nthreads, (f"all {start.shape[0]} tracks, {reps} repetitions "
+                                                      f"({dt:.1f} s, {nthreads} threads)")
+    n_batch = 1 if name == "cyclic7ph" else 1024
+    k = min(64, n_batch)
+    inst = np.unique(np.linspace(0, n_batch - 1, k).astype(np.int64))
+    d, start, p0, _, _, _ = make_workload(name, 0, 1)
+    from hc_inputs import rng
+    if name == "cyclic7ph":
+        from hc_inputs import systems
+        p1s = systems.cyclic_family_target(7)[None]
+    else:
+        p1s = np.concatenate([make_workload(name, int(b), int(b) + 1)[3] for b in inst])
+    hom = oracle.ph_homotopy(d, p0)
+    S = start.shape[0]
+    perm = rng.gen(20261017).permutation(S)
+    probe = perm[:max(4, min(S, 2 * nthreads // len(inst) + 2))]
+    t = time.perf_counter()
+    oracle.track(hom, start[probe], p1s=p1s, nthreads=nthreads)
+    per_track = (time.perf_counter() - t) / (len(probe) * len(inst))
+    m = int(min(S, max(len(probe), budget_s / max(per_track * len(inst), 1e-9))))
+    reps = 1
+    if m == S:
+        reps = int(min(100, max(1, budget_s / max(per_track * len(inst) * S, 1e-9))))
     t = time.perf_counter()
     for _ in range(reps):
-        run(start[:m], k)
+        oracle.track(hom, start[perm[:m]], p1s=p1s, nthreads=nthreads)
     dt = time.perf_counter() - t
-    what = (f"first {m} of {S} tracks of instance 0" if k == 1 else f"all {S} tracks of the first {k} instances")
-    if reps > 1:
-        what += f", {reps} repetitions"
-    return m * k * reps / dt, nthreads, f"{what} ({dt:.1f} s, {nthreads} threads)"
+    what = (f"{m} of {S} start solutions (seeded permutation) x {len(inst)} instances spread over the "
+            f"{n_batch}-instance batch" + (f", {reps} repetitions" if reps > 1 else ""))
+    return m * len(inst) * reps / dt, nthreads, f"{what} ({dt:.1f} s, {nthreads} threads)"
 
 
 def run_reference(args):
@@ -189,7 +221,7 @@ def run_reference(args):
             steps.append((v, sample))
     vals = [v for v, _ in steps]
     value = statistics.median(vals)
-    _, _, _, _, _, meta = make_workload(args.config, 1, 0)
+    _, _, _, _, _, meta = make_workload(args.config, 0, 1)
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "tracks/s", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": None, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "c128 (fp64)", "data": "synthetic",
@@ -235,12 +267,9 @@ def run_ours(args):
         if distributed:
             dist.barrier(device_ids=[local_rank])
 
-    B = args.instances
-    if args.total_instances:   # strong scaling: a fixed job (configs[4]: 8192 instances) split over the ranks
-        if args.total_instances % world:
-            raise SystemExit(f"--total-instances {args.total_instances} is not a multiple of {world} GPUs")
-        B = args.total_instances // world
-    d, start, p0, p1s, _, meta = make_workload(args.config, B, rank)
+    lo, hi = instance_range(args, rank, world)
+    B = hi - lo
+    d, start, p0, p1s, _, meta = make_workload(args.config, lo, hi)
     if p1s is not None:
         B = p1s.shape[0]   # single-instance workloads fix their own batch
     if start is None:
@@ -276,6 +305,13 @@ def run_ours(args):
         flush.fill_(1.0)
         hc.track_batch(sysh, x_start, t_p0, t_p1[:wb], st=st, stream=stream,
                        out=tuple(o[:wb] for o in out)).wait()
+    # ---- the FP64 peak measured in-process, on this GPU, with its clock (the roofline denominator
+    #      beside the derived 148 x 64 DFMA/clk x 2 x 1965 MHz) ----
+    pclk = ClockSampler(local_rank)
+    pclk.start()
+    time.sleep(0.3)
+    peak_meas = hc.fp64_peak_probe(local_rank)
+    peak_ck = pclk.stop()
     clocks = ClockSampler(local_rank)
     clocks.start()
     time.sleep(0.3)
@@ -305,13 +341,22 @@ def run_ours(args):
     prologue_ms = statistics.mean(p[1] for p in per_launch)
     ctr = out[2]
     solves = int(ctr[..., 3].sum().item())
+    # our kernels per step: coefficient prologue + tracker, + the Cauchy endgame kernel when the endgame
+    # is on, + its own prologue after a wide-layout tracker (abi.cpp hc_track_batch)
+    wide = launch["lanes_per_track"] == 32 and N <= 16
+    n_launch = 2 + (1 if st.eg_start > 0 else 0) + (1 if st.eg_start > 0 and wide else 0)
     status = out[1]
     flops = solves * info["flops_solve"]
     converged = int((status == hc.HC_CONVERGED).sum().item())
     for r in results:
         r.close()
 
-    tracks_total = world * B * S * args.steps
+    B_all = B
+    if distributed:   # uneven strong-scaling shards: count what every rank processed
+        tb = torch.tensor([B], dtype=torch.int64, device=dev)
+        dist.all_reduce(tb)
+        B_all = int(tb.item())
+    tracks_total = B_all * S * args.steps
     value = tracks_total / (elapsed_max / 1e3)
     sm_mhz = ck.get("sm_mhz") or SM_MAX_MHZ
     peak_max = 148 * FP64_DFMA_PER_CLK_PER_SM * 2 * SM_MAX_MHZ * 1e6 / 1e12
@@ -352,7 +397,7 @@ def run_ours(args):
             dist.all_reduce(tw, op=dist.ReduceOp.MAX)
         h2d = hstart.nbytes + hp0.nbytes + hp1.nbytes
         d2h = hx.nbytes + hs.nbytes + hcn.nbytes + hr.nbytes
-        e2e = {"value": world * B * S * k / float(tw.item()), "unit": "tracks/s", "h2d_bytes_per_step": int(h2d),
+        e2e = {"value": B_all * S * k / float(tw.item()), "unit": "tracks/s", "h2d_bytes_per_step": int(h2d),
                "d2h_bytes_per_step": int(d2h), "steps": k, "timing": "wall clock around synchronous hc_track_batch "
                "(HC_MEM_HOST, pinned buffers), max over ranks"}
 
@@ -369,8 +414,9 @@ def run_ours(args):
             "metric": METRIC, "value": value, "unit": "tracks/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": elapsed_max / args.steps, "higher_is_better": True,
             "scaling": "strong" if args.total_instances else "weak", "vs_baseline": None, "dtype": "c128 (fp64)",
-            "data": "synthetic", "instances_per_sec": world * B * args.steps / (elapsed_max / 1e3),
-            "config": {"workload": meta["workload"], "instances_per_gpu": B, "tracks_per_instance": S,
+            "data": "synthetic", "instances_per_sec": B_all * args.steps / (elapsed_max / 1e3),
+            "config": {"workload": meta["workload"], "instances_per_gpu": B, "instances_total": B_all,
+                       "instance_block_rank0": [lo, hi], "tracks_per_instance": S,
                        "N": N, "l2": "256 MB buffer written between steps (flush)", "parallelism": f"dp{world}",
                        "warmup_instances": wb,
                        "launch": launch},
@@ -380,9 +426,14 @@ def run_ours(args):
                          "peak_note": "FP64 vector: 148 SM x 64 DFMA/clk x 2 x 1965 MHz (derived, DESIGN.md); "
                                       "frac at the measured median clock: %.3f" %
                                       (achieved / (peak_max * sm_mhz / SM_MAX_MHZ)),
+                         "peak_measured": peak_meas, "frac_of_measured": achieved / peak_meas,
+                         "peak_measured_clocks": peak_ck,
+                         "peak_measured_note": "hc_fp64_peak_probe (8 independent DFMA chains per thread, "
+                                               "2048 threads/SM) run in this process before the timed region",
                          "flops_per_launch": flops,
                          "tracker_ms_per_launch": tracker_ms, "prologue_ms_per_launch": prologue_ms},
-            "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": 2 * args.steps,
+            "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": n_launch * args.steps,
+            "gpu_launches_per_step": n_launch,
             "clocks": ck, "converged_fraction": converged / (B * S), "gather_ms": gather_ms,
             "solves_per_track": solves / (B * S),
             "step_ms": {"median": statistics.median(step_ms), "p10": float(np.percentile(step_ms, 10)),

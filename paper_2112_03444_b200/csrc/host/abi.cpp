@@ -651,9 +651,23 @@ hc_status hc_track_batch(hc_system sys, const hc_tracker_settings *settings, con
   cudaEventRecord(r->ev[3], r->stream);
   // ---- the Cauchy endgame (reading R26) over the tracks the tracker handed over; the count stays
   //      on the device, so an empty list costs one short launch and no host synchronisation.  It
-  //      runs on the throughput-layout tables (the coefficient slots are the same in both layouts) ----
+  //      runs on the throughput-layout tables (after the wide layout, with their own coefficient
+  //      polynomials: slots are relabelled per layout) ----
   if (st.eg_start > 0.0) {
     TrackArgs ea = ta;
+    if (wide) {   // coefficient slots are bank-relabelled per layout: the throughput tables need their own
+      double2 *d_coef_n = nullptr;
+      if ((s = dev_alloc(r, &d_coef_n, (size_t)B * (sys->cs.D + 1) * sys->cs.ncoef)) != HC_OK) return bail(s);
+      PrologueArgs pn = pa;
+      pn.mono = sys->dt.d_mono;
+      pn.coef_mono_ptr = sys->dt.d_mono_ptr;
+      pn.ncoef = sys->cs.ncoef;
+      pn.D = sys->cs.D;
+      pn.coef_t = d_coef_n;
+      e = launch_prologue(pn, r->stream);
+      if (e != cudaSuccess) return bail(cuda_fail(e, "coef prologue launch (endgame tables)"));
+      ea.coef_t = d_coef_n;
+    }
     ea.ops = sys->dt.d_ops;
     ea.Q = sys->cs.Q;
     ea.mono_prog = sys->dt.d_mono_prog;
@@ -662,8 +676,6 @@ hc_status hc_track_batch(hc_system sys, const hc_tracker_settings *settings, con
     for (int l = 0; l < MAX_LEVELS; ++l) ea.level_end[l] = sys->cs.level_end[l];
     ea.mpos = sys->dt.d_mpos;
     ea.n_entries = sys->cs.n_entries;
-    if (sys->cs.ncoef != cs.ncoef || sys->cs.D != cs.D || sys->cs.ncoef_src != cs.ncoef_src)
-      return bail(fail(HC_E_INTERNAL, "lane layouts disagree on coefficient slots"));
     e = kEndgame[N](ea, sys->device, r->stream);
     if (e != cudaSuccess) return bail(cuda_fail(e, "endgame launch"));
   }

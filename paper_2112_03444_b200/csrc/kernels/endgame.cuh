@@ -81,16 +81,22 @@ __device__ __forceinline__ void endgame_body(const TrackArgs &A) {
   double s_h = 0.0, dt_h = 0.0;                                           // hand-over point
   int arc = 0, loops = 0, radius = 0, m = 0;
   bool have_est = false, need_track = true, cauchy_est = false;
+  double dbg_where = 0.0;
   double2 x = make_double2(0.0, 0.0), xr = x, sum = x, est = x, kacc = x, kprev = x, xc = x, xh = x;
   const bool valid = r < N;
   double2 cval_t = make_double2(-1.0, 0.0);   // t of the slot's cached coefficient values
 
   auto circ = [&](double theta) { double sn, cs; sincos(theta, &sn, &cs); return make_double2(cs, sn); };
+  int dbg = 0;
   auto done = [&](int status, double ra, double rr, int wind) {
     if (valid) A.x_out[(size_t)g * N + r] = x;
     if (r == 0) {
       A.status_out[g] = status;
       reinterpret_cast<int4 *>(A.counters_out)[g] = make_int4(steps, rej, newt, solves);
+      if (HCB_EG_DEBUG) {   // (failure reason, radius * 100 + loops at the failure, s there)
+        ra = dbg;
+        rr = dbg_where;
+      }
       reinterpret_cast<double2 *>(A.resid_out)[g] = make_double2(ra, rr);
       if (A.winding_out) A.winding_out[g] = wind;
     }
@@ -114,9 +120,9 @@ __device__ __forceinline__ void endgame_body(const TrackArgs &A) {
   };
   // the Cauchy endgame failed (or its estimate is not a root): resume plain tracking from the
   // hand-over point to t = 1 (R5-R9), then polish and classify
-  int dbg = 0;
   auto fallback = [&](int why) {
     dbg = why;
+    dbg_where = radius * 100 + loops + 1e-3 * arc;
     x = xh;
     tr = 1.0 - s_h;
     t_end = 1.0;
@@ -265,7 +271,7 @@ __device__ __forceinline__ void endgame_body(const TrackArgs &A) {
       } else if (!x_fin) {
         done(HC_NONFINITE, INFINITY, INFINITY, 0);
       } else {
-        done(conv ? HC_CONVERGED : HC_SINGULAR, res_abs, HCB_EG_DEBUG ? (double)dbg : res_rel, 0);
+        done(conv ? HC_CONVERGED : HC_SINGULAR, res_abs, res_rel, 0);
       }
       continue;
     }

@@ -325,7 +325,9 @@ __device__ __forceinline__ bool lu_rows(double2 (&a)[N + 1], int r, int seg, dou
   __syncwarp();
   // ---- the system is now diagonal in pivot order: x_{mystep} = b' / pivot, routed through shared memory ----
   double2 *xsol = prow;
-  if (mystep < N) xsol[mystep] = cmul(a[N], myinv);
+  // a row that was never a pivot (mystep == -1: only when the search found no usable candidate, i.e.
+  // a singular solve) writes nothing -- xsol[-1] would be the slot's always-zero entry of M
+  if (mystep >= 0 && mystep < N) xsol[mystep] = cmul(a[N], myinv);
   __syncwarp();
   const double2 sol = (r < N) ? xsol[r] : make_double2(0.0, 0.0);
   y = sol;
@@ -925,8 +927,13 @@ __device__ __forceinline__ void track_body(const TrackArgs &A) {
           e.s_next = 0.5 * s;
         }
         __syncwarp();
+#ifndef HCB_EG_BISECT_NOWRITE
         if (want && r == 0) *egs = e;
+#endif
       }
+#ifdef HCB_EG_BISECT_NODECIDE
+      eg_inf = eg_cauchy = false;
+#endif
       // the decision is carried out by the state machine below (one finish() call site): this
       // iteration's evaluation is a dummy for the slot and counts no solve
       if (eg_inf || eg_cauchy) {
