@@ -290,7 +290,8 @@ def run_ours(args):
     out = (torch.empty((B, S, N), dtype=torch.complex128, device=dev),
            torch.empty((B, S), dtype=torch.int32, device=dev),
            torch.empty((B, S, 4), dtype=torch.int32, device=dev),
-           torch.empty((B, S, 2), dtype=torch.float64, device=dev))
+           torch.empty((B, S, 2), dtype=torch.float64, device=dev),
+           torch.empty((B, S), dtype=torch.int32, device=dev))   # Cauchy endgame winding numbers
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)   # 256 MB > 126 MB L2
     stream = torch.cuda.current_stream(dev)
 
@@ -339,6 +340,7 @@ def run_ours(args):
     per_launch = [r.elapsed_ms() for r in results]   # (total, prologue, tracker) events on the launch stream
     tracker_ms = statistics.mean(p[2] for p in per_launch)
     prologue_ms = statistics.mean(p[1] for p in per_launch)
+    endgame_ms = statistics.mean(p[0] - p[1] - p[2] for p in per_launch)   # Cauchy endgame (+ its prologue)
     ctr = out[2]
     solves = int(ctr[..., 3].sum().item())
     # our kernels per step: coefficient prologue + tracker, + the Cauchy endgame kernel when the endgame
@@ -348,6 +350,8 @@ def run_ours(args):
     status = out[1]
     flops = solves * info["flops_solve"]
     converged = int((status == hc.HC_CONVERGED).sum().item())
+    status_counts = torch.bincount(status.reshape(-1).to(torch.int64), minlength=7).tolist()
+    eg_tracks = int((results[0].winding > 0).sum().item()) if results[0].winding is not None else None
     for r in results:
         r.close()
 
@@ -368,7 +372,7 @@ def run_ours(args):
         barrier()
         torch.cuda.synchronize()
         g0 = time.perf_counter()
-        gather_to_rank0(list(out))
+        gather_to_rank0(list(out[:4]))
         torch.cuda.synchronize()
         gather_ms = (time.perf_counter() - g0) * 1e3
 
@@ -431,10 +435,12 @@ def run_ours(args):
                          "peak_measured_note": "hc_fp64_peak_probe (8 independent DFMA chains per thread, "
                                                "2048 threads/SM) run in this process before the timed region",
                          "flops_per_launch": flops,
-                         "tracker_ms_per_launch": tracker_ms, "prologue_ms_per_launch": prologue_ms},
+                         "tracker_ms_per_launch": tracker_ms, "prologue_ms_per_launch": prologue_ms,
+                         "endgame_ms_per_launch": endgame_ms},
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": n_launch * args.steps,
             "gpu_launches_per_step": n_launch,
             "clocks": ck, "converged_fraction": converged / (B * S), "gather_ms": gather_ms,
+            "status_counts": dict(zip(hc.STATUS_NAMES, status_counts)), "cauchy_endgame_tracks": eg_tracks,
             "solves_per_track": solves / (B * S),
             "step_ms": {"median": statistics.median(step_ms), "p10": float(np.percentile(step_ms, 10)),
                         "p90": float(np.percentile(step_ms, 90)), "n": len(step_ms)},

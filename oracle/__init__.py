@@ -18,7 +18,8 @@ from dataclasses import dataclass, fields
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-_SO = os.path.join(_HERE, "liboracle.so")
+# ORACLE_SO: a prebuilt variant (e.g. the ASan/UBSan build of scripts/sanitize_host.sh)
+_SO = os.environ.get("ORACLE_SO") or os.path.join(_HERE, "liboracle.so")
 _SRC = [os.path.join(_HERE, "hc_oracle.c"), os.path.join(_HERE, "hc_oracle.h")]
 
 CONVERGED, DIVERGED, STEP_UNDERFLOW, MAX_STEPS, SINGULAR, NONFINITE, AT_INFINITY = range(7)
@@ -27,6 +28,8 @@ STATUS_NAMES = ["CONVERGED", "DIVERGED", "STEP_UNDERFLOW", "MAX_STEPS", "SINGULA
 
 def build(force: bool = False) -> str:
     """Compile liboracle.so with gcc (plain C99, -O2, no fast-math, no FMA contraction)."""
+    if os.environ.get("ORACLE_SO"):
+        return _SO
     stale = force or not os.path.exists(_SO) or any(os.path.getmtime(s) > os.path.getmtime(_SO) for s in _SRC)
     if stale:
         cmd = ["gcc", "-std=gnu99", "-O2", "-fPIC", "-shared", "-ffp-contract=off", "-fno-fast-math",

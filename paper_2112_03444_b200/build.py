@@ -35,8 +35,11 @@ elif VARIANT == "hybrid":   # experiment: 16-lane hybrid layout for N = 17, 18 (
 # any variant may add preprocessor switches for A/B experiments, e.g.
 # HCB_VARIANT=w16 HCB_DEFINES="HCB_MAXW_MID=16" (see the #ifndef switches in kernels/tracker.cuh)
 FLAGS = FLAGS + ["-D" + d for d in os.environ.get("HCB_DEFINES", "").split()] if VARIANT else FLAGS
+# HCB_HOST_FLAGS: extra g++ flags for the host translation units only (e.g. the sanitizer build,
+# scripts/sanitize_host.sh)
+HOST_FLAGS = os.environ.get("HCB_HOST_FLAGS", "").split() if VARIANT else []
 BUILD = os.path.join(PKG, "build" + ("_" + VARIANT if VARIANT else ""),
-                     hashlib.sha1(" ".join(ARCH + [f for f in FLAGS if not f.startswith("-I")]).encode()).hexdigest()[:10])
+                     hashlib.sha1(" ".join(ARCH + [f for f in FLAGS if not f.startswith("-I")] + HOST_FLAGS).encode()).hexdigest()[:10])
 
 
 def sources():
@@ -59,7 +62,8 @@ def _compile(src, hdr_mtime, verbose):
     if os.path.exists(obj) and os.path.getmtime(obj) >= max(os.path.getmtime(src), hdr_mtime):
         return obj, False
     lang = ["-x", "cu"] if src.endswith(".cu") else ["-x", "c++"]
-    cmd = [NVCC] + ARCH + FLAGS + lang + ["-c", src, "-o", obj]
+    host = [] if src.endswith(".cu") else [a for f in HOST_FLAGS for a in ("-Xcompiler", f)]
+    cmd = [NVCC] + ARCH + FLAGS + host + lang + ["-c", src, "-o", obj]
     if verbose:
         print(" ".join(cmd), flush=True)
     p = subprocess.run(cmd, capture_output=True, text=True)
@@ -78,7 +82,8 @@ def build(verbose: bool = False, jobs: int | None = None) -> str:
     objs = [o for o, _ in results]
     changed = any(c for _, c in results)
     if changed or not os.path.exists(LIB) or os.path.getmtime(LIB) < max(os.path.getmtime(o) for o in objs):
-        cmd = [NVCC] + ARCH + ["-shared", "-cudart", "static", "-o", LIB] + objs + ["-lpthread", "-ldl", "-lrt"]
+        cmd = ([NVCC] + ARCH + ["-shared", "-cudart", "static", "-o", LIB] + objs + ["-lpthread", "-ldl", "-lrt"]
+               + [a for f in HOST_FLAGS for a in ("-Xcompiler", f)])
         if verbose:
             print(" ".join(cmd), flush=True)
         subprocess.run(cmd, check=True)

@@ -8,6 +8,8 @@
 #include <string>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>   // header-only NVTX v3: ranges cost nothing unless a tool is attached
+
 #include "../hc_internal.h"
 #include "compiler.h"
 #include "../kernels/layout.h"
@@ -473,7 +475,21 @@ static bool wide_layout(int device, int N, int64_t tracks) {
   return tracks * 2 <= slots * 5;
 }
 
+// NVTX range over a scope (host side: the enqueue, or the whole call for HC_MEM_HOST)
+struct NvtxRange {
+  explicit NvtxRange(const char *name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
+
+static hc_status track_batch_impl(hc_system sys, const hc_tracker_settings *settings, const hc_batch *bt,
+                                  hc_result *out);
 hc_status hc_track_batch(hc_system sys, const hc_tracker_settings *settings, const hc_batch *bt, hc_result *out) {
+  NvtxRange range("hc_track_batch");
+  return track_batch_impl(sys, settings, bt, out);
+}
+
+static hc_status track_batch_impl(hc_system sys, const hc_tracker_settings *settings, const hc_batch *bt,
+                                  hc_result *out) {
   if (out) *out = nullptr;
   if (!sys || !bt) return fail(HC_E_INVALID_ARG, "null argument");
   hc_tracker_settings st;
@@ -581,7 +597,9 @@ hc_status hc_track_batch(hc_system sys, const hc_tracker_settings *settings, con
   pa.B = B;
   pa.coef_t = d_coef;
   cudaEventRecord(r->ev[0], r->stream);
+  nvtxRangePushA("hc: coefficient prologue");
   cudaError_t e = launch_prologue(pa, r->stream);
+  nvtxRangePop();
   if (e != cudaSuccess) return bail(cuda_fail(e, "coef prologue launch"));
   cudaEventRecord(r->ev[1], r->stream);
 
@@ -646,7 +664,9 @@ hc_status hc_track_batch(hc_system sys, const hc_tracker_settings *settings, con
     r->phase_cycles = pc;
   }
 #endif
+  nvtxRangePushA("hc: fused tracker");
   e = (wide ? tracker_launcher_wide(N) : tracker_launcher(N))(ta, sys->device, r->stream, &r->plan);
+  nvtxRangePop();
   if (e != cudaSuccess) return bail(cuda_fail(e, "tracker launch"));
   cudaEventRecord(r->ev[3], r->stream);
   // ---- the Cauchy endgame (reading R26) over the tracks the tracker handed over; the count stays
@@ -676,7 +696,9 @@ hc_status hc_track_batch(hc_system sys, const hc_tracker_settings *settings, con
     for (int l = 0; l < MAX_LEVELS; ++l) ea.level_end[l] = sys->cs.level_end[l];
     ea.mpos = sys->dt.d_mpos;
     ea.n_entries = sys->cs.n_entries;
+    nvtxRangePushA("hc: Cauchy endgame");
     e = kEndgame[N](ea, sys->device, r->stream);
+    nvtxRangePop();
     if (e != cudaSuccess) return bail(cuda_fail(e, "endgame launch"));
   }
   cudaEventRecord(r->ev[2], r->stream);

@@ -783,7 +783,13 @@ __device__ __forceinline__ void track_body(const TrackArgs &A) {
   unsigned char *sb = slots_base + (size_t)slot * slot_bytes(N, L * NC, ncoef, A.ncoef_src, A.n_mono, A.n_entries + 1);
   EgSample *egs = reinterpret_cast<EgSample *>(sb);   // endgame sampling state (R26), lane 0 writes
   double2 *vstate = reinterpret_cast<double2 *>(sb + EG_SAMPLE_BYTES);   // [3][NC][L]
-  double2 *cval = vstate + 3 * NC * L;
+  // per-lane copies of the slot's rarely touched scalars (structure of arrays, conflict-free): track
+  // id, step size, step / rejection / Newton / consecutive-accept counters -- in shared memory, so the
+  // loop's register budget (128 for N <= 16) goes to the rows being eliminated
+  long long *s_g = reinterpret_cast<long long *>(vstate + 3 * NC * L);
+  double *s_dt = reinterpret_cast<double *>(s_g + NC * L);
+  int *s_cnt = reinterpret_cast<int *>(s_dt + NC * L);   // [4][NC * L]: steps, rej, newt, acc
+  double2 *cval = vstate + 5 * NC * L;
   double2 *mono = cval + ncoef + A.ncoef_src;
   double2 *M = mono + A.n_mono;
   double2 *prow = M + A.n_entries + 1;
@@ -799,10 +805,16 @@ __device__ __forceinline__ void track_body(const TrackArgs &A) {
 
   // ---- slot state (replicated over the slot's lanes) ----
   int state = ST_DONE;
-  long long g = -1;
+  long long &g = s_g[r];
+  g = -1;
   const double2 *ct = A.coef_t;   // instance coefficient table
-  double t = 0.0, dt = 0.0, h = 0.0, t1 = 0.0;
-  int stage = 0, it = 0, acc = 0, steps = 0, rej = 0, newt = 0, solves = 0;
+  double t = 0.0, h = 0.0, t1 = 0.0;
+  double &dt = s_dt[r];
+  int &steps = s_cnt[0 * NC * L + r], &rej = s_cnt[1 * NC * L + r], &newt = s_cnt[2 * NC * L + r],
+      &acc = s_cnt[3 * NC * L + r];
+  dt = 0.0;
+  acc = steps = rej = newt = 0;
+  int stage = 0, it = 0, solves = 0;
   // component c of lane r is unknown r (c = 0) or 16 + r (c = 1, hybrid layout, r < E)
   // x stays in registers; the RK accumulators and the corrector's point live in the slot's shared
   // memory ([kacc | kprev | xc][NC][L], one conflict-free 16-byte word per lane): they are touched a

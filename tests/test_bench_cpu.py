@@ -16,7 +16,7 @@ CONFIGS = ["trifocal", "fourview", "fivepoint", "p3p", "cyclic7", "cyclic7ph", "
 
 @pytest.mark.parametrize("name", CONFIGS)
 def test_workload_shapes(name):
-    d, start, p0, p1s, _, meta = bench.make_workload(name, 2, 0)
+    d, start, p0, p1s, _, meta = bench.make_workload(name, 0, 2)
     assert meta["workload"]
     if start is None:   # total-degree single instance: the library builds start and parameters
         assert d.n_params == 0
@@ -27,10 +27,21 @@ def test_workload_shapes(name):
     assert np.all(np.isfinite(start)) and np.all(np.isfinite(p1s))
 
 
-def test_rank_offsets_give_distinct_instances():
-    """Weak scaling: rank r owns instances r*B .. r*B+B-1 (distinct seeds per rank)."""
-    a = bench.make_workload("fourview", 2, 0)[3]
-    b = bench.make_workload("fourview", 2, 1)[3]
+def test_rank_instance_blocks():
+    """Each rank's instances come from distributed.shard_range: weak scaling gives every rank its own
+    --instances block, strong scaling splits --total-instances (uneven totals too); instance b is the
+    same input whichever rank (and block size) builds it."""
+    import argparse
+    weak = argparse.Namespace(instances=3, total_instances=0)
+    strong = argparse.Namespace(instances=3, total_instances=7)
+    assert [bench.instance_range(weak, r, 2) for r in range(2)] == [(0, 3), (3, 6)]
+    assert [bench.instance_range(strong, r, 2) for r in range(2)] == [(0, 4), (4, 7)]
+    assert [bench.instance_range(strong, r, 3) for r in range(3)] == [(0, 3), (3, 5), (5, 7)]
+    whole = bench.make_workload("fourview", 0, 7)[3]
+    parts = np.concatenate([bench.make_workload("fourview", *bench.instance_range(strong, r, 3))[3] for r in range(3)])
+    assert np.array_equal(whole, parts)
+    a = bench.make_workload("fourview", 0, 2)[3]
+    b = bench.make_workload("fourview", 2, 4)[3]
     assert not np.allclose(a, b)
 
 
