@@ -344,9 +344,11 @@ def run_ours(args):
     ctr = out[2]
     solves = int(ctr[..., 3].sum().item())
     # our kernels per step: coefficient prologue + tracker, + the Cauchy endgame kernel when the endgame
-    # is on, + its own prologue after a wide-layout tracker (abi.cpp hc_track_batch)
+    # is on, + its own prologue when its layout (wide for N <= 16) differs from the tracker's
+    # (abi.cpp hc_track_batch)
     wide = launch["lanes_per_track"] == 32 and N <= 16
-    n_launch = 2 + (1 if st.eg_start > 0 else 0) + (1 if st.eg_start > 0 and wide else 0)
+    eg_on = st.eg_start > 0
+    n_launch = 2 + (1 if eg_on else 0) + (1 if eg_on and (N <= 16) != wide else 0)
     status = out[1]
     flops = solves * info["flops_solve"]
     converged = int((status == hc.HC_CONVERGED).sum().item())

@@ -16,7 +16,9 @@
 
 namespace hcb {
 // per-N launchers defined in csrc/kernels/tracker_n*.cu
-#define HCB_DECLW(N) cudaError_t launch_tracker_wide_##N(const TrackArgs &, int, cudaStream_t, TrackerPlan *);
+#define HCB_DECLW(N)                                                                        \
+  cudaError_t launch_tracker_wide_##N(const TrackArgs &, int, cudaStream_t, TrackerPlan *); \
+  cudaError_t launch_endgame_wide_##N(const TrackArgs &, int, cudaStream_t);
 HCB_DECLW(1) HCB_DECLW(2) HCB_DECLW(3) HCB_DECLW(4) HCB_DECLW(5) HCB_DECLW(6) HCB_DECLW(7) HCB_DECLW(8)
 HCB_DECLW(9) HCB_DECLW(10) HCB_DECLW(11) HCB_DECLW(12) HCB_DECLW(13) HCB_DECLW(14) HCB_DECLW(15) HCB_DECLW(16)
 #undef HCB_DECLW
@@ -66,6 +68,12 @@ static const tracker_launch_fn kTrackersWide[17] = {
     launch_tracker_wide_12, launch_tracker_wide_13, launch_tracker_wide_14, launch_tracker_wide_15,
     launch_tracker_wide_16};
 static tracker_launch_fn tracker_launcher_wide(int N) { return (N >= 1 && N <= 16) ? kTrackersWide[N] : nullptr; }
+static const endgame_fn kEndgameWide[17] = {
+    nullptr,               launch_endgame_wide_1,  launch_endgame_wide_2,  launch_endgame_wide_3,
+    launch_endgame_wide_4, launch_endgame_wide_5,  launch_endgame_wide_6,  launch_endgame_wide_7,
+    launch_endgame_wide_8, launch_endgame_wide_9,  launch_endgame_wide_10, launch_endgame_wide_11,
+    launch_endgame_wide_12, launch_endgame_wide_13, launch_endgame_wide_14, launch_endgame_wide_15,
+    launch_endgame_wide_16};
 
 cudaError_t launch_batched_zgesv(int n, int64_t batch, const double2 *A, const double2 *b, double2 *x,
                                  int32_t *info, double pivot_rel, cudaStream_t s) {
@@ -674,30 +682,39 @@ static hc_status track_batch_impl(hc_system sys, const hc_tracker_settings *sett
   //      runs on the throughput-layout tables (after the wide layout, with their own coefficient
   //      polynomials: slots are relabelled per layout) ----
   if (st.eg_start > 0.0) {
+    // the endgame's tracks are a latency chain: it runs in the wide layout (one track per warp on 32
+    // lanes) for N <= 16, else in the throughput layout; coefficient slots are bank-relabelled per
+    // layout, so a layout other than the tracker's gets its own coefficient polynomials
+    const bool eg_wide = sys->has_wide;
+    const CompiledSystem &ecs = eg_wide ? sys->cs_w : sys->cs;
+    const DevTables &edt = eg_wide ? sys->dt_w : sys->dt;
     TrackArgs ea = ta;
-    if (wide) {   // coefficient slots are bank-relabelled per layout: the throughput tables need their own
-      double2 *d_coef_n = nullptr;
-      if ((s = dev_alloc(r, &d_coef_n, (size_t)B * (sys->cs.D + 1) * sys->cs.ncoef)) != HC_OK) return bail(s);
-      PrologueArgs pn = pa;
-      pn.mono = sys->dt.d_mono;
-      pn.coef_mono_ptr = sys->dt.d_mono_ptr;
-      pn.ncoef = sys->cs.ncoef;
-      pn.D = sys->cs.D;
-      pn.coef_t = d_coef_n;
-      e = launch_prologue(pn, r->stream);
+    if (eg_wide != wide) {
+      double2 *d_coef_e = nullptr;
+      if ((s = dev_alloc(r, &d_coef_e, (size_t)B * (ecs.D + 1) * ecs.ncoef)) != HC_OK) return bail(s);
+      PrologueArgs pe = pa;
+      pe.mono = edt.d_mono;
+      pe.coef_mono_ptr = edt.d_mono_ptr;
+      pe.ncoef = ecs.ncoef;
+      pe.D = ecs.D;
+      pe.coef_t = d_coef_e;
+      e = launch_prologue(pe, r->stream);
       if (e != cudaSuccess) return bail(cuda_fail(e, "coef prologue launch (endgame tables)"));
-      ea.coef_t = d_coef_n;
+      ea.coef_t = d_coef_e;
     }
-    ea.ops = sys->dt.d_ops;
-    ea.Q = sys->cs.Q;
-    ea.mono_prog = sys->dt.d_mono_prog;
-    ea.n_mono = sys->cs.n_mono;
-    ea.n_levels = sys->cs.n_levels;
-    for (int l = 0; l < MAX_LEVELS; ++l) ea.level_end[l] = sys->cs.level_end[l];
-    ea.mpos = sys->dt.d_mpos;
-    ea.n_entries = sys->cs.n_entries;
+    ea.ops = edt.d_ops;
+    ea.Q = ecs.Q;
+    ea.mono_prog = edt.d_mono_prog;
+    ea.n_mono = ecs.n_mono;
+    ea.n_levels = ecs.n_levels;
+    for (int l = 0; l < MAX_LEVELS; ++l) ea.level_end[l] = ecs.level_end[l];
+    ea.mpos = edt.d_mpos;
+    ea.n_entries = ecs.n_entries;
+    ea.ncoef = ecs.ncoef;
+    ea.ncoef_src = ecs.ncoef_src;
+    ea.D = ecs.D;
     nvtxRangePushA("hc: Cauchy endgame");
-    e = kEndgame[N](ea, sys->device, r->stream);
+    e = (eg_wide ? kEndgameWide[N] : kEndgame[N])(ea, sys->device, r->stream);
     nvtxRangePop();
     if (e != cudaSuccess) return bail(cuda_fail(e, "endgame launch"));
   }

@@ -54,7 +54,7 @@ __device__ __forceinline__ void endgame_body(const TrackArgs &A) {
   const int slot = warp * TPW + seg;
   const int ncoef = A.ncoef, D = A.D;
   unsigned char *sb = slots_base + (size_t)slot * slot_bytes(N, L, ncoef, A.ncoef_src, A.n_mono, A.n_entries + 1);
-  double2 *cval = reinterpret_cast<double2 *>(sb + EG_SAMPLE_BYTES) + 5 * L;   // (the tracker's per-lane area is unused here)
+  double2 *cval = reinterpret_cast<double2 *>(sb + EG_SAMPLE_BYTES) + 7 * L;   // (the tracker's per-lane area is unused here)
   double2 *mono = cval + ncoef + A.ncoef_src;
   double2 *M = mono + A.n_mono;
   double2 *prow = M + A.n_entries + 1;
@@ -396,16 +396,17 @@ __device__ __forceinline__ void endgame_body(const TrackArgs &A) {
   }
 }
 
-template <int N>
+template <int N, int LW>
 __global__ void __launch_bounds__(128) hc_endgame_kernel(const TrackArgs A) {
-  endgame_body<N, lanes_for(N)>(A);
+  endgame_body<N, LW>(A);
 }
 
 // Launch over the tracks the tracker handed over (the count is read on the device: no host sync).
-// 4 warps per CTA, as many CTAs as fit (persistent), shared memory as in the tracker.
-template <int N>
+// 4 warps per CTA, one CTA per SM (persistent), shared memory as in the tracker.  LW = 32 (N <= 16):
+// the wide latency layout, one track per warp -- the few handed-over tracks are a latency chain.
+template <int N, int LW = lanes_for(N)>
 cudaError_t launch_endgame_n(const TrackArgs &A, int device, cudaStream_t stream) {
-  constexpr int L = lanes_for(N);
+  constexpr int L = LW;
   constexpr int TPW = 32 / L;
   const size_t tables = table_bytes(A.Q, L, A.n_mono - (N + 1), N) + align16((size_t)2 * A.n_entries);
   const size_t per_warp = (size_t)TPW * slot_bytes(N, L, A.ncoef, A.ncoef_src, A.n_mono, A.n_entries + 1);
@@ -415,12 +416,12 @@ cudaError_t launch_endgame_n(const TrackArgs &A, int device, cudaStream_t stream
   while (warps > 1 && tables + warps * per_warp > (size_t)smem_max) --warps;
   const size_t smem = tables + warps * per_warp;
   if (smem > (size_t)smem_max) return cudaErrorInvalidConfiguration;
-  const void *fn = (const void *)hc_endgame_kernel<N>;
+  const void *fn = (const void *)hc_endgame_kernel<N, LW>;
   cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   int sms = 0;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
-  hc_endgame_kernel<N><<<(unsigned)sms, warps * 32, smem, stream>>>(A);
+  hc_endgame_kernel<N, LW><<<(unsigned)sms, warps * 32, smem, stream>>>(A);
   return cudaGetLastError();
 }
 

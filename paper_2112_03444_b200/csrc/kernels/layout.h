@@ -9,15 +9,15 @@ namespace hcb {
 __host__ __device__ inline size_t align16(size_t b) { return (b + 15) & ~size_t(15); }
 
 // Per track slot: the endgame sampling state (80 bytes, EgSample), the RK / corrector vectors
-// [kacc | kprev | xc][lnc] (lnc = lanes per track x unknowns per lane) and per-lane scalars (32 bytes
-// per lane: track id, step, four counters), cval[ncoef + ncoef_src]
+// [kacc | kprev | xc][lnc] (lnc = lanes per track x unknowns per lane) and per-lane scalars (64 bytes
+// per lane: track id, step, h, t1, the t of the cached coefficients, four counters), cval[ncoef + ncoef_src]
 // (c(t) for every slot, c'(t) for the rhs slots), mono[n_mono] (x_0..x_{N-1}, 1, shared products),
 // M[n_entries] (non-zero entries of [dH/dx | rhs]), prow[2 * (N + 1)] (double-buffered pivot row),
 // rabs[N] (doubles).
 constexpr size_t EG_SAMPLE_BYTES = 80;
 __host__ __device__ inline size_t slot_bytes(int N, int lnc, int ncoef, int ncoef_src, int n_mono, int n_entries) {
   return EG_SAMPLE_BYTES +
-         align16(sizeof(double) * 2 * ((size_t)5 * lnc + ncoef + ncoef_src + n_mono + n_entries + 2 * (N + 1)) +
+         align16(sizeof(double) * 2 * ((size_t)7 * lnc + ncoef + ncoef_src + n_mono + n_entries + 2 * (N + 1)) +
                  sizeof(double) * N);
 }
 

@@ -787,9 +787,9 @@ __device__ __forceinline__ void track_body(const TrackArgs &A) {
   // id, step size, step / rejection / Newton / consecutive-accept counters -- in shared memory, so the
   // loop's register budget (128 for N <= 16) goes to the rows being eliminated
   long long *s_g = reinterpret_cast<long long *>(vstate + 3 * NC * L);
-  double *s_dt = reinterpret_cast<double *>(s_g + NC * L);
-  int *s_cnt = reinterpret_cast<int *>(s_dt + NC * L);   // [4][NC * L]: steps, rej, newt, acc
-  double2 *cval = vstate + 5 * NC * L;
+  double *s_dt = reinterpret_cast<double *>(s_g + NC * L);   // [4][NC * L]: dt, h, t1, cval_t
+  int *s_cnt = reinterpret_cast<int *>(s_dt + 4 * NC * L);   // [4][NC * L]: steps, rej, newt, acc
+  double2 *cval = vstate + 7 * NC * L;
   double2 *mono = cval + ncoef + A.ncoef_src;
   double2 *M = mono + A.n_mono;
   double2 *prow = M + A.n_entries + 1;
@@ -808,8 +808,9 @@ __device__ __forceinline__ void track_body(const TrackArgs &A) {
   long long &g = s_g[r];
   g = -1;
   const double2 *ct = A.coef_t;   // instance coefficient table
-  double t = 0.0, h = 0.0, t1 = 0.0;
-  double &dt = s_dt[r];
+  double t = 0.0;
+  double &dt = s_dt[r], &h = s_dt[NC * L + r], &t1 = s_dt[2 * NC * L + r];
+  h = t1 = 0.0;
   int &steps = s_cnt[0 * NC * L + r], &rej = s_cnt[1 * NC * L + r], &newt = s_cnt[2 * NC * L + r],
       &acc = s_cnt[3 * NC * L + r];
   dt = 0.0;
@@ -829,7 +830,8 @@ __device__ __forceinline__ void track_body(const TrackArgs &A) {
   auto comp_row = [&](int c) -> int { return c == 0 ? r : 16 + r; };
   bool need_track = true;
   bool fresh_k1 = false;   // the last solve was a successful RK stage 1 (endgame sampling)
-  double cval_t = -1.0;   // t at which the slot's coefficient values were last evaluated (-1: none)
+  double &cval_t = s_dt[3 * NC * L + r];   // t at which the slot's coefficient values were last evaluated
+  cval_t = -1.0;                           // (-1: none)
 #ifdef HCB_PHASE_TIMING
   unsigned long long hcb_phase[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   long long hcb_iter0 = clock64();

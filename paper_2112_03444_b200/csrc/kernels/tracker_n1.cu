@@ -16,4 +16,7 @@ cudaError_t launch_zgesv_1(int64_t batch, const double2 *A, const double2 *b, do
 cudaError_t launch_endgame_1(const TrackArgs &A, int device, cudaStream_t s) {
   return launch_endgame_n<1>(A, device, s);
 }
+cudaError_t launch_endgame_wide_1(const TrackArgs &A, int device, cudaStream_t s) {
+  return launch_endgame_n<1, 32>(A, device, s);
+}
 }  // namespace hcb

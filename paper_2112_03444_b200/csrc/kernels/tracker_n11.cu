@@ -16,4 +16,7 @@ cudaError_t launch_zgesv_11(int64_t batch, const double2 *A, const double2 *b, d
 cudaError_t launch_endgame_11(const TrackArgs &A, int device, cudaStream_t s) {
   return launch_endgame_n<11>(A, device, s);
 }
+cudaError_t launch_endgame_wide_11(const TrackArgs &A, int device, cudaStream_t s) {
+  return launch_endgame_n<11, 32>(A, device, s);
+}
 }  // namespace hcb

@@ -16,4 +16,7 @@ cudaError_t launch_zgesv_2(int64_t batch, const double2 *A, const double2 *b, do
 cudaError_t launch_endgame_2(const TrackArgs &A, int device, cudaStream_t s) {
   return launch_endgame_n<2>(A, device, s);
 }
+cudaError_t launch_endgame_wide_2(const TrackArgs &A, int device, cudaStream_t s) {
+  return launch_endgame_n<2, 32>(A, device, s);
+}
 }  // namespace hcb

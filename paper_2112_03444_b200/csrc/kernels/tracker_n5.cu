@@ -16,4 +16,7 @@ cudaError_t launch_zgesv_5(int64_t batch, const double2 *A, const double2 *b, do
 cudaError_t launch_endgame_5(const TrackArgs &A, int device, cudaStream_t s) {
   return launch_endgame_n<5>(A, device, s);
 }
+cudaError_t launch_endgame_wide_5(const TrackArgs &A, int device, cudaStream_t s) {
+  return launch_endgame_n<5, 32>(A, device, s);
+}
 }  // namespace hcb

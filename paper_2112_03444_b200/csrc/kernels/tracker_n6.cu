@@ -16,4 +16,7 @@ cudaError_t launch_zgesv_6(int64_t batch, const double2 *A, const double2 *b, do
 cudaError_t launch_endgame_6(const TrackArgs &A, int device, cudaStream_t s) {
   return launch_endgame_n<6>(A, device, s);
 }
+cudaError_t launch_endgame_wide_6(const TrackArgs &A, int device, cudaStream_t s) {
+  return launch_endgame_n<6, 32>(A, device, s);
+}
 }  // namespace hcb

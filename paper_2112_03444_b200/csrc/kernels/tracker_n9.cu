@@ -16,4 +16,7 @@ cudaError_t launch_zgesv_9(int64_t batch, const double2 *A, const double2 *b, do
 cudaError_t launch_endgame_9(const TrackArgs &A, int device, cudaStream_t s) {
   return launch_endgame_n<9>(A, device, s);
 }
+cudaError_t launch_endgame_wide_9(const TrackArgs &A, int device, cudaStream_t s) {
+  return launch_endgame_n<9, 32>(A, device, s);
+}
 }  // namespace hcb

@@ -9,7 +9,7 @@ ASAN=$(gcc -print-file-name=libasan.so)
 UBSAN=$(gcc -print-file-name=libubsan.so)
 gcc -std=gnu99 -O1 -g -fPIC -shared -ffp-contract=off -fno-fast-math -fsanitize=address,undefined \
     -fno-omit-frame-pointer -o /tmp/hc_asan/liboracle.so oracle/hc_oracle.c -lm -lpthread
-HCB_VARIANT=asan HCB_DEFINES="HCB_ASAN_BUILD=1" HCB_HOST_FLAGS="-fsanitize=address,undefined -fno-omit-frame-pointer" \
+HCB_VARIANT=asan HCB_DEFINES="HCB_ASAN_BUILD=1" HCB_HOST_FLAGS="-fsanitize=address -fsanitize=undefined -fno-omit-frame-pointer" \
     python paper_2112_03444_b200/build.py > /dev/null
 export ASAN_OPTIONS=detect_leaks=0:halt_on_error=1:verify_asan_link_order=0
 export UBSAN_OPTIONS=halt_on_error=1:print_stacktrace=1
