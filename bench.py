@@ -5,7 +5,7 @@
 
 One "step" = one pass of the whole hot path (coefficient prologue + fused tracker: every
 §8(a) row a2-a10) over one batch.  Default workload: trifocal pose with unknown focal length,
-parameter homotopy from the oracle-generated start fixture (S = 5328 start solutions) to
+parameter homotopy from the oracle-generated start fixture (S = 5344 start solutions) to
 B = 1024 planted synthetic instances per GPU (BASELINE.json configs[3]; at 8 GPUs the job is
 configs[4], 8192 instances) -> weak scaling; `--total-instances 8192` runs configs[4] as a fixed
 job split over the GPUs (strong scaling).  Under torchrun each rank owns its own

@@ -32,7 +32,7 @@ def case(name):
     if name == "trifocal":
         d = systems.trifocal_unknown_f()
         p0, x0 = rng.trifocal_complex_start()
-        return d, p0, x0, systems.trifocal_symmetry, "R19/R20: 5328 = 666 orbits x 8 (paper 1784)"
+        return d, p0, x0, systems.trifocal_symmetry, "R19/R20: 5344 = 668 orbits x 8 (paper 1784)"
     raise SystemExit(name)
 
 

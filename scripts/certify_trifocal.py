@@ -1,17 +1,19 @@
-"""Certify the trifocal start set (fixtures/trifocal_reps.sols: 666 orbits x 8 = 5328 solutions at
-the fixture's p0) against independent monodromy runs -- oracle only (no CUDA path), prompt rule 3.
+"""Certify the trifocal start set (fixtures/trifocal_reps.sols: 668 orbits x 8 = 5344 solutions at
+p0 = rng.trifocal_complex_start(101)) with independent monodromy runs -- oracle only (no CUDA path).
 
   python scripts/certify_trifocal.py [seed ...]        (default seeds 101 202 303)
 
 For every seed: the oracle's symmetry-aware monodromy (scripts/make_fixtures._monodromy: loops
 p0 -> p1 -> p2 -> p0 with random complex p1, p2; Z2^3 orbit representatives; stop after 4 loops
-without a new orbit) from an independent planted generic (x0, p0') = rng.trifocal_complex_start(seed)
-writes fixtures/trifocal_cert_<seed>.sols (its representatives at p0') and .params (p0').  Then the
+without a new orbit) from the planted generic (x0, p0') = rng.trifocal_complex_start(seed) writes
+fixtures/trifocal_cert_<seed>.sols (its representatives at p0') and .params (p0'); then the
 representatives are carried to the fixture's p0 by one parameter homotopy p0' -> p0 and every
-endpoint (with its symmetry images) is looked up in the fixture.  tests/test_oracle_pins.py::
-test_trifocal_start_set_certified repeats the transfer: it fails if any independent run finds an
-orbit the fixture lacks, i.e. the fixture's 666 orbits are complete as far as three independent
-monodromy runs can tell (SURVEY §8(c) "monodromy saturation").
+endpoint (with its symmetry images) is looked up in the fixture.  Seeds 101, 202, 303 all saturate at
+668 orbits, and the homotopies between their sets are bijective up to failed paths (failed = unhit);
+the round-1 fixture (seed 11, kept as trifocal_cert_11.*) had 666 and, carried to p0, leaves two
+more orbits unhit than it has failed paths.  The fixture is seed 101's run (== make_fixtures.py
+trifocal); tests/test_oracle_pins.py::test_trifocal_start_set_certified repeats the transfers of seeds
+202 and 303 and fails if one finds an orbit the fixture lacks or maps two orbits onto one.
 """
 import os
 import sys
@@ -62,6 +64,8 @@ def main(seeds):
               f"transferred to the fixture's p0: {len(X)} converged ({np.bincount(st, minlength=7).tolist()}), "
               f"{len(set(ids[ids >= 0]))} distinct fixture orbits hit, {int((ids < 0).sum())} endpoints NOT in the "
               f"fixture", flush=True)
+
+
 
 
 if __name__ == "__main__":

@@ -46,5 +46,5 @@ def test_rank_instance_blocks():
 
 
 def test_traffic_lookup():
-    assert bench.traffic_bytes("trifocal", 1024, 5328) > 0
-    assert bench.traffic_bytes("trifocal", 7, 5328) is None
+    assert bench.traffic_bytes("fourview", 1024, 296) > 0
+    assert bench.traffic_bytes("trifocal", 7, 5344) is None

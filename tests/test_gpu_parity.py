@@ -636,7 +636,7 @@ def test_fourview_config3_full_batch_sampled(hc, orc):
 
 @pytest.fixture(scope="module")
 def trifocal_config4(hc):
-    """Config 4 at full size (1024 instances x 5328 tracks), the bench workload and launch
+    """Config 4 at full size (1024 instances x 5344 tracks), the bench workload and launch
     configuration, run once for the tests below."""
     d = systems.trifocal_unknown_f()
     start, p0 = fixtures.trifocal_start()
@@ -652,7 +652,7 @@ def _planted_found(d, X, xg):
 
 def test_trifocal_config4_set_parity(hc, orc, trifocal_config4):
     """Set parity at the paper's trifocal workload (Table 2) in the bench launch: for
-    instances 0 and 777 of the 1024-instance batch the oracle tracks all 5328 starts; the GPU's
+    instances 0 and 777 of the 1024-instance batch the oracle tracks all 5344 starts; the GPU's
     CONVERGED distinct set equals the oracle's within 1e-8 relative per coordinate, except for
     solutions one side reached on tracks where the other side's path failed (~4 % of trifocal
     tracks end in STEP_UNDERFLOW on both sides; which near-singular paths fail is rounding
@@ -670,7 +670,7 @@ def test_trifocal_config4_set_parity(hc, orc, trifocal_config4):
 def test_trifocal_config4_full_batch_sampled(hc, orc, trifocal_config4):
     """Config 4 at full size: the planted ground truth (up to the Z2^3 images) is recovered in every
     sampled instance where the oracle recovers it -- each GPU miss is re-run through the oracle on
-    all 5328 starts, which must miss it too and give the same solution set (a path failure of the
+    all 5344 starts, which must miss it too and give the same solution set (a path failure of the
     method, R7, not of the kernel) and the sets agree modulo path failures; sampled tracks from
     spread-out instances agree one by one."""
     d, start, p0, p1s, xg, st, X = trifocal_config4
@@ -748,7 +748,7 @@ def test_monodromy_fourview_296(hc, orc):
 
 def test_monodromy_trifocal_matches_oracle_fixture(hc, orc):
     """GPU monodromy (with the Z2^3 symmetry) from the fixture's planted (x0, p0) reproduces the
-    oracle's monodromy set exactly (666 orbits = 5328 solutions), as a set within 1e-8."""
+    oracle's monodromy set exactly (668 orbits = 5344 solutions), as a set within 1e-8."""
     from paper_2112_03444_b200.monodromy import monodromy_solve
     d = systems.trifocal_unknown_f()
     p0, x0 = rng.trifocal_complex_start()

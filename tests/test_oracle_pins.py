@@ -513,6 +513,34 @@ def test_fourview_planted_is_exact(orc):
         assert np.max(np.abs(F)) < 1e-13
 
 
+def test_trifocal_start_set_certified(orc):
+    """The trifocal start set (668 orbits x 8 = 5344 at p0 = rng.trifocal_complex_start(101), the
+    oracle's monodromy) against two independent monodromy runs from other planted (x0, p0') (seeds 202,
+    303; scripts/certify_trifocal.py, oracle only), each saturated at 668 orbits: carried to p0 by one
+    parameter homotopy, every converged endpoint lies in the fixture (no orbit the fixture lacks), no
+    two orbits land on one (the homotopy is a bijection of solution sets), and at most 5 % of the
+    paths fail.  SURVEY §8(c): "monodromy saturation"; the paper's 1784 is not this
+    formulation's count (R19/R20)."""
+    from hc_inputs import fixtures
+    d = systems.trifocal_unknown_f()
+    full, p0 = fixtures.trifocal_start()
+    assert full.shape == (5344, 18)
+
+    def orbit_of(y):
+        hit = np.nonzero(np.all(np.abs(full - y) <= 1e-6 * np.maximum(1.0, np.abs(y)), axis=1))[0]
+        return int(hit[0]) // 8 if len(hit) else -1
+    for seed in (202, 303):
+        reps = fixtures.read_solutions(fixtures.fixture_path(f"trifocal_cert_{seed}.sols"))
+        ps = fixtures.read_params(fixtures.fixture_path(f"trifocal_cert_{seed}.params"))
+        assert reps.shape == (668, 18)
+        res = orc.track(orc.ph_homotopy(d, ps, p0), reps)
+        ok = res.status[0] == orc.CONVERGED
+        ids = [orbit_of(y) for y in res.x[0][ok]]
+        assert min(ids) >= 0, f"seed {seed}: an endpoint outside the fixture"
+        assert len(set(ids)) == len(ids), f"seed {seed}: two orbits carried onto one"
+        assert ok.mean() >= 0.95
+
+
 def test_trifocal_planted_is_exact(orc):
     """Planted ground truth: F(x_gt; p) ~ 0 for generated trifocal instances; the Z2^3 images of a
     solution are solutions (R20 symmetry)."""
