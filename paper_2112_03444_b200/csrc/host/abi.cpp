@@ -366,8 +366,10 @@ static void fill_info(const CompiledSystem &cs, hc_system_info *o) {
   o->mono_levels = cs.n_levels;
   o->flops_eval_kernel = cs.flops_eval_kernel;
   o->flops_solve_kernel = cs.flops_solve_kernel;
-  o->smem_per_track =
-      (int64_t)slot_bytes(cs.N, cs.L * (hy_layout(cs.N) ? 2 : 1), cs.ncoef, cs.ncoef_src, cs.n_mono, cs.n_entries + 1);
+  // (the tracker keeps its per-lane state in shared memory when its CTA shape is 16 warps per SM)
+  const bool ss = tracker_maxw(cs.N, cs.L) * tracker_minb(cs.N) >= 16;
+  o->smem_per_track = (int64_t)slot_bytes(cs.N, ss ? cs.L * (hy_layout(cs.N) ? 2 : 1) : 0, cs.ncoef, cs.ncoef_src,
+                                          cs.n_mono, cs.n_entries + 1);
 }
 
 hc_status hc_system_info_get(hc_system sys, hc_system_info *o) {

@@ -60,6 +60,11 @@ struct TrackerShape {
   static constexpr int NC = HY ? 2 : 1;       // unknown components per lane
   static constexpr int MAXW = tracker_maxw(N, LW);
   static constexpr int MINB = tracker_minb(N);
+  // 128-register kernels (16 resident warps per SM) keep the RK / corrector vectors and the rarely
+  // touched per-track scalars in shared memory, the others (N >= 17: 168 registers) in registers,
+  // where the shared memory would only shrink the L1 that serves the coefficient tables
+  static constexpr bool SMEM_STATE = MAXW * MINB >= 16;
+  static constexpr int LNC = SMEM_STATE ? L * NC : 0;   // per-lane state words in the slot (layout.h)
 };
 
 __device__ __forceinline__ double2 cmul(double2 a, double2 b) {
@@ -780,16 +785,18 @@ __device__ __forceinline__ void track_body(const TrackArgs &A) {
   const int seg = lane / L, r = lane % L;
   const int slot = warp * TPW + seg;
   const int ncoef = A.ncoef, D = A.D;
-  unsigned char *sb = slots_base + (size_t)slot * slot_bytes(N, L * NC, ncoef, A.ncoef_src, A.n_mono, A.n_entries + 1);
+  constexpr bool SS = TrackerShape<N, LW>::SMEM_STATE;
+  constexpr int LNC = TrackerShape<N, LW>::LNC;
+  unsigned char *sb = slots_base + (size_t)slot * slot_bytes(N, LNC, ncoef, A.ncoef_src, A.n_mono, A.n_entries + 1);
   EgSample *egs = reinterpret_cast<EgSample *>(sb);   // endgame sampling state (R26), lane 0 writes
-  double2 *vstate = reinterpret_cast<double2 *>(sb + EG_SAMPLE_BYTES);   // [3][NC][L]
+  double2 *vstate = reinterpret_cast<double2 *>(sb + EG_SAMPLE_BYTES);   // [3][NC][L] (SS only)
   // per-lane copies of the slot's rarely touched scalars (structure of arrays, conflict-free): track
-  // id, step size, step / rejection / Newton / consecutive-accept counters -- in shared memory, so the
-  // loop's register budget (128 for N <= 16) goes to the rows being eliminated
-  long long *s_g = reinterpret_cast<long long *>(vstate + 3 * NC * L);
-  double *s_dt = reinterpret_cast<double *>(s_g + NC * L);   // [4][NC * L]: dt, h, t1, cval_t
-  int *s_cnt = reinterpret_cast<int *>(s_dt + 4 * NC * L);   // [4][NC * L]: steps, rej, newt, acc
-  double2 *cval = vstate + 7 * NC * L;
+  // id, step size, step / rejection / Newton / consecutive-accept counters -- in shared memory for the
+  // 128-register kernels, so their register budget goes to the rows being eliminated (SS only)
+  long long *s_g = reinterpret_cast<long long *>(vstate + 3 * LNC);
+  double *s_dt = reinterpret_cast<double *>(s_g + LNC);   // [4][LNC]: dt, h, t1, cval_t
+  int *s_cnt = reinterpret_cast<int *>(s_dt + 4 * LNC);   // [4][LNC]: steps, rej, newt, acc
+  double2 *cval = vstate + 7 * LNC;
   double2 *mono = cval + ncoef + A.ncoef_src;
   double2 *M = mono + A.n_mono;
   double2 *prow = M + A.n_entries + 1;
@@ -805,33 +812,37 @@ __device__ __forceinline__ void track_body(const TrackArgs &A) {
 
   // ---- slot state (replicated over the slot's lanes) ----
   int state = ST_DONE;
-  long long &g = s_g[r];
+  long long g_r = -1;
+  long long &g = SS ? s_g[SS ? r : 0] : g_r;
   g = -1;
   const double2 *ct = A.coef_t;   // instance coefficient table
   double t = 0.0;
-  double &dt = s_dt[r], &h = s_dt[NC * L + r], &t1 = s_dt[2 * NC * L + r];
+  double dt_r = 0.0, h_r = 0.0, t1_r = 0.0, cval_t_r = -1.0;
+  int steps_r = 0, rej_r = 0, newt_r = 0, acc_r = 0;
+  double &dt = SS ? s_dt[r] : dt_r, &h = SS ? s_dt[LNC + r] : h_r, &t1 = SS ? s_dt[2 * LNC + r] : t1_r;
   h = t1 = 0.0;
-  int &steps = s_cnt[0 * NC * L + r], &rej = s_cnt[1 * NC * L + r], &newt = s_cnt[2 * NC * L + r],
-      &acc = s_cnt[3 * NC * L + r];
+  int &steps = SS ? s_cnt[0 * LNC + r] : steps_r, &rej = SS ? s_cnt[1 * LNC + r] : rej_r,
+      &newt = SS ? s_cnt[2 * LNC + r] : newt_r, &acc = SS ? s_cnt[3 * LNC + r] : acc_r;
   dt = 0.0;
   acc = steps = rej = newt = 0;
   int stage = 0, it = 0, solves = 0;
   // component c of lane r is unknown r (c = 0) or 16 + r (c = 1, hybrid layout, r < E)
-  // x stays in registers; the RK accumulators and the corrector's point live in the slot's shared
-  // memory ([kacc | kprev | xc][NC][L], one conflict-free 16-byte word per lane): they are touched a
-  // few times per iteration, and the registers they free keep the N <= 16 kernels within 128
-  double2 x[NC];
-  auto KACC = [&](int c) -> double2 & { return vstate[(0 * NC + c) * L + r]; };
-  auto KPREV = [&](int c) -> double2 & { return vstate[(1 * NC + c) * L + r]; };
-  auto XC = [&](int c) -> double2 & { return vstate[(2 * NC + c) * L + r]; };
+  // x stays in registers; in the 128-register kernels (SS) the RK accumulators and the corrector's
+  // point live in the slot's shared memory ([kacc | kprev | xc][NC][L], one conflict-free 16-byte word
+  // per lane): they are touched a few times per iteration, and the registers they free keep the
+  // N <= 16 kernels within 128
+  double2 x[NC], kacc_r[NC], kprev_r[NC], xc_r[NC];
+  auto KACC = [&](int c) -> double2 & { return SS ? vstate[(0 * NC + c) * L + r] : kacc_r[c]; };
+  auto KPREV = [&](int c) -> double2 & { return SS ? vstate[(1 * NC + c) * L + r] : kprev_r[c]; };
+  auto XC = [&](int c) -> double2 & { return SS ? vstate[(2 * NC + c) * L + r] : xc_r[c]; };
 #pragma unroll
   for (int c = 0; c < NC; ++c) x[c] = KACC(c) = KPREV(c) = XC(c) = make_double2(0.0, 0.0);
   auto comp_valid = [&](int c) -> bool { return c == 0 ? (r < N) : (r < E); };
   auto comp_row = [&](int c) -> int { return c == 0 ? r : 16 + r; };
   bool need_track = true;
   bool fresh_k1 = false;   // the last solve was a successful RK stage 1 (endgame sampling)
-  double &cval_t = s_dt[3 * NC * L + r];   // t at which the slot's coefficient values were last evaluated
-  cval_t = -1.0;                           // (-1: none)
+  double &cval_t = SS ? s_dt[3 * LNC + r] : cval_t_r;   // t at which the slot's coefficient values were
+  cval_t = -1.0;                                        // last evaluated (-1: none)
 #ifdef HCB_PHASE_TIMING
   unsigned long long hcb_phase[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   long long hcb_iter0 = clock64();
@@ -1148,7 +1159,7 @@ cudaError_t launch_tracker_n(const TrackArgs &A, int device, cudaStream_t stream
   constexpr int TPW = 32 / L;
   const size_t tables = table_bytes(A.Q, L, A.n_mono - (N + 1), N) + align16((size_t)2 * A.n_entries);
   const size_t per_warp =
-      (size_t)TPW * slot_bytes(N, L * TrackerShape<N, LW>::NC, A.ncoef, A.ncoef_src, A.n_mono, A.n_entries + 1);
+      (size_t)TPW * slot_bytes(N, TrackerShape<N, LW>::LNC, A.ncoef, A.ncoef_src, A.n_mono, A.n_entries + 1);
   int smem_max = 0;
   cudaDeviceGetAttribute(&smem_max, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
   int warps = TrackerShape<N, LW>::MAXW;
