@@ -284,6 +284,9 @@ def run_ours(args):
     S, N = start.shape
     info = sysh.info
     st = hc.hc_tracker_settings_default()
+    if args.config in ("trifocal", "fourview", "fivepoint", "p3p"):   # sharded multi-instance job: pinned layout
+        from paper_2112_03444_b200.distributed import sharded_settings
+        st = sharded_settings(st)
     x_start = torch.from_numpy(start).to(dev)
     t_p0 = torch.from_numpy(np.ascontiguousarray(p0)).to(dev)
     t_p1 = torch.from_numpy(np.ascontiguousarray(p1s)).to(dev)

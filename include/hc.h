@@ -24,8 +24,11 @@
  *    thread-local message for the last failing call.  A per-track numerical failure is
  *    never an error: it is reported in the track's status ("the batch call never fails
  *    wholesale").
- *  - Determinism: a track's arithmetic depends only on its inputs, never on scheduling,
- *    batch size or GPU count: identical inputs give identical output bits.
+ *  - Determinism: a track's arithmetic depends only on its inputs and the lane layout, never on
+ *    scheduling, CTA shape, batch size or GPU count: identical inputs in the same layout give
+ *    identical output bits.  For N <= 16 the default layout choice (HC_LAYOUT_AUTO) depends on
+ *    the batch size, so a sharded job pins hc_tracker_settings.lane_layout to get the same bits
+ *    for every shard size (paper_2112_03444_b200.distributed does).
  */
 #ifndef HC_H
 #define HC_H
@@ -63,6 +66,7 @@ typedef enum {
 
 typedef enum { HC_RK4 = 0, HC_EULER = 1 } hc_predictor;
 typedef enum { HC_MEM_DEVICE = 0, HC_MEM_HOST = 1 } hc_memory;
+typedef enum { HC_LAYOUT_AUTO = 0, HC_LAYOUT_THROUGHPUT = 1, HC_LAYOUT_WIDE = 2 } hc_lane_layout;
 
 typedef struct hc_system_s *hc_system;  /* opaque, library-owned */
 typedef struct hc_result_s *hc_result;  /* opaque, library-owned */
@@ -177,6 +181,13 @@ typedef struct {
   int32_t eg_max_winding; /* (8) */
   int32_t eg_max_radii; /* (12) */
   double eg_tol;        /* (1e-10) */
+  /* Lane layout of the tracker kernel for N <= 16 (a launch choice; results agree as solution
+   * sets, bits may differ between layouts because the op list is balanced over a different number
+   * of lanes): HC_LAYOUT_AUTO picks by batch size (see hc_track_batch), HC_LAYOUT_THROUGHPUT /
+   * HC_LAYOUT_WIDE pin it, so a job sharded over GPUs gives the same bits for any shard size.
+   * Ignored for N > 16 (one layout).  The environment variable HC_LANES=wide|narrow overrides
+   * HC_LAYOUT_AUTO only. */
+  int32_t lane_layout;  /* hc_lane_layout (HC_LAYOUT_AUTO) */
 } hc_tracker_settings;
 hc_status hc_tracker_settings_default(hc_tracker_settings *out);
 
@@ -210,8 +221,9 @@ typedef struct {
  * because the op list is balanced over a different number of lanes): for N <= 16 a batch of at
  * most ~2.5 waves of one-track-per-warp slots runs in the wide latency layout (32 lanes per track,
  * e.g. single-instance katsura-6 / cyclic-7 solves), larger batches in the throughput layout
- * (next_pow2(N) lanes per track, 32 / that tracks per warp).  Environment HC_LANES=wide|narrow
- * overrides the choice; hc_result_launch reports it. */
+ * (next_pow2(N) lanes per track, 32 / that tracks per warp).  settings->lane_layout pins the
+ * choice; with HC_LAYOUT_AUTO the environment HC_LANES=wide|narrow overrides it; hc_result_launch
+ * reports it. */
 hc_status hc_track_batch(hc_system sys, const hc_tracker_settings *settings, const hc_batch *batch,
                          hc_result *out);
 /* Block until the batch finished. */

@@ -16,6 +16,7 @@ HC_CONVERGED, HC_DIVERGED, HC_STEP_UNDERFLOW, HC_MAX_STEPS, HC_SINGULAR, HC_NONF
 STATUS_NAMES = ["CONVERGED", "DIVERGED", "STEP_UNDERFLOW", "MAX_STEPS", "SINGULAR", "NONFINITE", "AT_INFINITY"]
 HC_RK4, HC_EULER = 0, 1
 HC_MEM_DEVICE, HC_MEM_HOST = 0, 1
+HC_LAYOUT_AUTO, HC_LAYOUT_THROUGHPUT, HC_LAYOUT_WIDE = 0, 1, 2
 
 EXPORTED = [
     "hc_system_create", "hc_system_create_total_degree", "hc_total_degree_params", "hc_total_degree_count",
@@ -59,7 +60,8 @@ class hc_tracker_settings(C.Structure):
                 ("pivot_rel", C.c_double), ("eg_start", C.c_double), ("eg_inf_mu", C.c_double),
                 ("eg_sing_mu", C.c_double), ("eg_stab", C.c_double), ("eg_inf_s", C.c_double),
                 ("eg_inf_norm", C.c_double), ("eg_samples", C.c_int32), ("eg_max_winding", C.c_int32),
-                ("eg_max_radii", C.c_int32), ("eg_tol", C.c_double)]
+                ("eg_max_radii", C.c_int32), ("eg_tol", C.c_double),
+                ("lane_layout", C.c_int32)]
 
 
 class hc_batch(C.Structure):

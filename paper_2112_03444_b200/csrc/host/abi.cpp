@@ -199,6 +199,7 @@ hc_status hc_tracker_settings_default(hc_tracker_settings *s) {
   s->eg_max_winding = 8;
   s->eg_max_radii = 12;
   s->eg_tol = 1e-10;
+  s->lane_layout = HC_LAYOUT_AUTO;
   return HC_OK;
 }
 
@@ -464,6 +465,7 @@ static hc_status check_settings(const hc_tracker_settings &s) {
                            !(s.eg_tol > 0) || !(s.eg_inf_s >= 0) || !(s.eg_inf_norm > 0) || !(s.eg_sing_mu > 0) ||
                            !(s.eg_inf_mu < 0)))
     return fail(HC_E_INVALID_ARG, "endgame settings");
+  if (s.lane_layout < HC_LAYOUT_AUTO || s.lane_layout > HC_LAYOUT_WIDE) return fail(HC_E_INVALID_ARG, "lane_layout");
   return HC_OK;
 }
 
@@ -474,7 +476,9 @@ static bool aligned16(const void *p) { return (reinterpret_cast<uintptr_t>(p) & 
 // shape as its __launch_bounds__: 16 for N <= 16), i.e.
 // small single-instance solves (katsura-6: 64 tracks, cyclic-7: 5040), where the makespan is one
 // track's chain of solves and spreading its op list over 32 lanes shortens every solve.
-static bool wide_layout(int device, int N, int64_t tracks) {
+static bool wide_layout(int device, int N, int64_t tracks, int32_t layout) {
+  if (layout == HC_LAYOUT_WIDE) return true;
+  if (layout == HC_LAYOUT_THROUGHPUT) return false;
   if (const char *ev = getenv("HC_LANES")) {
     if (!strcmp(ev, "wide")) return true;
     if (!strcmp(ev, "narrow")) return false;
@@ -513,7 +517,7 @@ static hc_status track_batch_impl(hc_system sys, const hc_tracker_settings *sett
   // ---- lane layout: the wide latency layout (one track per warp, 32 lanes) when the batch
   //      under-fills the GPU in the throughput layout (policy in wide_layout()); HC_LANES=wide|narrow
   //      overrides it (experiments and tests) ----
-  const bool wide = sys->has_wide && wide_layout(sys->device, N, bt->n_instances * bt->n_start);
+  const bool wide = sys->has_wide && wide_layout(sys->device, N, bt->n_instances * bt->n_start, st.lane_layout);
   const CompiledSystem &cs = wide ? sys->cs_w : sys->cs;
   const DevTables &dt = wide ? sys->dt_w : sys->dt;
   if (!bt->start_x) return fail(HC_E_INVALID_ARG, "start_x is null");

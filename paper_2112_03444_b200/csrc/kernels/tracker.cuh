@@ -271,6 +271,9 @@ __device__ __forceinline__ int seg_argmax(double v, int r, double &vmax) {
 // Returns the solution component y_r in lane r and a slot-uniform success flag.
 // prow: 2 * (N + 1) double2 (per slot shared memory).
 // ------------------------------------------------------------------------------------------
+#ifndef HCB_LU_PIPE   // software-pipelined column schedule (A/B switch; 0 = the round-1 order)
+#define HCB_LU_PIPE 0
+#endif
 template <int N, int L>
 __device__ __forceinline__ bool lu_rows(double2 (&a)[N + 1], int r, int seg, double2 *prow,
                                         double pivot_rel, double lane_max, double2 &y) {
@@ -287,6 +290,61 @@ __device__ __forceinline__ bool lu_rows(double2 (&a)[N + 1], int r, int seg, dou
   if (!(v0 >= 0.0)) v0 = -1.0;   // NaN is never a pivot
   int p = seg_argmax_thr<L>(v0, r, thr, sing);
   double2 spec = crecip(a[0]);   // speculative 1/a_rk of this lane's candidate (overlaps the search)
+#if HCB_LU_PIPE
+  // Software-pipelined order (same arithmetic, same pivots): the dependency chain of a column is
+  // multiplier -> column k+1 -> |a|^2 -> arg-max -> shuffles of 1/pivot and the next pivot row's
+  // column k+2; the trailing update of columns k+3..N does not feed it, so it is issued after the
+  // next column's shuffles (their latency hides under it) and the next pivot lane publishes its
+  // row after it.  (The round-1 order ran the whole trailing update between the arg-max and the
+  // shuffles, putting its issue time on every column's chain.)
+  double2 inv = shfl2(spec, p, L);
+  double2 u1 = shfl2(a[1], p, L);
+  if (r == p) {   // pivot row of step 0: columns 2..N through shared memory
+#pragma unroll
+    for (int j = 2; j <= N; ++j) prow[j] = a[j];
+    used = true;
+    mystep = 0;
+    myinv = spec;
+  }
+  __syncwarp();
+#pragma unroll
+  for (int k = 0; k < N; ++k) {
+    const double2 *pr = prow + (k & 1) * (N + 1);         // pivot row of step k (columns k+2..N)
+    double2 *pn = prow + ((k + 1) & 1) * (N + 1);         // pivot row of step k+1 (columns k+3..N)
+    const bool me = (r == p);
+    const double2 lc = cmul(a[k], inv);
+    const double2 l = me ? make_double2(0.0, 0.0) : lc;
+    a[k + 1] = cfms(a[k + 1], l, u1);   // column k+1 (k + 1 == N: the right-hand side)
+    if (k + 1 < N) {
+      a[k + 2] = cfms(a[k + 2], l, pr[k + 2]);   // column k+2: the next pivot row's broadcast needs it
+      double v = abs2(a[k + 1]);
+      if (used || (L < 32 && !(v >= 0.0))) v = -1.0;   // NaN is never a pivot (the REDUX path excludes it itself)
+      spec = crecip(a[k + 1]);
+      p = seg_argmax_thr<L>(v, r, thr, sing);
+      inv = shfl2(spec, p, L);
+      u1 = shfl2(a[k + 2], p, L);
+      // trailing update of step k, columns k+3..N, in chunks of 4 (loads before their FMAs)
+#pragma unroll
+      for (int j0 = k + 3; j0 <= N; j0 += 4) {
+        double2 u[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+          if (j0 + i <= N) u[i] = pr[j0 + i];
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+          if (j0 + i <= N) a[j0 + i] = cfms(a[j0 + i], l, u[i]);
+      }
+      if (r == p) {   // the pivot lane of step k+1 publishes columns k+3..N of its (now updated) row
+#pragma unroll
+        for (int j = k + 3; j <= N; ++j) pn[j] = a[j];
+        used = true;
+        mystep = k + 1;
+        myinv = spec;
+      }
+      __syncwarp();   // the published row is visible (and pr's readers are done before it is reused)
+    }
+  }
+#else
 #pragma unroll
   for (int k = 0; k < N; ++k) {
     double2 *pr = prow + (k & 1) * (N + 1);
@@ -327,6 +385,7 @@ __device__ __forceinline__ bool lu_rows(double2 (&a)[N + 1], int r, int seg, dou
       }
     }
   }
+#endif
   __syncwarp();
   // ---- the system is now diagonal in pivot order: x_{mystep} = b' / pivot, routed through shared memory ----
   double2 *xsol = prow;

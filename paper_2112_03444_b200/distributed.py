@@ -20,6 +20,16 @@ def shard_range(n_total: int, rank: int, world: int) -> tuple[int, int]:
     return lo, hi
 
 
+def sharded_settings(st):
+    """Tracker settings for a job sharded over GPUs: the lane layout pinned to the throughput layout
+    when left on HC_LAYOUT_AUTO (whose choice depends on the batch size for N <= 16), so every track
+    gives the same bits for any shard size or GPU count (include/hc.h, Determinism)."""
+    from . import hc
+    if st.lane_layout == hc.HC_LAYOUT_AUTO:
+        st.lane_layout = hc.HC_LAYOUT_THROUGHPUT
+    return st
+
+
 def env_rank_world() -> tuple[int, int, int]:
     """(rank, local_rank, world_size) from the torchrun environment (1 process when unset)."""
     return (int(os.environ.get("RANK", 0)), int(os.environ.get("LOCAL_RANK", 0)),

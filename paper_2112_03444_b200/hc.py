@@ -14,7 +14,7 @@ import numpy as np
 
 from . import _lib as L
 from ._lib import (HC_AT_INFINITY, HC_CONVERGED, HC_DIVERGED, HC_EULER, HC_MAX_STEPS, HC_MEM_DEVICE,  # noqa: F401
-                   HC_MEM_HOST,
+                   HC_MEM_HOST, HC_LAYOUT_AUTO, HC_LAYOUT_THROUGHPUT, HC_LAYOUT_WIDE,
                    HC_NONFINITE, HC_RK4, HC_SINGULAR, HC_STEP_UNDERFLOW, STATUS_NAMES, HCError, check)
 
 

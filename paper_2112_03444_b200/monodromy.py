@@ -8,8 +8,8 @@ hc_track_batch call on the fused kernel); endpoints back at p0 that are new are 
 `symmetry(x) -> list of solutions` (a group action that commutes with the homotopy, e.g.
 hc_inputs.systems.trifocal_symmetry) lets only one representative per orbit be tracked.
 
-Host orchestration only: every path is tracked by libhc.so; deduplication (reading R11) is host
-post-processing.
+Host orchestration only: every path is tracked by libhc.so; deduplication (reading R11) is the
+library's host post-processing (hc_solutions: greedy matching in order against the known points).
 """
 from __future__ import annotations
 
@@ -29,10 +29,14 @@ class MonodromyResult:
     history: list = field(default_factory=list)   # known count after each loop
 
 
-def _contains(S: np.ndarray, y: np.ndarray, tol: float) -> bool:
-    if S.shape[0] == 0:
-        return False
-    return bool(np.any(np.all(np.abs(S - y) <= tol * np.maximum(1.0, np.abs(y)), axis=1)))
+def _new_points(known: np.ndarray, X: np.ndarray, tol: float) -> list:
+    """Indices of the rows of X that match neither a known point nor an earlier row of X (reading
+    R11, through hc_solutions on [known; X]: a row is new when it is kept as its own representative)."""
+    if X.shape[0] == 0:
+        return []
+    n = known.shape[0]
+    _, _, _, rep = hc.solutions(np.concatenate([known, X]) if n else X, None, tol=tol)
+    return [i for i in range(X.shape[0]) if rep[n + i] == n + i]
 
 
 def monodromy_solve(system: "hc.System", x0, p0, *, symmetry=None, max_loops: int = 60, stall_loops: int = 4,
@@ -67,11 +71,16 @@ def monodromy_solve(system: "hc.System", x0, p0, *, symmetry=None, max_loops: in
             X = res.x.cpu().numpy()[0][ok]
             res.close()
         new = 0
-        for y in X:
-            if not _contains(known, y, tol):
-                reps.append(y)
-                known = np.concatenate([known, np.array(orbit(y), dtype=np.complex128)])
-                new += 1
+        added = np.zeros((0, known.shape[1]), dtype=np.complex128)   # orbits added in this loop
+        for i in _new_points(known, X, tol):
+            y = X[i]
+            if added.shape[0] and not _new_points(added, y[None], tol):
+                continue   # in the orbit of a point added earlier in this loop
+            reps.append(y)
+            orb = np.array(orbit(y), dtype=np.complex128)
+            known = np.concatenate([known, orb])
+            added = np.concatenate([added, orb])
+            new += 1
         hist.append(int(known.shape[0]))
         stall = stall + 1 if new == 0 else 0
         if stall >= stall_loops or (target is not None and known.shape[0] >= target):

@@ -41,6 +41,15 @@ def test_settings_defaults_match_readings(hc):
     s = hc.hc_tracker_settings_default()
     assert (s.predictor, s.dt_init, s.dt_min, s.dt_max, s.grow_after, s.grow, s.shrink) == (0, 0.01, 1e-14, 0.1, 4, 2.0, 0.5)
     assert (s.max_newton, s.newton_tol, s.max_steps, s.inf_norm, s.end_newton) == (3, 1e-8, 10000, 1e14, 3)
+    assert s.lane_layout == hc.HC_LAYOUT_AUTO
+
+
+def test_sharded_settings_pin_the_lane_layout(hc):
+    """A sharded job pins the lane layout (the auto choice depends on the batch size for N <= 16,
+    include/hc.h Determinism); an out-of-range layout is rejected by the C ABI."""
+    from paper_2112_03444_b200.distributed import sharded_settings
+    assert sharded_settings(hc.hc_tracker_settings_default()).lane_layout == hc.HC_LAYOUT_THROUGHPUT
+    assert sharded_settings(hc.settings(lane_layout=hc.HC_LAYOUT_WIDE)).lane_layout == hc.HC_LAYOUT_WIDE
 
 
 def mono_factors(prog, N):
@@ -229,3 +238,17 @@ def test_solutions_post_processing_matches_oracle(hc, orc):
     assert np.array_equal(real, orc.is_real(A))
     assert np.all(rep[status != 0] == -1) and np.all(rep[status == 0] >= 0)
     assert hc.solutions(X[:0])[0].shape == (0, N)   # empty instance
+
+
+def test_monodromy_matching_goes_through_hc_solutions(hc):
+    """monodromy._new_points (R11 matching of loop endpoints against the known set) is the library's
+    hc_solutions: points within the tolerance of a known point or of an earlier new point are not new."""
+    from paper_2112_03444_b200.monodromy import _new_points
+    g = rng.gen(9)
+    known = g.standard_normal((20, 4)) + 1j * g.standard_normal((20, 4))
+    fresh = g.standard_normal((3, 4)) + 1j * g.standard_normal((3, 4))
+    X = np.concatenate([known[[4, 7]] * (1 + 1e-9), fresh[[0]], fresh[[0]] * (1 + 1e-10), fresh[[1]],
+                        known[[2]] * (1 + 1e-3)])
+    assert _new_points(known, X, 1e-6) == [2, 4, 5]
+    assert _new_points(known[:0], X[:2], 1e-6) == [0, 1]
+    assert _new_points(known, X[:0], 1e-6) == []
