@@ -15,8 +15,13 @@ __host__ __device__ inline size_t align16(size_t b) { return (b + 15) & ~size_t(
 // M[n_entries] (non-zero entries of [dH/dx | rhs]), prow[2 * (N + 1)] (double-buffered pivot row),
 // rabs[N] (doubles).
 constexpr size_t EG_SAMPLE_BYTES = 80;
+// Output staging per slot (OutStage): the chunk bookkeeping and the small per-track outputs (status,
+// winding, counters, residuals: 40 bytes per track) of the slot's current chunk of OUT_CHUNK
+// consecutive tracks, written to global memory as whole 32-byte sectors when the chunk is done.
+constexpr int OUT_CHUNK = 8;
+constexpr size_t OUT_STAGE_BYTES = 32 + (size_t)OUT_CHUNK * 40;
 __host__ __device__ inline size_t slot_bytes(int N, int lnc, int ncoef, int ncoef_src, int n_mono, int n_entries) {
-  return EG_SAMPLE_BYTES +
+  return EG_SAMPLE_BYTES + OUT_STAGE_BYTES +
          align16(sizeof(double) * 2 * ((size_t)7 * lnc + ncoef + ncoef_src + n_mono + n_entries + 2 * (N + 1)) +
                  sizeof(double) * N);
 }
