@@ -203,20 +203,29 @@ hc_status hc_tracker_settings_default(hc_tracker_settings *s) {
   return HC_OK;
 }
 
+// The op table, the monomial program and the entry map are staged into shared memory by the tracker
+// with 1-D bulk async copies (cp.async.bulk, 16-byte granules): each device copy is zero-padded to
+// a multiple of 16 bytes (the padded bytes land in the shared-memory alignment padding).
+static hc_status upload_padded16(void **dst, const void *src, size_t bytes) {
+  const size_t padded = std::max<size_t>(16, (bytes + 15) & ~size_t(15));
+  std::vector<unsigned char> buf(padded, 0);
+  if (bytes) std::memcpy(buf.data(), src, bytes);
+  CK(cudaMalloc(dst, padded));
+  CK(cudaMemcpy(*dst, buf.data(), padded, cudaMemcpyHostToDevice));
+  return HC_OK;
+}
+
 static hc_status upload_tables(const CompiledSystem &cs, DevTables &t) {
-  CK(cudaMalloc(&t.d_ops, sizeof(uint2) * std::max<size_t>(1, cs.ops.size())));
-  CK(cudaMalloc(&t.d_mono_prog, sizeof(uint32_t) * std::max<size_t>(1, cs.mono_prog.size())));
+  hc_status s = upload_padded16((void **)&t.d_ops, cs.ops.data(), sizeof(uint2) * cs.ops.size());
+  if (s == HC_OK) s = upload_padded16((void **)&t.d_mono_prog, cs.mono_prog.data(), sizeof(uint32_t) * cs.mono_prog.size());
   // device copy of the entry map: structural zeros point at the extra always-zero entry n_entries
   std::vector<int16_t> mp(cs.mpos);
   for (auto &v : mp)
     if (v < 0) v = (int16_t)cs.n_entries;
-  CK(cudaMalloc(&t.d_mpos, sizeof(int16_t) * mp.size()));
-  CK(cudaMemcpy(t.d_mpos, mp.data(), sizeof(int16_t) * mp.size(), cudaMemcpyHostToDevice));
+  if (s == HC_OK) s = upload_padded16((void **)&t.d_mpos, mp.data(), sizeof(int16_t) * mp.size());
+  if (s != HC_OK) return s;
   CK(cudaMalloc(&t.d_mono, sizeof(CoefMono) * std::max<size_t>(1, cs.mono.size())));
   CK(cudaMalloc(&t.d_mono_ptr, sizeof(int32_t) * cs.mono_ptr.size()));
-  if (!cs.ops.empty()) CK(cudaMemcpy(t.d_ops, cs.ops.data(), sizeof(uint2) * cs.ops.size(), cudaMemcpyHostToDevice));
-  if (!cs.mono_prog.empty())
-    CK(cudaMemcpy(t.d_mono_prog, cs.mono_prog.data(), sizeof(uint32_t) * cs.mono_prog.size(), cudaMemcpyHostToDevice));
   if (!cs.mono.empty())
     CK(cudaMemcpy(t.d_mono, cs.mono.data(), sizeof(CoefMono) * cs.mono.size(), cudaMemcpyHostToDevice));
   CK(cudaMemcpy(t.d_mono_ptr, cs.mono_ptr.data(), sizeof(int32_t) * cs.mono_ptr.size(), cudaMemcpyHostToDevice));
@@ -369,7 +378,8 @@ static void fill_info(const CompiledSystem &cs, hc_system_info *o) {
   o->flops_solve_kernel = cs.flops_solve_kernel;
   // (the tracker keeps its per-lane state in shared memory when its CTA shape is 16 warps per SM)
   const bool ss = tracker_maxw(cs.N, cs.L) * tracker_minb(cs.N) >= 16;
-  o->smem_per_track = (int64_t)slot_bytes(cs.N, ss ? cs.L * (hy_layout(cs.N) ? 2 : 1) : 0, cs.ncoef, cs.ncoef_src,
+  o->smem_per_track = (int64_t)slot_bytes(cs.N, ss ? state_lanes(cs.N, cs.L, hy_layout(cs.N) && cs.L == lanes_for(cs.N) ? 2 : 1) : 0,
+                                          cs.ncoef, cs.ncoef_src,
                                           cs.n_mono, cs.n_entries + 1);
 }
 

@@ -28,6 +28,7 @@
 
 #include "../hc_internal.h"
 #include "layout.h"
+#include "bulk.cuh"
 
 namespace hcb {
 
@@ -68,7 +69,8 @@ struct TrackerShape {
 #else
   static constexpr bool SMEM_STATE = MAXW * MINB >= 16;
 #endif
-  static constexpr int LNC = SMEM_STATE ? L * NC : 0;   // per-lane state words in the slot (layout.h)
+  static constexpr int LNC = SMEM_STATE ? state_lanes(N, L, NC) : 0;   // state lanes in the slot (layout.h)
+  static constexpr int LV = SMEM_STATE ? LNC / NC : 1;                 // ... per unknown component
 };
 
 __device__ __forceinline__ double2 cmul(double2 a, double2 b) {
@@ -849,15 +851,24 @@ __device__ __forceinline__ void track_body(const TrackArgs &A) {
   constexpr int TPW = 32 / L;
   extern __shared__ __align__(16) unsigned char smem_raw[];
 
-  // ---- stage the op table and the monomial program in shared memory (constant for the kernel) ----
+  // ---- stage the op table, the monomial program and the entry map in shared memory (constant for
+  //      the kernel) with bulk async copies (TMA engine, 1-D; the device copies are zero-padded to
+  //      16-byte multiples by the host), completed on an mbarrier ----
+  __shared__ __align__(8) unsigned long long tables_bar;
   uint2 *ops_s = reinterpret_cast<uint2 *>(smem_raw);
   const int nops = A.Q * L;
-  for (int i = threadIdx.x; i < nops; i += blockDim.x) ops_s[i] = __ldg(&A.ops[i]);
   const int nprog = A.n_mono - (N + 1);
   uint32_t *prog_s = reinterpret_cast<uint32_t *>(smem_raw + align16((size_t)8 * nops));
-  for (int i = threadIdx.x; i < nprog; i += blockDim.x) prog_s[i] = __ldg(&A.mono_prog[i]);
   int16_t *mpos_s = reinterpret_cast<int16_t *>(smem_raw + align16((size_t)8 * nops) + align16((size_t)4 * nprog));
-  for (int i = threadIdx.x; i < N * (N + 1); i += blockDim.x) mpos_s[i] = __ldg(&A.mpos[i]);
+  if (threadIdx.x == 0) {
+    const unsigned b_ops = (unsigned)align16((size_t)8 * nops), b_prog = (unsigned)align16((size_t)4 * nprog),
+                   b_mpos = (unsigned)align16((size_t)2 * N * (N + 1));
+    mbar_init(&tables_bar, 1);
+    mbar_arrive_expect_tx(&tables_bar, b_ops + b_prog + b_mpos);
+    if (b_ops) bulk_copy_g2s(ops_s, A.ops, b_ops, &tables_bar);
+    if (b_prog) bulk_copy_g2s(prog_s, A.mono_prog, b_prog, &tables_bar);
+    bulk_copy_g2s(mpos_s, A.mpos, b_mpos, &tables_bar);
+  }
   unsigned char *slots_base = smem_raw + table_bytes(A.Q, L, nprog, N) + align16((size_t)2 * A.n_entries);
   // compact entry -> row (for the relative residual of rhs entries)
   int16_t *row_of = reinterpret_cast<int16_t *>(smem_raw + table_bytes(A.Q, L, nprog, N));
@@ -873,14 +884,15 @@ __device__ __forceinline__ void track_body(const TrackArgs &A) {
   unsigned char *sb = slots_base + (size_t)slot * slot_bytes(N, LNC, ncoef, A.ncoef_src, A.n_mono, A.n_entries + 1);
   EgSample *egs = reinterpret_cast<EgSample *>(sb);   // endgame sampling state (R26), lane 0 writes
   OutStage *os = reinterpret_cast<OutStage *>(sb + EG_SAMPLE_BYTES);   // chunk + staged outputs (lane 0 writes)
-  double2 *vstate = reinterpret_cast<double2 *>(sb + EG_SAMPLE_BYTES + OUT_STAGE_BYTES);   // [3][NC][L] (SS only)
-  // per-lane copies of the slot's rarely touched scalars (structure of arrays, conflict-free): track
-  // id, step size, step / rejection / Newton / consecutive-accept counters -- in shared memory for the
-  // 128-register kernels, so their register budget goes to the rows being eliminated (SS only)
+  double2 *vstate = reinterpret_cast<double2 *>(sb + EG_SAMPLE_BYTES + OUT_STAGE_BYTES);   // [3][NC][LV] (SS only)
+  // one copy of the slot's rarely touched scalars (track id, step size, h, t1, the t of the cached
+  // coefficients, step / rejection / Newton / consecutive-accept counters; every lane of the slot
+  // reads and writes the same values) -- in shared memory for the 128-register kernels, so their
+  // register budget goes to the rows being eliminated (SS only)
   long long *s_g = reinterpret_cast<long long *>(vstate + 3 * LNC);
-  double *s_dt = reinterpret_cast<double *>(s_g + LNC);   // [4][LNC]: dt, h, t1, cval_t
-  int *s_cnt = reinterpret_cast<int *>(s_dt + 4 * LNC);   // [4][LNC]: steps, rej, newt, acc
-  double2 *cval = vstate + 7 * LNC;
+  double *s_dt = reinterpret_cast<double *>(s_g + 1);   // dt, h, t1, cval_t
+  int *s_cnt = reinterpret_cast<int *>(s_dt + 4);       // steps, rej, newt, acc
+  double2 *cval = reinterpret_cast<double2 *>(reinterpret_cast<unsigned char *>(vstate) + state_bytes(LNC));
   double2 *mono = cval + ncoef + A.ncoef_src;
   double2 *M = mono + A.n_mono;
   double2 *prow = M + A.n_entries + 1;
@@ -890,7 +902,8 @@ __device__ __forceinline__ void track_body(const TrackArgs &A) {
     M[A.n_entries] = make_double2(0.0, 0.0);     // the entry every structural zero reads
     os->base = os->next = os->end = 0;           // no chunk yet
   }
-  __syncthreads();
+  __syncthreads();                   // (the barrier's initialisation is visible to every waiter)
+  mbar_wait_parity(&tables_bar, 0);  // the staged tables have landed
 
   const DevSettings &st = A.st;
   const int n_rk = (st.predictor == HC_EULER) ? 1 : 4;
@@ -898,16 +911,16 @@ __device__ __forceinline__ void track_body(const TrackArgs &A) {
   // ---- slot state (replicated over the slot's lanes) ----
   int state = ST_DONE;
   long long g_r = -1;
-  long long &g = SS ? s_g[SS ? r : 0] : g_r;
+  long long &g = SS ? s_g[0] : g_r;
   g = -1;
   const double2 *ct = A.coef_t;   // instance coefficient table
   double t = 0.0;
   double dt_r = 0.0, h_r = 0.0, t1_r = 0.0, cval_t_r = -1.0;
   int steps_r = 0, rej_r = 0, newt_r = 0, acc_r = 0;
-  double &dt = SS ? s_dt[r] : dt_r, &h = SS ? s_dt[LNC + r] : h_r, &t1 = SS ? s_dt[2 * LNC + r] : t1_r;
+  double &dt = SS ? s_dt[0] : dt_r, &h = SS ? s_dt[1] : h_r, &t1 = SS ? s_dt[2] : t1_r;
   h = t1 = 0.0;
-  int &steps = SS ? s_cnt[0 * LNC + r] : steps_r, &rej = SS ? s_cnt[1 * LNC + r] : rej_r,
-      &newt = SS ? s_cnt[2 * LNC + r] : newt_r, &acc = SS ? s_cnt[3 * LNC + r] : acc_r;
+  int &steps = SS ? s_cnt[0] : steps_r, &rej = SS ? s_cnt[1] : rej_r, &newt = SS ? s_cnt[2] : newt_r,
+      &acc = SS ? s_cnt[3] : acc_r;
   dt = 0.0;
   acc = steps = rej = newt = 0;
   int stage = 0, it = 0, solves = 0;
@@ -917,16 +930,18 @@ __device__ __forceinline__ void track_body(const TrackArgs &A) {
   // per lane): they are touched a few times per iteration, and the registers they free keep the
   // N <= 16 kernels within 128
   double2 x[NC], kacc_r[NC], kprev_r[NC], xc_r[NC];
-  auto KACC = [&](int c) -> double2 & { return SS ? vstate[(0 * NC + c) * L + r] : kacc_r[c]; };
-  auto KPREV = [&](int c) -> double2 & { return SS ? vstate[(1 * NC + c) * L + r] : kprev_r[c]; };
-  auto XC = [&](int c) -> double2 & { return SS ? vstate[(2 * NC + c) * L + r] : xc_r[c]; };
+  constexpr int LV = TrackerShape<N, LW>::LV;
+  const int vr = (SS && LV < L) ? (r < N ? r : N) : r;   // state lane (lanes without a row share a dummy)
+  auto KACC = [&](int c) -> double2 & { return SS ? vstate[(0 * NC + c) * LV + vr] : kacc_r[c]; };
+  auto KPREV = [&](int c) -> double2 & { return SS ? vstate[(1 * NC + c) * LV + vr] : kprev_r[c]; };
+  auto XC = [&](int c) -> double2 & { return SS ? vstate[(2 * NC + c) * LV + vr] : xc_r[c]; };
 #pragma unroll
   for (int c = 0; c < NC; ++c) x[c] = KACC(c) = KPREV(c) = XC(c) = make_double2(0.0, 0.0);
   auto comp_valid = [&](int c) -> bool { return c == 0 ? (r < N) : (r < E); };
   auto comp_row = [&](int c) -> int { return c == 0 ? r : 16 + r; };
   bool need_track = true;
   bool fresh_k1 = false;   // the last solve was a successful RK stage 1 (endgame sampling)
-  double &cval_t = SS ? s_dt[3 * LNC + r] : cval_t_r;   // t at which the slot's coefficient values were
+  double &cval_t = SS ? s_dt[3] : cval_t_r;   // t at which the slot's coefficient values were
   cval_t = -1.0;                                        // last evaluated (-1: none)
 #ifdef HCB_PHASE_TIMING
   unsigned long long hcb_phase[8] = {0, 0, 0, 0, 0, 0, 0, 0};
@@ -1309,7 +1324,8 @@ cudaError_t launch_tracker_n(const TrackArgs &A, int device, cudaStream_t stream
   // tail stays balanced.  Small batches: single tracks throughout.
   TrackArgs K = A;
   const long long slots = ctas * warps * TPW;
-  if (A.total >= 128 * slots) {
+  const char *ev_chunk = getenv("HC_TRACK_CHUNK");   // experiment override: 1 = single tracks only
+  if (A.total >= 128 * slots && !(ev_chunk && atoi(ev_chunk) == 1)) {
     K.chunk = OUT_CHUNK;
     K.chunk_end = (A.total - 8 * slots) / OUT_CHUNK * OUT_CHUNK;
   } else {

@@ -13,6 +13,7 @@
 #   sanitize                   compute-sanitizer memcheck / racecheck / synccheck over small cases of every path
 #   traffic                    DRAM bytes per launch (ncu) for trifocal and 4-view
 #   zgesv                      Fig. 3 re-run (N1): fused batched LU vs cuBLAS getrf/getrsBatched
+#   warps                      trifocal x64 step time at 4, 8, 12 warps per CTA (HC_TRACKER_WARPS; latency hiding)
 set -u
 mkdir -p gpurun_out
 build() { python -c "import __graft_entry__ as g; g.build()" 2>&1 | tail -1; }
@@ -69,11 +70,25 @@ while [ $# -gt 0 ]; do
         echo "== $tool exit $?"; tail -4 gpurun_out/sanitizer_$tool.log
       done ;;
     traffic)
-      timeout 900 python scripts/record_traffic.py trifocal 1024 gpurun_out/traffic.json >> gpurun_out/traffic.log 2>&1
+      timeout 900 python scripts/record_traffic.py trifocal ${TRAFFIC_TRI_B:-1024} gpurun_out/traffic.json >> gpurun_out/traffic.log 2>&1
       timeout 600 python scripts/record_traffic.py fourview 1024 gpurun_out/traffic.json >> gpurun_out/traffic.log 2>&1
       tail -2 gpurun_out/traffic.log ;;
     zgesv)
       timeout 900 python scripts/bench_zgesv.py > gpurun_out/zgesv_fig3.jsonl 2> gpurun_out/zgesv.err; tail -5 gpurun_out/zgesv_fig3.jsonl ;;
+    env)   # env VAR=VALUE ... : the AB_CFGS configs with the product library, once per setting (VAR= : unset)
+      while [ $# -gt 0 ] && [[ $1 == *=* ]]; do
+        kv=$1; shift
+        for cfg in $AB_CFGS; do
+          c=${cfg%%:*}; b=${cfg#*:}
+          env ${kv%%=*}=${kv#*=} timeout 900 python bench.py --config $c --instances $b --steps 1 --warmup 1 --no-cpu-baseline --no-e2e \
+            2>/dev/null | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('ENV', '$kv', '$c', round(d['ms_per_step'],2), round(d['roofline']['frac'],4), d['roofline']['tracker_ms_per_launch'], d['clocks']['sm_mhz'])"
+        done
+      done | tee -a gpurun_out/env.log ;;
+    warps)
+      for w in 4 8 12; do
+        HC_TRACKER_WARPS=$w timeout 900 python bench.py --config trifocal --instances 64 --steps 1 --warmup 1 --no-cpu-baseline --no-e2e \
+          2>/dev/null | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('WARPS', $w, round(d['ms_per_step'],2), round(d['roofline']['frac'],4), d['config']['launch'])"
+      done | tee -a gpurun_out/warps.log ;;
     *) echo "unknown job $job"; exit 2 ;;
   esac
 done
