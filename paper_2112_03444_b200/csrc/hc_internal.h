@@ -79,10 +79,7 @@ struct TrackArgs {
   const double2 *coef_t;     // [B][D+1][ncoef]
   const double2 *start_x;    // [S][N]
   int64_t S, total;          // tracks = B * S
-  unsigned long long *queue; // work counters (zeroed before launch): [0] chunks of `chunk` tracks below
-                             // chunk_end, [3] single tracks from chunk_end on (queue[1], [2]: endgame)
-  int32_t chunk;             // tracks per chunk (1 or OUT_CHUNK; set by the launcher)
-  int64_t chunk_end;         // tracks [0, chunk_end) are handed out in chunks (a multiple of chunk)
+  unsigned long long *queue; // work counter (zeroed before launch)
   double2 *x_out;            // [total][N]
   int32_t *status_out;       // [total]
   int32_t *counters_out;     // [total][4]

@@ -595,10 +595,9 @@ static hc_status track_batch_impl(hc_system sys, const hc_tracker_settings *sett
   double2 *d_coef = nullptr;
   unsigned long long *d_queue = nullptr;
   if ((s = dev_alloc(r, &d_coef, (size_t)B * (cs.D + 1) * cs.ncoef)) != HC_OK) return bail(s);
-  // work counters: [0] the tracker's chunk queue, [1] tracks handed to the endgame, [2] the endgame's
-  // queue, [3] the tracker's single-track queue (the tail)
-  if ((s = dev_alloc(r, &d_queue, 4)) != HC_OK) return bail(s);
-  if (cudaMemsetAsync(d_queue, 0, 4 * sizeof(unsigned long long), r->stream) != cudaSuccess)
+  // work counters: [0] the tracker's queue, [1] tracks handed to the endgame, [2] the endgame's queue
+  if ((s = dev_alloc(r, &d_queue, 3)) != HC_OK) return bail(s);
+  if (cudaMemsetAsync(d_queue, 0, 3 * sizeof(unsigned long long), r->stream) != cudaSuccess)
     return bail(cuda_fail(cudaGetLastError(), "memset queue"));
   int64_t *d_eg_list = nullptr;
   if (st.eg_start > 0.0 && (s = dev_alloc(r, &d_eg_list, (size_t)total)) != HC_OK) return bail(s);

@@ -54,8 +54,8 @@ __device__ __forceinline__ void endgame_body(const TrackArgs &A) {
   const int slot = warp * TPW + seg;
   const int ncoef = A.ncoef, D = A.D;
   unsigned char *sb = slots_base + (size_t)slot * slot_bytes(N, L, ncoef, A.ncoef_src, A.n_mono, A.n_entries + 1);
-  // (the tracker's output staging and per-lane state areas are unused here)
-  double2 *cval = reinterpret_cast<double2 *>(sb + EG_SAMPLE_BYTES + OUT_STAGE_BYTES + state_bytes(L));
+  // (the tracker's per-lane state area is unused here)
+  double2 *cval = reinterpret_cast<double2 *>(sb + EG_SAMPLE_BYTES + state_bytes(L));
   double2 *mono = cval + ncoef + A.ncoef_src;
   double2 *M = mono + A.n_mono;
   double2 *prow = M + A.n_entries + 1;

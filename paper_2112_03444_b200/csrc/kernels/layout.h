@@ -8,17 +8,11 @@ namespace hcb {
 
 __host__ __device__ inline size_t align16(size_t b) { return (b + 15) & ~size_t(15); }
 
-// Per track slot: the endgame sampling state (80 bytes, EgSample), the output staging (OutStage), the
-// shared-memory tracker state (state_bytes, below), cval[ncoef + ncoef_src]
+// Per track slot: the endgame sampling state (80 bytes, EgSample), the shared-memory tracker state (state_bytes, below), cval[ncoef + ncoef_src]
 // (c(t) for every slot, c'(t) for the rhs slots), mono[n_mono] (x_0..x_{N-1}, 1, shared products),
 // M[n_entries] (non-zero entries of [dH/dx | rhs]), prow[2 * (N + 1)] (double-buffered pivot row),
 // rabs[N] (doubles).
 constexpr size_t EG_SAMPLE_BYTES = 80;
-// Output staging per slot (OutStage): the chunk bookkeeping and the small per-track outputs (status,
-// winding, counters, residuals: 40 bytes per track) of the slot's current chunk of OUT_CHUNK
-// consecutive tracks, written to global memory as whole 32-byte sectors when the chunk is done.
-constexpr int OUT_CHUNK = 8;
-constexpr size_t OUT_STAGE_BYTES = 32 + (size_t)OUT_CHUNK * 40;
 // Per-lane tracker state kept in shared memory (the 128-register kernels): the RK / corrector vectors
 // [kacc | kprev | xc][lnc] (double2) and one copy of the slot's scalars (64 bytes: track id, step, h,
 // t1, the t of the cached coefficients, four counters).  lnc = state lanes x unknowns per lane: the
@@ -26,7 +20,7 @@ constexpr size_t OUT_STAGE_BYTES = 32 + (size_t)OUT_CHUNK * 40;
 __host__ __device__ constexpr int state_lanes(int N, int L, int NC) { return (NC == 1 && L > N) ? N + 1 : L * NC; }
 __host__ __device__ inline size_t state_bytes(int lnc) { return lnc ? (size_t)48 * lnc + 64 : 0; }
 __host__ __device__ inline size_t slot_bytes(int N, int lnc, int ncoef, int ncoef_src, int n_mono, int n_entries) {
-  return EG_SAMPLE_BYTES + OUT_STAGE_BYTES + state_bytes(lnc) +
+  return EG_SAMPLE_BYTES + state_bytes(lnc) +
          align16(sizeof(double) * 2 * ((size_t)ncoef + ncoef_src + n_mono + n_entries + 2 * (N + 1)) +
                  sizeof(double) * N);
 }

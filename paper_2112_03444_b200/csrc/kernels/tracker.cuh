@@ -164,18 +164,6 @@ __device__ __forceinline__ bool seg_all(bool p, int seg) {
   return (b & m) == m;
 }
 
-// Per-slot output staging (layout.h OUT_STAGE_BYTES): the slot's chunk [base, end) of consecutive
-// tracks (next: the next one to start) and the small outputs of its finished tracks, flushed as
-// whole sectors when the chunk is done (partial-sector stores of 4-16 bytes per track made the DRAM
-// read-modify-write: 2.1x the algorithmic bytes, round-1 traffic.json).
-struct OutStage {
-  long long base, next, end, pad;
-  int32_t status[OUT_CHUNK], wind[OUT_CHUNK];
-  int4 ctr[OUT_CHUNK];
-  double2 res[OUT_CHUNK];
-};
-static_assert(sizeof(OutStage) == OUT_STAGE_BYTES, "OutStage layout");
-
 enum SlotState : int { ST_RK = 0, ST_NEWTON = 1, ST_POLISH = 2, ST_RESID = 3, ST_DONE = 4, ST_EGFIN = 5 };
 
 // ------------------------------------------------------------------------------------------
@@ -883,8 +871,7 @@ __device__ __forceinline__ void track_body(const TrackArgs &A) {
   constexpr int LNC = TrackerShape<N, LW>::LNC;
   unsigned char *sb = slots_base + (size_t)slot * slot_bytes(N, LNC, ncoef, A.ncoef_src, A.n_mono, A.n_entries + 1);
   EgSample *egs = reinterpret_cast<EgSample *>(sb);   // endgame sampling state (R26), lane 0 writes
-  OutStage *os = reinterpret_cast<OutStage *>(sb + EG_SAMPLE_BYTES);   // chunk + staged outputs (lane 0 writes)
-  double2 *vstate = reinterpret_cast<double2 *>(sb + EG_SAMPLE_BYTES + OUT_STAGE_BYTES);   // [3][NC][LV] (SS only)
+  double2 *vstate = reinterpret_cast<double2 *>(sb + EG_SAMPLE_BYTES);   // [3][NC][LV] (SS only)
   // one copy of the slot's rarely touched scalars (track id, step size, h, t1, the t of the cached
   // coefficients, step / rejection / Newton / consecutive-accept counters; every lane of the slot
   // reads and writes the same values) -- in shared memory for the 128-register kernels, so their
@@ -900,7 +887,6 @@ __device__ __forceinline__ void track_body(const TrackArgs &A) {
   if (r == 0) {
     mono[N] = make_double2(1.0, 0.0);            // constant-one slot
     M[A.n_entries] = make_double2(0.0, 0.0);     // the entry every structural zero reads
-    os->base = os->next = os->end = 0;           // no chunk yet
   }
   __syncthreads();                   // (the barrier's initialisation is visible to every waiter)
   mbar_wait_parity(&tables_bar, 0);  // the staged tables have landed
@@ -969,12 +955,11 @@ __device__ __forceinline__ void track_body(const TrackArgs &A) {
 #pragma unroll
     for (int c = 0; c < NC; ++c)
       if (comp_valid(c)) A.x_out[(size_t)g * N + comp_row(c)] = x[c];
-    if (r == 0) {   // small outputs: staged, written with the chunk (refill below)
-      const int i = (int)(g - os->base);
-      os->status[i] = status;
-      os->ctr[i] = make_int4(steps, rej, newt, solves);
-      os->res[i] = make_double2(ra, rr);
-      os->wind[i] = 0;
+    if (r == 0) {
+      A.status_out[g] = status;
+      reinterpret_cast<int4 *>(A.counters_out)[g] = make_int4(steps, rej, newt, solves);
+      reinterpret_cast<double2 *>(A.resid_out)[g] = make_double2(ra, rr);
+      if (A.winding_out) A.winding_out[g] = 0;
       // a singular endpoint (reading R26): the Cauchy endgame kernel continues this track from
       // (x, t = 1 - ra) with step rr; the list entry is the track id
       if (status == HC_EG_PENDING) A.eg_list[atomicAdd(A.eg_count, 1ULL)] = g;
@@ -988,37 +973,8 @@ __device__ __forceinline__ void track_body(const TrackArgs &A) {
     //      all 32 lanes (warp collectives are never inside slot-divergent branches). ----
     {
       unsigned long long got = 0;
-      if (__any_sync(FULL, need_track)) {   // (once per track: the per-iteration cost is the vote)
-        __syncwarp();   // lane 0's staged outputs and chunk fields are visible to the slot's lanes
-        if (need_track) {
-          const long long cb = os->base, cn = os->next, ce = os->end;
-          if (cn >= ce && ce > cb) {   // the chunk is done: its small outputs as whole sectors
-            for (int i = r; i < (int)(ce - cb); i += L) {
-              A.status_out[cb + i] = os->status[i];
-              reinterpret_cast<int4 *>(A.counters_out)[cb + i] = os->ctr[i];
-              reinterpret_cast<double2 *>(A.resid_out)[cb + i] = os->res[i];
-              if (A.winding_out) A.winding_out[cb + i] = os->wind[i];
-            }
-          }
-          if (r == 0) {
-            long long nb = cn, ne = ce;
-            if (cn >= ce) {   // next chunk: OUT_CHUNK-aligned chunks first, then single tracks
-              nb = (long long)atomicAdd(A.queue, (unsigned long long)A.chunk);
-              if (nb < A.chunk_end) {
-                ne = nb + A.chunk;
-              } else {
-                nb = A.chunk_end + (long long)atomicAdd(A.queue + 3, 1ULL);
-                ne = nb + 1;
-              }
-              os->base = nb;
-            }
-            got = (unsigned long long)nb;
-            os->next = nb + 1;
-            os->end = (nb < A.total) ? ne : nb;   // past the end: nothing left to flush
-          }
-        }
-        got = __shfl_sync(FULL, got, seg * L);
-      }
+      if (need_track && r == 0) got = atomicAdd(A.queue, 1ULL);
+      got = __shfl_sync(FULL, got, seg * L);
       if (need_track) {
         need_track = false;
         if ((long long)got < A.total) {
@@ -1319,20 +1275,7 @@ cudaError_t launch_tracker_n(const TrackArgs &A, int device, cudaStream_t stream
     plan->ctas = (int)ctas;
     plan->smem_bytes = smem;
   }
-  // work distribution: chunks of OUT_CHUNK consecutive tracks per slot (whole-sector output writes)
-  // when every slot gets >= 128 tracks; the last ~8 tracks per slot are handed out singly, so the
-  // tail stays balanced.  Small batches: single tracks throughout.
-  TrackArgs K = A;
-  const long long slots = ctas * warps * TPW;
-  const char *ev_chunk = getenv("HC_TRACK_CHUNK");   // experiment override: 1 = single tracks only
-  if (A.total >= 128 * slots && !(ev_chunk && atoi(ev_chunk) == 1)) {
-    K.chunk = OUT_CHUNK;
-    K.chunk_end = (A.total - 8 * slots) / OUT_CHUNK * OUT_CHUNK;
-  } else {
-    K.chunk = 1;
-    K.chunk_end = A.total;
-  }
-  hc_track_kernel<N, LW><<<(unsigned)ctas, warps * 32, smem, stream>>>(K);
+  hc_track_kernel<N, LW><<<(unsigned)ctas, warps * 32, smem, stream>>>(A);
   return cudaGetLastError();
 }
 

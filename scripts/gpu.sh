@@ -13,6 +13,7 @@
 #   sanitize                   compute-sanitizer memcheck / racecheck / synccheck over small cases of every path
 #   traffic                    DRAM bytes per launch (ncu) for trifocal and 4-view
 #   zgesv                      Fig. 3 re-run (N1): fused batched LU vs cuBLAS getrf/getrsBatched
+#   env VAR=VAL ...            the AB_CFGS configs with the product library under each environment setting
 #   warps                      trifocal x64 step time at 4, 8, 12 warps per CTA (HC_TRACKER_WARPS; latency hiding)
 set -u
 mkdir -p gpurun_out
@@ -75,9 +76,10 @@ while [ $# -gt 0 ]; do
       tail -2 gpurun_out/traffic.log ;;
     zgesv)
       timeout 900 python scripts/bench_zgesv.py > gpurun_out/zgesv_fig3.jsonl 2> gpurun_out/zgesv.err; tail -5 gpurun_out/zgesv_fig3.jsonl ;;
-    env)   # env VAR=VALUE ... : the AB_CFGS configs with the product library, once per setting (VAR= : unset)
-      while [ $# -gt 0 ] && [[ $1 == *=* ]]; do
-        kv=$1; shift
+    env)   # env VAR=VALUE ... : the AB_CFGS configs with the product library, once per setting
+      kvs=()
+      while [ $# -gt 0 ] && [[ $1 == *=* ]]; do kvs+=("$1"); shift; done
+      for kv in "${kvs[@]}"; do
         for cfg in $AB_CFGS; do
           c=${cfg%%:*}; b=${cfg#*:}
           env ${kv%%=*}=${kv#*=} timeout 900 python bench.py --config $c --instances $b --steps 1 --warmup 1 --no-cpu-baseline --no-e2e \
