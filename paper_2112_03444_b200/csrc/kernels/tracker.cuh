@@ -273,87 +273,32 @@ __device__ __forceinline__ int seg_argmax(double v, int r, double &vmax) {
 // pivot lane, 1/pivot and the pivot row's column k+1 are shuffled from it while the rest of its row
 // goes through a double-buffered shared row (one __syncwarp per column); every other row updates
 // column k+1 first, and the arg-max for step k+1 starts on it while the remaining columns are
-// updated.  Solution components are collected through shared memory.
+// updated.  The pivot lane also parks 1/pivot in pinv[k] (scratch that is dead during the solve)
+// for the final division.  Solution components are collected through shared memory.
 // Returns the solution component y_r in lane r and a slot-uniform success flag.
-// prow: 2 * (N + 1) double2 (per slot shared memory).
+// prow: 2 * (N + 1) double2, pinv: N double2 (per slot shared memory).
 // ------------------------------------------------------------------------------------------
-#ifndef HCB_LU_PIPE   // software-pipelined column schedule (A/B switch; 0 = the round-1 order)
-#define HCB_LU_PIPE 0
-#endif
-#ifndef HCB_LU_SYNC_EARLY   // round-1 order with the __syncwarp right after the publish (A/B switch)
-#define HCB_LU_SYNC_EARLY 0
+#ifndef HCB_LU_SYNC_EARLY   // __syncwarp right after the publish (1), or after the next arg-max (0)
+#define HCB_LU_SYNC_EARLY (-1)   // -1: by N (measured: N <= 16 +4.5 %, N = 18 -0.7 %)
 #endif
 template <int N, int L>
-__device__ __forceinline__ bool lu_rows(double2 (&a)[N + 1], int r, int seg, double2 *prow,
+__device__ __forceinline__ bool lu_rows(double2 (&a)[N + 1], int r, int seg, double2 *prow, double2 *pinv,
                                         double pivot_rel, double lane_max, double2 &y) {
-  bool used = (r >= N);
-  int mystep = used ? N : -1;
-  double2 myinv = make_double2(0.0, 0.0);
+  constexpr bool SYNC_EARLY = (HCB_LU_SYNC_EARLY < 0) ? (N <= 16) : (HCB_LU_SYNC_EARLY != 0);
+  // rows already pivoted (and padding rows) are excluded from the arg-max by a -inf bias on |a|^2
+  // (one DADD per column; a NaN result is never a candidate either)
+  double vbias = (r >= N) ? -INFINITY : 0.0;
+  int mystep = (r >= N) ? N : -1;
   // lane_max: max |A_ij|^2 over the entries this lane holds or produced (NaN entries are ignored by
   // fmax; they make the solve fail through the non-finite solution check)
   const double am = seg_max<L>(lane_max);
   const double thr = pivot_rel * pivot_rel * am;
   bool sing = !(am < INFINITY);
   // pivot of step 0
-  double v0 = used ? -1.0 : abs2(a[0]);
+  double v0 = abs2(a[0]) + vbias;
   if (!(v0 >= 0.0)) v0 = -1.0;   // NaN is never a pivot
   int p = seg_argmax_thr<L>(v0, r, thr, sing);
   double2 spec = crecip(a[0]);   // speculative 1/a_rk of this lane's candidate (overlaps the search)
-#if HCB_LU_PIPE
-  // Software-pipelined order (same arithmetic, same pivots): the dependency chain of a column is
-  // multiplier -> column k+1 -> |a|^2 -> arg-max -> shuffles of 1/pivot and the next pivot row's
-  // column k+2; the trailing update of columns k+3..N does not feed it, so it is issued after the
-  // next column's shuffles (their latency hides under it) and the next pivot lane publishes its
-  // row after it.  (The round-1 order ran the whole trailing update between the arg-max and the
-  // shuffles, putting its issue time on every column's chain.)
-  double2 inv = shfl2(spec, p, L);
-  double2 u1 = shfl2(a[1], p, L);
-  if (r == p) {   // pivot row of step 0: columns 2..N through shared memory
-#pragma unroll
-    for (int j = 2; j <= N; ++j) prow[j] = a[j];
-    used = true;
-    mystep = 0;
-    myinv = spec;
-  }
-  __syncwarp();
-#pragma unroll
-  for (int k = 0; k < N; ++k) {
-    const double2 *pr = prow + (k & 1) * (N + 1);         // pivot row of step k (columns k+2..N)
-    double2 *pn = prow + ((k + 1) & 1) * (N + 1);         // pivot row of step k+1 (columns k+3..N)
-    const bool me = (r == p);
-    const double2 lc = cmul(a[k], inv);
-    const double2 l = me ? make_double2(0.0, 0.0) : lc;
-    a[k + 1] = cfms(a[k + 1], l, u1);   // column k+1 (k + 1 == N: the right-hand side)
-    if (k + 1 < N) {
-      a[k + 2] = cfms(a[k + 2], l, pr[k + 2]);   // column k+2: the next pivot row's broadcast needs it
-      double v = abs2(a[k + 1]);
-      if (used || (L < 32 && !(v >= 0.0))) v = -1.0;   // NaN is never a pivot (the REDUX path excludes it itself)
-      spec = crecip(a[k + 1]);
-      p = seg_argmax_thr<L>(v, r, thr, sing);
-      inv = shfl2(spec, p, L);
-      u1 = shfl2(a[k + 2], p, L);
-      // trailing update of step k, columns k+3..N, in chunks of 4 (loads before their FMAs)
-#pragma unroll
-      for (int j0 = k + 3; j0 <= N; j0 += 4) {
-        double2 u[4];
-#pragma unroll
-        for (int i = 0; i < 4; ++i)
-          if (j0 + i <= N) u[i] = pr[j0 + i];
-#pragma unroll
-        for (int i = 0; i < 4; ++i)
-          if (j0 + i <= N) a[j0 + i] = cfms(a[j0 + i], l, u[i]);
-      }
-      if (r == p) {   // the pivot lane of step k+1 publishes columns k+3..N of its (now updated) row
-#pragma unroll
-        for (int j = k + 3; j <= N; ++j) pn[j] = a[j];
-        used = true;
-        mystep = k + 1;
-        myinv = spec;
-      }
-      __syncwarp();   // the published row is visible (and pr's readers are done before it is reused)
-    }
-  }
-#else
 #pragma unroll
   for (int k = 0; k < N; ++k) {
     double2 *pr = prow + (k & 1) * (N + 1);
@@ -364,13 +309,11 @@ __device__ __forceinline__ bool lu_rows(double2 (&a)[N + 1], int r, int seg, dou
     if (me) {   // the pivot lane publishes the rest of its row (columns k+2..N) through shared memory
 #pragma unroll
       for (int j = k + 2; j <= N; ++j) pr[j] = a[j];
-      used = true;
+      pinv[k] = spec;   // 1/pivot for the final division (pinv: slot scratch, dead during the solve)
+      vbias = -INFINITY;
       mystep = k;
-      myinv = spec;
     }
-#if HCB_LU_SYNC_EARLY
-    __syncwarp();   // the published row is visible: its loads may start under the arg-max chain
-#endif
+    if constexpr (SYNC_EARLY) __syncwarp();   // the published row is visible: its loads may start early
     // Gauss-Jordan: every row except the pivot row eliminates column k -- the rows pivoted earlier
     // too, which in this one-row-per-lane layout costs no extra instruction (the whole warp runs
     // the update anyway) and removes the sequential back-substitution.  Padding rows are zero.
@@ -378,13 +321,11 @@ __device__ __forceinline__ bool lu_rows(double2 (&a)[N + 1], int r, int seg, dou
     const double2 l = me ? make_double2(0.0, 0.0) : lc;
     a[k + 1] = cfms(a[k + 1], l, u1);   // column k+1 first (k + 1 == N: the right-hand side)
     if (k + 1 < N) {
-      double v = abs2(a[k + 1]);
-      if (used || (L < 32 && !(v >= 0.0))) v = -1.0;   // NaN is never a pivot (the REDUX path excludes it itself)
+      double v = abs2(a[k + 1]) + vbias;
+      if (L < 32 && !(v >= 0.0)) v = -1.0;   // NaN is never a pivot (the REDUX path excludes it itself)
       spec = crecip(a[k + 1]);
       p = seg_argmax_thr<L>(v, r, thr, sing);
-#if !HCB_LU_SYNC_EARLY
-      __syncwarp();   // the published row is visible
-#endif
+      if constexpr (!SYNC_EARLY) __syncwarp();   // the published row is visible
       // trailing update in chunks of 4 columns: the 4 shared loads are issued before their FMAs so
       // the load latency overlaps (the compiler otherwise keeps only ~2 loads in flight)
 #pragma unroll
@@ -399,13 +340,11 @@ __device__ __forceinline__ bool lu_rows(double2 (&a)[N + 1], int r, int seg, dou
       }
     }
   }
-#endif
-  __syncwarp();
   // ---- the system is now diagonal in pivot order: x_{mystep} = b' / pivot, routed through shared memory ----
   double2 *xsol = prow;
   // a row that was never a pivot (mystep == -1: only when the search found no usable candidate, i.e.
   // a singular solve) writes nothing -- xsol[-1] would be the slot's always-zero entry of M
-  if (mystep >= 0 && mystep < N) xsol[mystep] = cmul(a[N], myinv);
+  if (mystep >= 0 && mystep < N) xsol[mystep] = cmul(a[N], pinv[mystep]);
   __syncwarp();
   const double2 sol = (r < N) ? xsol[r] : make_double2(0.0, 0.0);
   y = sol;
@@ -822,7 +761,7 @@ __device__ __forceinline__ bool eval_solve(const TrackArgs &A, const uint2 *__re
   fabs_r[0] = (r < N && want_abs) ? rabs[r] : 0.0;
   HCB_T(c4);
   HCB_ACC(3, c3, c4);
-  const bool ok = lu_rows<N, L>(a, r, seg, prow, A.st.pivot_rel, jmax, y[0]);
+  const bool ok = lu_rows<N, L>(a, r, seg, prow, M, A.st.pivot_rel, jmax, y[0]);
   HCB_T(c5);
   HCB_ACC(4, c4, c5);
   return ok;

@@ -54,7 +54,7 @@ __global__ void __launch_bounds__(128) batched_zgesv_kernel(const double2 *__res
     double amax = 0.0;
 #pragma unroll
     for (int j = 0; j < N; ++j) amax = fmax(amax, abs2(a[j]));
-    const bool ok = lu_rows<N, L>(a, r, seg, prow, pivot_rel, amax, y);
+    const bool ok = lu_rows<N, L>(a, r, seg, prow, stage + seg * N * SP, pivot_rel, amax, y);   // (the staging tile is dead here)
     if (valid) {
       if (r < N) x[(size_t)k * N + r] = y;
       if (r == 0) info[k] = ok ? 0 : 1;

@@ -8,7 +8,8 @@
 #   ncu CFG B TAG              one ncu --set full capture of the tracker kernel (bench --config CFG --instances B)
 #   ab NAME=DEFINES ...        A/B of variant libraries built HERE from the committed sources: each NAME is built
 #                              with HCB_VARIANT=NAME HCB_DEFINES="DEFINES" (comma-separated defines) into
-#                              lib_NAME/; NAME=base is the product library; trifocal x64 and 4-view x1024 step times
+#                              lib_NAME/; NAME=base is the product library, NAME=@dir a prebuilt dir/libhc.so (e.g. the
+#                              previous commit's, built locally into abl/); the AB_CFGS step times
 #   phase                      per-phase cycle breakdown (HCB_VARIANT=timing build), trifocal and 4-view
 #   sanitize                   compute-sanitizer memcheck / racecheck / synccheck over small cases of every path
 #   traffic                    DRAM bytes per launch (ncu) for trifocal and 4-view
@@ -48,6 +49,7 @@ while [ $# -gt 0 ]; do
       while [ $# -gt 0 ] && [[ $1 == *=* ]]; do
         name=${1%%=*}; defs=${1#*=}; shift
         if [ "$name" = base ]; then libs+=(lib); continue; fi
+        if [[ $defs == @* ]]; then libs+=("../${defs#@}"); continue; fi   # NAME=@dir: a prebuilt dir/libhc.so (repo-relative)
         HCB_VARIANT=$name HCB_DEFINES="${defs//,/ }" python paper_2112_03444_b200/build.py > /dev/null || echo "build $name failed"
         libs+=(lib_$name)
       done
