@@ -281,6 +281,12 @@ __device__ __forceinline__ int seg_argmax(double v, int r, double &vmax) {
 #ifndef HCB_LU_SYNC_EARLY   // __syncwarp right after the publish (1), or after the next arg-max (0)
 #define HCB_LU_SYNC_EARLY (-1)   // -1: by N (measured: N <= 16 +4.5 %, N = 18 -0.7 %)
 #endif
+// 16-byte shared-memory store under a predicate (a predicated st.shared, not a divergent branch)
+__device__ __forceinline__ void st_shared_if(bool pred, double2 *dst, double2 v) {
+  asm volatile("{\n .reg .pred p;\n setp.ne.u32 p, %0, 0;\n @p st.shared.v2.f64 [%1], {%2, %3};\n}" ::"r"((unsigned)pred),
+               "r"(smem_u32(dst)), "d"(v.x), "d"(v.y)
+               : "memory");
+}
 template <int N, int L>
 __device__ __forceinline__ bool lu_rows(double2 (&a)[N + 1], int r, int seg, double2 *prow, double2 *pinv,
                                         double pivot_rel, double lane_max, double2 &y) {
@@ -306,10 +312,13 @@ __device__ __forceinline__ bool lu_rows(double2 (&a)[N + 1], int r, int seg, dou
     const double2 inv = shfl2(spec, p, L);
     const double2 u1 = shfl2(a[k + 1], p, L);
     const bool me = (r == p);
-    if (me) {   // the pivot lane publishes the rest of its row (columns k+2..N) through shared memory
+    // the pivot lane publishes the rest of its row (columns k+2..N) through shared memory, and parks
+    // 1/pivot for the final division (pinv: slot scratch, dead during the solve).  Predicated stores
+    // (not a branch), so the scheduler can interleave them with the FP64 work around them.
 #pragma unroll
-      for (int j = k + 2; j <= N; ++j) pr[j] = a[j];
-      pinv[k] = spec;   // 1/pivot for the final division (pinv: slot scratch, dead during the solve)
+    for (int j = k + 2; j <= N; ++j) st_shared_if(me, &pr[j], a[j]);
+    st_shared_if(me, &pinv[k], spec);
+    if (me) {
       vbias = -INFINITY;
       mystep = k;
     }
