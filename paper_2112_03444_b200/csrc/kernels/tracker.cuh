@@ -278,6 +278,9 @@ __device__ __forceinline__ int seg_argmax(double v, int r, double &vmax) {
 // Returns the solution component y_r in lane r and a slot-uniform success flag.
 // prow: 2 * (N + 1) double2, pinv: N double2 (per slot shared memory).
 // ------------------------------------------------------------------------------------------
+#ifndef HCB_LU_PINV   // 1/pivot parked in shared scratch (1) or kept in registers (0) (A/B switch)
+#define HCB_LU_PINV 1
+#endif
 #ifndef HCB_LU_SYNC_EARLY   // __syncwarp right after the publish (1), or after the next arg-max (0)
 #define HCB_LU_SYNC_EARLY (-1)   // -1: by N (measured: N <= 16 +4.5 %, N = 18 -0.7 %)
 #endif
@@ -295,6 +298,7 @@ __device__ __forceinline__ bool lu_rows(double2 (&a)[N + 1], int r, int seg, dou
   // (one DADD per column; a NaN result is never a candidate either)
   double vbias = (r >= N) ? -INFINITY : 0.0;
   int mystep = (r >= N) ? N : -1;
+  double2 myinv = make_double2(0.0, 0.0);   // (HCB_LU_PINV == 0: 1/pivot kept in registers)
   // lane_max: max |A_ij|^2 over the entries this lane holds or produced (NaN entries are ignored by
   // fmax; they make the solve fail through the non-finite solution check)
   const double am = seg_max<L>(lane_max);
@@ -317,10 +321,11 @@ __device__ __forceinline__ bool lu_rows(double2 (&a)[N + 1], int r, int seg, dou
     // (not a branch), so the scheduler can interleave them with the FP64 work around them.
 #pragma unroll
     for (int j = k + 2; j <= N; ++j) st_shared_if(me, &pr[j], a[j]);
-    st_shared_if(me, &pinv[k], spec);
+    if constexpr (HCB_LU_PINV) st_shared_if(me, &pinv[k], spec);
     if (me) {
       vbias = -INFINITY;
       mystep = k;
+      if constexpr (!HCB_LU_PINV) myinv = spec;
     }
     if constexpr (SYNC_EARLY) __syncwarp();   // the published row is visible: its loads may start early
     // Gauss-Jordan: every row except the pivot row eliminates column k -- the rows pivoted earlier
@@ -353,7 +358,7 @@ __device__ __forceinline__ bool lu_rows(double2 (&a)[N + 1], int r, int seg, dou
   double2 *xsol = prow;
   // a row that was never a pivot (mystep == -1: only when the search found no usable candidate, i.e.
   // a singular solve) writes nothing -- xsol[-1] would be the slot's always-zero entry of M
-  if (mystep >= 0 && mystep < N) xsol[mystep] = cmul(a[N], pinv[mystep]);
+  if (mystep >= 0 && mystep < N) xsol[mystep] = cmul(a[N], HCB_LU_PINV ? pinv[mystep] : myinv);
   __syncwarp();
   const double2 sol = (r < N) ? xsol[r] : make_double2(0.0, 0.0);
   y = sol;
