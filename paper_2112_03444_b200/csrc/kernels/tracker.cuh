@@ -278,6 +278,9 @@ __device__ __forceinline__ int seg_argmax(double v, int r, double &vmax) {
 // Returns the solution component y_r in lane r and a slot-uniform success flag.
 // prow: 2 * (N + 1) double2, pinv: N double2 (per slot shared memory).
 // ------------------------------------------------------------------------------------------
+#ifndef HCB_LU_PRED_PUBLISH   // 32-lane tracks publish the pivot row with predicated stores (A/B switch)
+#define HCB_LU_PRED_PUBLISH 1
+#endif
 #ifndef HCB_LU_PINV   // 1/pivot parked in shared scratch (1) or kept in registers (0) (A/B switch)
 #define HCB_LU_PINV 1
 #endif
@@ -317,11 +320,18 @@ __device__ __forceinline__ bool lu_rows(double2 (&a)[N + 1], int r, int seg, dou
     const double2 u1 = shfl2(a[k + 1], p, L);
     const bool me = (r == p);
     // the pivot lane publishes the rest of its row (columns k+2..N) through shared memory, and parks
-    // 1/pivot for the final division (pinv: slot scratch, dead during the solve).  Predicated stores
-    // (not a branch), so the scheduler can interleave them with the FP64 work around them.
+    // 1/pivot for the final division (pinv: slot scratch, dead during the solve).  32-lane tracks:
+    // predicated stores (not a branch), so the scheduler interleaves them with the FP64 work around
+    // them (trifocal +2.3 %); narrower tracks keep the branch (4-view: 2.3 % faster with it).
+    if constexpr (L == 32 && HCB_LU_PRED_PUBLISH) {
 #pragma unroll
-    for (int j = k + 2; j <= N; ++j) st_shared_if(me, &pr[j], a[j]);
-    if constexpr (HCB_LU_PINV) st_shared_if(me, &pinv[k], spec);
+      for (int j = k + 2; j <= N; ++j) st_shared_if(me, &pr[j], a[j]);
+      if constexpr (HCB_LU_PINV) st_shared_if(me, &pinv[k], spec);
+    } else if (me) {
+#pragma unroll
+      for (int j = k + 2; j <= N; ++j) pr[j] = a[j];
+      if constexpr (HCB_LU_PINV) pinv[k] = spec;
+    }
     if (me) {
       vbias = -INFINITY;
       mystep = k;
