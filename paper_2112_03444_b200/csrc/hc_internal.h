@@ -25,9 +25,6 @@ namespace hcb {
 //    last entry and never store.
 //      x: coefficient slot (bits 0..15) | monomial index (bits 16..31)
 //      y: dest entry (bits 0..15, 0xFFFF = none) | flags << 16 (OP_LAST, OP_RHS)
-//    Device op records (the copy the kernels read, abi.cpp upload_tables): the same fields as
-//    byte offsets (x16) into the kernel's coefficient values, monomials and entries, with the rhs
-//    ops' slots moved to region 2 of the coefficient values (+ ncoef; tracker.cuh horner).
 //  * entries are stored compactly (only structurally non-zero entries of [dH/dx | rhs]);
 //    mpos[row*(N+1)+col] is the compact index or -1 for a structural zero.
 // ------------------------------------------------------------------------------------------

@@ -216,21 +216,7 @@ static hc_status upload_padded16(void **dst, const void *src, size_t bytes) {
 }
 
 static hc_status upload_tables(const CompiledSystem &cs, DevTables &t) {
-  // device op table (hc_internal.h "device op records"): rhs ops address region 2 of the kernel's
-  // coefficient values (c'(t) or c(t) by what the right-hand side is, tracker.cuh horner), so their
-  // slot moves up by ncoef; slot, monomial and destination are stored as byte offsets (x16), which
-  // saves the kernel an address multiply per operand
-  if ((cs.ncoef + cs.ncoef_src) * 16 > 0xFFFF || cs.n_mono * 16 > 0xFFFF || (cs.n_entries + 1) * 16 > 0xFFFF)
-    return fail(HC_E_TOO_LARGE, "evaluation tables exceed the kernel's 16-bit byte offsets");
-  std::vector<uint2> dops(cs.ops);
-  for (auto &w : dops) {
-    const uint32_t fl = w.y >> 16;
-    const uint32_t slot = (w.x & 0xFFFFu) + ((fl & OP_RHS) ? (uint32_t)cs.ncoef : 0u);
-    const uint32_t mono = w.x >> 16, dest = (fl & OP_LAST) ? (w.y & 0xFFFFu) : 0u;
-    w.x = (slot * 16u) | ((mono * 16u) << 16);
-    w.y = (dest * 16u) | (fl << 16);
-  }
-  hc_status s = upload_padded16((void **)&t.d_ops, dops.data(), sizeof(uint2) * dops.size());
+  hc_status s = upload_padded16((void **)&t.d_ops, cs.ops.data(), sizeof(uint2) * cs.ops.size());
   if (s == HC_OK) s = upload_padded16((void **)&t.d_mono_prog, cs.mono_prog.data(), sizeof(uint32_t) * cs.mono_prog.size());
   // device copy of the entry map: structural zeros point at the extra always-zero entry n_entries
   std::vector<int16_t> mp(cs.mpos);

@@ -85,8 +85,7 @@ __device__ __forceinline__ void endgame_body(const TrackArgs &A) {
   double dbg_where = 0.0;
   double2 x = make_double2(0.0, 0.0), xr = x, sum = x, est = x, kacc = x, kprev = x, xc = x, xh = x;
   const bool valid = r < N;
-  double2 cval_t = make_double2(-1.0, 0.0);   // t of the slot's cached coefficient values (region 1)
-  double2 cval_k2 = cval_t;                    // region 2's key: t, real part + 10 when it holds c'(t)
+  double2 cval_t = make_double2(-1.0, 0.0);   // t of the slot's cached coefficient values
 
   auto circ = [&](double theta) { double sn, cs; sincos(theta, &sn, &cs); return make_double2(cs, sn); };
   int dbg = 0;
@@ -175,7 +174,7 @@ __device__ __forceinline__ void endgame_body(const TrackArgs &A) {
           g = A.eg_list[got];
           const long long b = g / A.S;
           ct = A.coef_t + (size_t)b * (D + 1) * ncoef;
-          cval_t = cval_k2 = make_double2(-1.0, 0.0);
+          cval_t = make_double2(-1.0, 0.0);
           x = valid ? A.x_out[(size_t)g * N + r] : make_double2(0.0, 0.0);
           xh = x;
           const int4 c0 = reinterpret_cast<const int4 *>(A.counters_out)[g];
@@ -234,14 +233,11 @@ __device__ __forceinline__ void endgame_body(const TrackArgs &A) {
       xe = x;
     }
     const bool want_abs = __any_sync(FULL, mode == EG_RESID);
-    const bool rk = rhs_off != 0;
-    const double2 key2 = make_double2(te.x + (rk ? 10.0 : 0.0), te.y);
-    const int coef_mode = (te.x != cval_t.x || te.y != cval_t.y) ? 1 : (key2.x != cval_k2.x || key2.y != cval_k2.y) ? 2 : 0;
+    const bool need_coef = te.x != cval_t.x || te.y != cval_t.y;
     cval_t = te;
-    cval_k2 = key2;
     double2 xa[1] = {xe}, yv[1], fr[1];
     double fa[1];
-    const bool ok = eval_solve<N, L, 1>(A, ops_s, prog_s, mpos_s, row_of, ct, te, coef_mode, rk, want_abs, cval,
+    const bool ok = eval_solve<N, L, 1>(A, ops_s, prog_s, mpos_s, row_of, ct, te, need_coef, rhs_off, want_abs, cval,
                                         mono, M, prow, rabs, r, seg, xa, yv, fr, fa);
     const double2 y = yv[0];
 

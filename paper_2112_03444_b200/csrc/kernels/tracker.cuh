@@ -559,21 +559,9 @@ __device__ __forceinline__ bool lu_rows_hy(double2 (&a)[N + 1], double2 (&e)[E][
 // products shared through the monomial program).  ABS also accumulates sum |c m| for the
 // relative residual of the rhs rows (reading R10).
 // ------------------------------------------------------------------------------------------
-// One op: accumulate c*m; at the entry's last op store the entry and reset.  HCB_OP_ACC2: the complex
-// product is split over two accumulators (c.x*m and the c.y part) so the four DFMAs of an op depend
-// only on the previous op's same-part accumulator (chain of 1); else one accumulator (chain of 2,
-// but no final add and half the reset).  Device op records carry byte offsets (hc_internal.h).
-#ifndef HCB_OP_ACC2
-#define HCB_OP_ACC2 1
-#endif
-template <typename T>
-__device__ __forceinline__ T &at_byte(T *base, uint32_t off) {
-  return *reinterpret_cast<T *>(reinterpret_cast<unsigned char *>(base) + off);
-}
-template <typename T>
-__device__ __forceinline__ const T &at_byte(const T *base, uint32_t off) {
-  return *reinterpret_cast<const T *>(reinterpret_cast<const unsigned char *>(base) + off);
-}
+// One op: accumulate c*m; at the entry's last op store the entry and reset.  The complex product is
+// split over two accumulators (c.x*m and the c.y part) so the four DFMAs of an op depend only on
+// the previous op's same-part accumulator (chain of 1).
 template <int N, bool ABS>
 __device__ __forceinline__ void op_accumulate(uint2 op, double2 c, double2 m, double2 &acc, double2 &acc2,
                                               double &acc_abs, double2 *__restrict__ M, double *__restrict__ rabs,
@@ -582,19 +570,14 @@ __device__ __forceinline__ void op_accumulate(uint2 op, double2 c, double2 m, do
   if (ABS) acc_abs += sqrt(abs2(cmul(c, m)));
   acc.x = fma(c.x, m.x, acc.x);
   acc.y = fma(c.x, m.y, acc.y);
-  if (HCB_OP_ACC2) {
-    acc2.x = fma(-c.y, m.y, acc2.x);
-    acc2.y = fma(c.y, m.x, acc2.y);
-  } else {
-    acc.x = fma(-c.y, m.y, acc.x);
-    acc.y = fma(c.y, m.x, acc.y);
-  }
+  acc2.x = fma(-c.y, m.y, acc2.x);
+  acc2.y = fma(c.y, m.x, acc2.y);
   if (fl & OP_LAST) {
-    const uint32_t dest = op.y & 0xFFFFu;   // byte offset
-    at_byte(M, dest) = HCB_OP_ACC2 ? make_double2(acc.x + acc2.x, acc.y + acc2.y) : acc;
-    if (ABS && (fl & OP_RHS)) rabs[row_of[dest >> 4]] = acc_abs;
+    const uint32_t dest = op.y & 0xFFFFu;
+    M[dest] = make_double2(acc.x + acc2.x, acc.y + acc2.y);
+    if (ABS && (fl & OP_RHS)) rabs[row_of[dest]] = acc_abs;
     acc = make_double2(0.0, 0.0);
-    if (HCB_OP_ACC2) acc2 = make_double2(0.0, 0.0);
+    acc2 = make_double2(0.0, 0.0);
     acc_abs = 0.0;
   }
 }
@@ -604,7 +587,7 @@ __device__ __forceinline__ void op_accumulate(uint2 op, double2 c, double2 m, do
 // M would otherwise serialise every op behind the previous op's store: the compiler cannot prove
 // that M does not alias the op table, both being shared memory).
 template <int N, int L, bool ABS>
-__device__ __forceinline__ void run_ops(const uint2 *__restrict__ ops_s, int Q,
+__device__ __forceinline__ void run_ops(const uint2 *__restrict__ ops_s, int Q, int rhs_off,
                                         const double2 *__restrict__ cval, const double2 *__restrict__ mono,
                                         double2 *__restrict__ M, double *__restrict__ rabs, const int16_t *row_of,
                                         int r) {
@@ -618,30 +601,26 @@ __device__ __forceinline__ void run_ops(const uint2 *__restrict__ ops_s, int Q,
     for (int i = 0; i < 4; ++i) op[i] = ops_s[(q + i) * L + r];
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
-      c[i] = at_byte(cval, op[i].x & 0xFFFFu);   // (rhs ops address region 2, see horner)
-      m[i] = at_byte(mono, op[i].x >> 16);
+      c[i] = cval[(int)(op[i].x & 0xFFFFu) + (((op[i].y >> 16) & OP_RHS) ? rhs_off : 0)];
+      m[i] = mono[op[i].x >> 16];
     }
 #pragma unroll
     for (int i = 0; i < 4; ++i) op_accumulate<N, ABS>(op[i], c[i], m[i], acc, acc2, acc_abs, M, rabs, row_of);
   }
   for (; q < Q; ++q) {
     const uint2 o = ops_s[q * L + r];
-    op_accumulate<N, ABS>(o, at_byte(cval, o.x & 0xFFFFu), at_byte(mono, o.x >> 16), acc, acc2, acc_abs, M, rabs,
-                          row_of);
+    const double2 c = cval[(int)(o.x & 0xFFFFu) + (((o.y >> 16) & OP_RHS) ? rhs_off : 0)];
+    op_accumulate<N, ABS>(o, c, mono[o.x >> 16], acc, acc2, acc_abs, M, rabs, row_of);
   }
 }
 
 // ------------------------------------------------------------------------------------------
-// Coefficient values at t, by Horner on the prologue's polynomials coef_t[d][j] (d <= D): region 1
-// cval[0, ncoef) holds c_j(t) for every slot; region 2 cval[ncoef, ncoef + nsrc) holds, for the
-// descriptor's coefficients j < nsrc that the right-hand side uses, c_j'(t) when the right-hand side
-// is dH/dt (an RK stage, rk) and c_j(t) when it is H (Newton, polish, residual).  The device op table
-// addresses region 2 for every rhs op (upload_tables adds ncoef to their slot), so an op's
-// coefficient is one load with no per-op select.  Two slots per lane per iteration, all loads issued
-// before the FMA chains.
+// Coefficient values at t: c_j(t) for every slot and c_j'(t) for the rhs slots (j < nsrc), by
+// Horner on the prologue's polynomials coef_t[d][j] (d <= D); two slots per lane per iteration,
+// all loads issued before the FMA chains.
 // ------------------------------------------------------------------------------------------
 template <int D, int L>
-__device__ __forceinline__ void horner(const double2 *__restrict__ ct, double t, int ncoef, int nsrc, bool rk,
+__device__ __forceinline__ void horner(const double2 *__restrict__ ct, double t, int ncoef, int nsrc,
                                        double2 *__restrict__ cval, int r) {
   for (int j0 = r; j0 < ncoef; j0 += 2 * L) {
     const int j1 = j0 + L;
@@ -661,44 +640,18 @@ __device__ __forceinline__ void horner(const double2 *__restrict__ ct, double t,
       p1 = make_double2(fma(p1.x, t, c1[d].x), fma(p1.y, t, c1[d].y));
     }
     cval[j0] = p0;
-    if (j0 < nsrc) cval[ncoef + j0] = rk ? q0 : p0;
+    if (j0 < nsrc) cval[ncoef + j0] = q0;
     if (has1) {
       cval[j1] = p1;
-      if (j1 < nsrc) cval[ncoef + j1] = rk ? q1 : p1;
+      if (j1 < nsrc) cval[ncoef + j1] = q1;
     }
-  }
-}
-
-// Region 2 only (region 1 already holds c(t) at this t): c'(t) by Horner for an RK stage, else a
-// copy of c(t).
-template <int L, typename TT>
-__device__ __forceinline__ void coef_region2(const double2 *__restrict__ ct, TT t, int D, int ncoef, int nsrc,
-                                             bool rk, double2 *__restrict__ cval, int r) {
-  for (int j = r; j < nsrc; j += L) {
-    double2 q = cval[j];
-    if (rk) {
-      double2 p = __ldg(&ct[(size_t)D * ncoef + j]);
-      q = make_double2(0.0, 0.0);
-#pragma unroll 1
-      for (int d = D - 1; d >= 0; --d) {
-        const double2 c = __ldg(&ct[(size_t)d * ncoef + j]);
-        if constexpr (sizeof(TT) == sizeof(double2)) {
-          q = cfma(q, t, p);
-          p = cfma(p, t, c);
-        } else {
-          q = make_double2(fma(q.x, t, p.x), fma(q.y, t, p.y));
-          p = make_double2(fma(p.x, t, c.x), fma(p.y, t, c.y));
-        }
-      }
-    }
-    cval[ncoef + j] = q;
   }
 }
 
 // Coefficient values at a complex t (the Cauchy endgame tracks around |1 - t| = s, reading R26):
 // the same Horner recurrences in complex arithmetic, any degree D.
 template <int L>
-__device__ __forceinline__ void horner_c(const double2 *__restrict__ ct, double2 t, int D, int ncoef, int nsrc, bool rk,
+__device__ __forceinline__ void horner_c(const double2 *__restrict__ ct, double2 t, int D, int ncoef, int nsrc,
                                          double2 *__restrict__ cval, int r) {
   for (int j = r; j < ncoef; j += L) {
     double2 p = __ldg(&ct[(size_t)D * ncoef + j]), q = make_double2(0.0, 0.0);
@@ -709,7 +662,7 @@ __device__ __forceinline__ void horner_c(const double2 *__restrict__ ct, double2
       p = cfma(p, t, c);   // p = p t + c
     }
     cval[j] = p;
-    if (j < nsrc) cval[ncoef + j] = rk ? q : p;
+    if (j < nsrc) cval[ncoef + j] = q;
   }
 }
 
@@ -721,15 +674,13 @@ struct is_complex_t<double2> { static constexpr bool value = true; };
 // ------------------------------------------------------------------------------------------
 // Evaluate [dH/dx | rhs] into the slot's M (shared), then fused LU + solve.  Returns the solution
 // component y_r in lane r (r < N) and whether the solve succeeded (uniform over the slot).
-// rk: rhs = dH/dt (coefficients c'(t)), else rhs = H (coefficients c(t)).  coef_mode: 1 = the slot's
-// coefficient values are stale (Horner into both regions), 2 = region 1 is current but region 2
-// holds the other kind (region 2 only), 0 = both current.
+// rhs_off = 0 -> rhs = H (coefficients c(t)); rhs_off = ncoef -> rhs = dH/dt (coefficients c'(t)).
 // ------------------------------------------------------------------------------------------
 template <int N, int L, int NC, typename TT>
 __device__ __forceinline__ bool eval_solve(const TrackArgs &A, const uint2 *__restrict__ ops_s,
                                            const uint32_t *__restrict__ prog_s, const int16_t *__restrict__ mpos_s,
                                            const int16_t *__restrict__ row_of, const double2 *__restrict__ ct,
-                                           TT t, int coef_mode, bool rk, bool want_abs, double2 *cval,
+                                           TT t, bool need_coef, int rhs_off, bool want_abs, double2 *cval,
                                            double2 *mono,
                                            double2 *M, double2 *prow, double *rabs, int r, int seg,
                                            const double2 (&xr)[NC],
@@ -747,14 +698,12 @@ __device__ __forceinline__ bool eval_solve(const TrackArgs &A, const uint2 *__re
   if constexpr (NC == 2) {
     if (r < E) mono[16 + r] = xr[NC - 1];
   }
-  if (coef_mode == 2) {
-    coef_region2<L>(ct, t, D, ncoef, A.ncoef_src, rk, cval, r);
-  } else if constexpr (is_complex_t<TT>::value) {
-    if (coef_mode == 1) horner_c<L>(ct, t, D, ncoef, A.ncoef_src, rk, cval, r);
-  } else if (coef_mode == 1) switch (D) {   // D is uniform: the common degrees keep all loads of a coefficient in flight together
-    case 1: horner<1, L>(ct, t, ncoef, A.ncoef_src, rk, cval, r); break;
-    case 2: horner<2, L>(ct, t, ncoef, A.ncoef_src, rk, cval, r); break;
-    case 3: horner<3, L>(ct, t, ncoef, A.ncoef_src, rk, cval, r); break;
+  if constexpr (is_complex_t<TT>::value) {
+    if (need_coef) horner_c<L>(ct, t, D, ncoef, A.ncoef_src, cval, r);
+  } else if (need_coef) switch (D) {   // D is uniform: the common degrees keep all loads of a coefficient in flight together
+    case 1: horner<1, L>(ct, t, ncoef, A.ncoef_src, cval, r); break;
+    case 2: horner<2, L>(ct, t, ncoef, A.ncoef_src, cval, r); break;
+    case 3: horner<3, L>(ct, t, ncoef, A.ncoef_src, cval, r); break;
     default:
       for (int j = r; j < ncoef; j += L) {
         double2 p = __ldg(&ct[(size_t)D * ncoef + j]), q = make_double2(0.0, 0.0);
@@ -765,7 +714,7 @@ __device__ __forceinline__ bool eval_solve(const TrackArgs &A, const uint2 *__re
           p = make_double2(fma(p.x, t, c.x), fma(p.y, t, c.y));
         }
         cval[j] = p;
-        if (j < A.ncoef_src) cval[ncoef + j] = rk ? q : p;
+        if (j < A.ncoef_src) cval[ncoef + j] = q;
       }
   }
   __syncwarp();
@@ -794,8 +743,8 @@ __device__ __forceinline__ bool eval_solve(const TrackArgs &A, const uint2 *__re
   HCB_T(c2);
   HCB_ACC(1, c1, c2);
   // ---- homogenised term evaluation, lane-balanced op list ----
-  if (want_abs) run_ops<N, L, true>(ops_s, A.Q, cval, mono, M, rabs, row_of, r);
-  else run_ops<N, L, false>(ops_s, A.Q, cval, mono, M, rabs, row_of, r);
+  if (want_abs) run_ops<N, L, true>(ops_s, A.Q, rhs_off, cval, mono, M, rabs, row_of, r);
+  else run_ops<N, L, false>(ops_s, A.Q, rhs_off, cval, mono, M, rabs, row_of, r);
   __syncwarp();
   HCB_T(c3);
   HCB_ACC(2, c2, c3);
@@ -900,8 +849,8 @@ __device__ __forceinline__ void track_body(const TrackArgs &A) {
   // reads and writes the same values) -- in shared memory for the 128-register kernels, so their
   // register budget goes to the rows being eliminated (SS only)
   long long *s_g = reinterpret_cast<long long *>(vstate + 3 * LNC);
-  double *s_dt = reinterpret_cast<double *>(s_g + 1);   // dt, h, t1, cval_t, cval_k2
-  int *s_cnt = reinterpret_cast<int *>(s_dt + 5);       // steps, rej, newt, acc
+  double *s_dt = reinterpret_cast<double *>(s_g + 1);   // dt, h, t1, cval_t
+  int *s_cnt = reinterpret_cast<int *>(s_dt + 4);       // steps, rej, newt, acc
   double2 *cval = reinterpret_cast<double2 *>(reinterpret_cast<unsigned char *>(vstate) + state_bytes(LNC));
   double2 *mono = cval + ncoef + A.ncoef_src;
   double2 *M = mono + A.n_mono;
@@ -924,7 +873,7 @@ __device__ __forceinline__ void track_body(const TrackArgs &A) {
   g = -1;
   const double2 *ct = A.coef_t;   // instance coefficient table
   double t = 0.0;
-  double dt_r = 0.0, h_r = 0.0, t1_r = 0.0, cval_t_r = -1.0, cval_k2_r = -1.0;
+  double dt_r = 0.0, h_r = 0.0, t1_r = 0.0, cval_t_r = -1.0;
   int steps_r = 0, rej_r = 0, newt_r = 0, acc_r = 0;
   double &dt = SS ? s_dt[0] : dt_r, &h = SS ? s_dt[1] : h_r, &t1 = SS ? s_dt[2] : t1_r;
   h = t1 = 0.0;
@@ -952,8 +901,6 @@ __device__ __forceinline__ void track_body(const TrackArgs &A) {
   bool fresh_k1 = false;   // the last solve was a successful RK stage 1 (endgame sampling)
   double &cval_t = SS ? s_dt[3] : cval_t_r;   // t at which the slot's coefficient values were
   cval_t = -1.0;                                        // last evaluated (-1: none)
-  double &cval_k2 = SS ? s_dt[4] : cval_k2_r;  // region 2's key: t, + 10 when it holds c'(t)
-  cval_k2 = -1.0;
 #ifdef HCB_PHASE_TIMING
   unsigned long long hcb_phase[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   long long hcb_iter0 = clock64();
@@ -1006,7 +953,7 @@ __device__ __forceinline__ void track_body(const TrackArgs &A) {
           g = (long long)got;
           const long long b = g / A.S, s = g % A.S;
           ct = A.coef_t + (size_t)b * (D + 1) * ncoef;
-          cval_t = cval_k2 = -1.0;   // new instance: coefficient values are stale
+          cval_t = -1.0;   // new instance: coefficient values are stale
 #pragma unroll
           for (int c = 0; c < NC; ++c) x[c] = comp_valid(c) ? A.start_x[s * N + comp_row(c)] : make_double2(0.0, 0.0);
           t = 0.0;
@@ -1113,12 +1060,9 @@ __device__ __forceinline__ void track_body(const TrackArgs &A) {
     double fa[NC];
     // coefficient values depend only on (instance, t): RK stages 2/3 share t + h/2, and stage 4,
     // the Newton iterations and the next step's stage 1 share t + h, so Horner is skipped then
-    const bool rk = rhs_off != 0;
-    const double key2 = te + (rk ? 10.0 : 0.0);
-    const int coef_mode = (te != cval_t) ? 1 : (key2 != cval_k2) ? 2 : 0;
+    const bool need_coef = (te != cval_t);
     cval_t = te;
-    cval_k2 = key2;
-    const bool ok = eval_solve<N, L, NC>(A, ops_s, prog_s, mpos_s, row_of, ct, te, coef_mode, rk, want_abs, cval, mono,
+    const bool ok = eval_solve<N, L, NC>(A, ops_s, prog_s, mpos_s, row_of, ct, te, need_coef, rhs_off, want_abs, cval, mono,
                                      M, prow, rabs,
                                      r, seg, xe, yv, fr, fa
 #ifdef HCB_PHASE_TIMING
