@@ -281,9 +281,6 @@ __device__ __forceinline__ int seg_argmax(double v, int r, double &vmax) {
 #ifndef HCB_LU_PRED_PUBLISH   // 32-lane tracks publish the pivot row with predicated stores (A/B switch)
 #define HCB_LU_PRED_PUBLISH 1
 #endif
-#ifndef HCB_LU_SHFL_ROW   // wide layout, N <= 8: pivot row by shuffles (A/B switch)
-#define HCB_LU_SHFL_ROW 0
-#endif
 #ifndef HCB_LU_PINV   // 1/pivot parked in shared scratch (1) or kept in registers (0) (A/B switch)
 #define HCB_LU_PINV 1
 #endif
@@ -300,9 +297,6 @@ template <int N, int L>
 __device__ __forceinline__ bool lu_rows(double2 (&a)[N + 1], int r, int seg, double2 *prow, double2 *pinv,
                                         double pivot_rel, double lane_max, double2 &y) {
   constexpr bool SYNC_EARLY = (HCB_LU_SYNC_EARLY < 0) ? (N <= 16) : (HCB_LU_SYNC_EARLY != 0);
-  // small systems in the wide latency layout: the pivot row reaches the other lanes by shuffles
-  // instead of the shared-memory round trip and its __syncwarp (no smem on the column chain)
-  constexpr bool SHFL_ROW = HCB_LU_SHFL_ROW && L == 32 && N <= 8;
   // rows already pivoted (and padding rows) are excluded from the arg-max by a -inf bias on |a|^2
   // (one DADD per column; a NaN result is never a candidate either)
   double vbias = (r >= N) ? -INFINITY : 0.0;
@@ -329,10 +323,7 @@ __device__ __forceinline__ bool lu_rows(double2 (&a)[N + 1], int r, int seg, dou
     // 1/pivot for the final division (pinv: slot scratch, dead during the solve).  32-lane tracks:
     // predicated stores (not a branch), so the scheduler interleaves them with the FP64 work around
     // them (trifocal +2.3 %); narrower tracks keep the branch (4-view: 2.3 % faster with it).
-    const int pk = p;   // pivot lane of step k
-    if constexpr (SHFL_ROW) {   // (the trailing update takes the pivot row by shuffles)
-      if (me) pinv[k] = spec;
-    } else if constexpr (L == 32 && HCB_LU_PRED_PUBLISH) {
+    if constexpr (L == 32 && HCB_LU_PRED_PUBLISH) {
 #pragma unroll
       for (int j = k + 2; j <= N; ++j) st_shared_if(me, &pr[j], a[j]);
       if constexpr (HCB_LU_PINV) st_shared_if(me, &pinv[k], spec);
@@ -346,7 +337,7 @@ __device__ __forceinline__ bool lu_rows(double2 (&a)[N + 1], int r, int seg, dou
       mystep = k;
       if constexpr (!HCB_LU_PINV) myinv = spec;
     }
-    if constexpr (SYNC_EARLY && !SHFL_ROW) __syncwarp();   // the published row is visible: its loads may start early
+    if constexpr (SYNC_EARLY) __syncwarp();   // the published row is visible: its loads may start early
     // Gauss-Jordan: every row except the pivot row eliminates column k -- the rows pivoted earlier
     // too, which in this one-row-per-lane layout costs no extra instruction (the whole warp runs
     // the update anyway) and removes the sequential back-substitution.  Padding rows are zero.
@@ -358,7 +349,7 @@ __device__ __forceinline__ bool lu_rows(double2 (&a)[N + 1], int r, int seg, dou
       if (L < 32 && !(v >= 0.0)) v = -1.0;   // NaN is never a pivot (the REDUX path excludes it itself)
       spec = crecip(a[k + 1]);
       p = seg_argmax_thr<L>(v, r, thr, sing);
-      if constexpr (!SYNC_EARLY && !SHFL_ROW) __syncwarp();   // the published row is visible
+      if constexpr (!SYNC_EARLY) __syncwarp();   // the published row is visible
       // trailing update in chunks of 4 columns: the 4 shared loads are issued before their FMAs so
       // the load latency overlaps (the compiler otherwise keeps only ~2 loads in flight)
 #pragma unroll
@@ -366,7 +357,7 @@ __device__ __forceinline__ bool lu_rows(double2 (&a)[N + 1], int r, int seg, dou
         double2 u[4];
 #pragma unroll
         for (int i = 0; i < 4; ++i)
-          if (j0 + i <= N) u[i] = SHFL_ROW ? shfl2(a[j0 + i], pk, L) : pr[j0 + i];
+          if (j0 + i <= N) u[i] = pr[j0 + i];
 #pragma unroll
         for (int i = 0; i < 4; ++i)
           if (j0 + i <= N) a[j0 + i] = cfms(a[j0 + i], l, u[i]);

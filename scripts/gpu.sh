@@ -58,7 +58,7 @@ while [ $# -gt 0 ]; do
           for cfg in $AB_CFGS; do
             c=${cfg%%:*}; b=${cfg#*:}
             HC_LIB_PATH=paper_2112_03444_b200/$L/libhc.so timeout 900 python bench.py --config $c --instances $b --steps 1 --warmup 1 \
-              --no-cpu-baseline --no-e2e 2>/dev/null | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('AB', $round, '$L', '$c', round(d['ms_per_step'],2), round(d['roofline']['frac'],4), d['config']['launch'])"
+              --no-cpu-baseline --no-e2e 2>/dev/null | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('AB', $round, '$L', '$c', round(d['ms_per_step'],2), round(d['roofline']['frac'],4), round(d['roofline']['tracker_ms_per_launch'],3), d['config']['launch'])"
           done
         done
       done | tee -a gpurun_out/ab.log ;;
