@@ -107,6 +107,9 @@ __device__ __forceinline__ double2 shfl2(double2 v, int src, int width) {
   return make_double2(__shfl_sync(FULL, v.x, src, width), __shfl_sync(FULL, v.y, src, width));
 }
 
+#ifndef HCB_OUT_EXPERIMENT   // DRAM-traffic experiment only (results invalid): 1 = no status/counter/
+#define HCB_OUT_EXPERIMENT 0  // residual writes, 2 = no x writes (scripts/gpu.sh traffic_ab)
+#endif
 #ifndef HCB_EG_SAMPLING   // endgame sampling in the tracker (A/B switch; 0 = no endgame hand-off)
 #define HCB_EG_SAMPLING 1
 #endif
@@ -917,12 +920,14 @@ __device__ __forceinline__ void track_body(const TrackArgs &A) {
   auto finish = [&](int status, double ra, double rr) {
 #pragma unroll
     for (int c = 0; c < NC; ++c)
-      if (comp_valid(c)) A.x_out[(size_t)g * N + comp_row(c)] = x[c];
-    if (r == 0) {
+      if (comp_valid(c) && HCB_OUT_EXPERIMENT != 2) A.x_out[(size_t)g * N + comp_row(c)] = x[c];
+    if (r == 0 && HCB_OUT_EXPERIMENT != 1) {
       A.status_out[g] = status;
       reinterpret_cast<int4 *>(A.counters_out)[g] = make_int4(steps, rej, newt, solves);
       reinterpret_cast<double2 *>(A.resid_out)[g] = make_double2(ra, rr);
       if (A.winding_out) A.winding_out[g] = 0;
+    }
+    if (r == 0) {
       // a singular endpoint (reading R26): the Cauchy endgame kernel continues this track from
       // (x, t = 1 - ra) with step rr; the list entry is the track id
       if (status == HC_EG_PENDING) A.eg_list[atomicAdd(A.eg_count, 1ULL)] = g;
