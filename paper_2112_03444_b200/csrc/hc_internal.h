@@ -65,7 +65,8 @@ struct EgSample {
 struct TrackArgs {
   // system tables
   const uint2 *ops;          // [Q * L]
-  int32_t Q;
+  int32_t Q;                 // op steps (paired table: 2 x pair steps, the table's size in uint2 units)
+  int32_t Qp;                // pair steps of a paired op table (0: single ops; abi.cpp pair_ops)
   const uint32_t *mono_prog; // [n_mono - (N + 1)]
   int32_t n_mono;            // monomial table size including the N unknowns and the constant
   int32_t n_levels;

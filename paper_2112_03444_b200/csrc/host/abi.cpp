@@ -104,6 +104,7 @@ static hc_status cuda_fail(cudaError_t e, const char *where) {
 // A compiled table set on the device (one per lane layout).
 struct DevTables {
   uint2 *d_ops = nullptr;
+  int Qp = 0;                // pair steps when d_ops holds the paired table (pair_ops), else 0
   uint32_t *d_mono_prog = nullptr;
   int16_t *d_mpos = nullptr;
   CoefMono *d_mono = nullptr;
@@ -215,8 +216,57 @@ static hc_status upload_padded16(void **dst, const void *src, size_t bytes) {
   return HC_OK;
 }
 
+// Paired op table (tracker.cuh run_ops_pairs): per lane, the ops of each entry two at a time in one
+// 16-byte record {slot_a | mono_a << 16, slot_b | mono_b << 16, dest | flags << 16, 0}; an odd
+// entry's last record pairs its term with the constant-zero monomial mono[n_mono] (same slot, so
+// the coefficient is finite and the term exactly 0); lanes past their last entry get neutral
+// records.  Returns the pair steps Qp; the table is [Qp][L] records (2 uint2 each).
+static int pair_ops(const CompiledSystem &cs, std::vector<uint2> &out) {
+  const int L = cs.L, Q = cs.Q;
+  std::vector<std::vector<uint4>> lanes(L);
+  for (int l = 0; l < L; ++l) {
+    std::vector<uint2> cur;
+    for (int q = 0; q < Q; ++q) {
+      const uint2 o = cs.ops[(size_t)q * L + l];
+      const uint32_t fl = o.y >> 16;
+      cur.push_back(o);
+      if (!(fl & OP_LAST)) continue;
+      for (size_t i = 0; i < cur.size(); i += 2) {
+        const uint2 a = cur[i];
+        const bool has_b = i + 1 < cur.size();
+        const uint2 b = has_b ? cur[i + 1] : uint2{(a.x & 0xFFFFu) | ((uint32_t)cs.n_mono << 16), 0u};
+        const bool last = i + 2 >= cur.size();
+        uint4 rec;
+        rec.x = a.x;
+        rec.y = b.x;
+        rec.z = last ? o.y : (OP_NO_DEST | ((fl & OP_RHS) << 16));
+        rec.w = 0u;
+        lanes[l].push_back(rec);
+      }
+      cur.clear();
+    }
+    // (trailing ops without OP_LAST are the compiler's never-stored padding: dropped)
+  }
+  int Qp = 0;
+  for (auto &v : lanes) Qp = std::max(Qp, (int)v.size());
+  const uint4 neutral{(uint32_t)cs.n_mono << 16, (uint32_t)cs.n_mono << 16, OP_NO_DEST, 0u};
+  out.assign((size_t)Qp * L * 2, uint2{0u, 0u});
+  for (int q = 0; q < Qp; ++q)
+    for (int l = 0; l < L; ++l) {
+      const uint4 r = q < (int)lanes[l].size() ? lanes[l][q] : neutral;
+      out[((size_t)q * L + l) * 2] = uint2{r.x, r.y};
+      out[((size_t)q * L + l) * 2 + 1] = uint2{r.z, r.w};
+    }
+  return Qp;
+}
+
 static hc_status upload_tables(const CompiledSystem &cs, DevTables &t) {
-  hc_status s = upload_padded16((void **)&t.d_ops, cs.ops.data(), sizeof(uint2) * cs.ops.size());
+  // HC_OP_PAIRS=1: the paired op table (experiment switch until measured)
+  const char *ev = getenv("HC_OP_PAIRS");
+  std::vector<uint2> pops;
+  t.Qp = (ev && atoi(ev) == 1) ? pair_ops(cs, pops) : 0;
+  hc_status s = t.Qp ? upload_padded16((void **)&t.d_ops, pops.data(), sizeof(uint2) * pops.size())
+                     : upload_padded16((void **)&t.d_ops, cs.ops.data(), sizeof(uint2) * cs.ops.size());
   if (s == HC_OK) s = upload_padded16((void **)&t.d_mono_prog, cs.mono_prog.data(), sizeof(uint32_t) * cs.mono_prog.size());
   // device copy of the entry map: structural zeros point at the extra always-zero entry n_entries
   std::vector<int16_t> mp(cs.mpos);
@@ -630,7 +680,8 @@ static hc_status track_batch_impl(hc_system sys, const hc_tracker_settings *sett
   // ---- the fused tracker ----
   TrackArgs ta{};
   ta.ops = dt.d_ops;
-  ta.Q = cs.Q;
+  ta.Q = dt.Qp ? 2 * dt.Qp : cs.Q;
+  ta.Qp = dt.Qp;
   ta.mono_prog = dt.d_mono_prog;
   ta.n_mono = cs.n_mono;
   ta.n_levels = cs.n_levels;
@@ -719,7 +770,8 @@ static hc_status track_batch_impl(hc_system sys, const hc_tracker_settings *sett
       ea.coef_t = d_coef_e;
     }
     ea.ops = edt.d_ops;
-    ea.Q = ecs.Q;
+    ea.Q = edt.Qp ? 2 * edt.Qp : ecs.Q;
+    ea.Qp = edt.Qp;
     ea.mono_prog = edt.d_mono_prog;
     ea.n_mono = ecs.n_mono;
     ea.n_levels = ecs.n_levels;

@@ -57,11 +57,12 @@ __device__ __forceinline__ void endgame_body(const TrackArgs &A) {
   // (the tracker's per-lane state area is unused here)
   double2 *cval = reinterpret_cast<double2 *>(sb + EG_SAMPLE_BYTES + state_bytes(L));
   double2 *mono = cval + ncoef + A.ncoef_src;
-  double2 *M = mono + A.n_mono;
+  double2 *M = mono + A.n_mono + 1;   // (mono[n_mono]: the constant zero of paired op tables)
   double2 *prow = M + A.n_entries + 1;
   double *rabs = reinterpret_cast<double *>(prow + 2 * (N + 1));
   if (r == 0) {
     mono[N] = make_double2(1.0, 0.0);
+    mono[A.n_mono] = make_double2(0.0, 0.0);
     M[A.n_entries] = make_double2(0.0, 0.0);
   }
   __syncthreads();

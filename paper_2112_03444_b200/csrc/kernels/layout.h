@@ -9,7 +9,7 @@ namespace hcb {
 __host__ __device__ inline size_t align16(size_t b) { return (b + 15) & ~size_t(15); }
 
 // Per track slot: the endgame sampling state (80 bytes, EgSample), the shared-memory tracker state (state_bytes, below), cval[ncoef + ncoef_src]
-// (c(t) for every slot, c'(t) for the rhs slots), mono[n_mono] (x_0..x_{N-1}, 1, shared products),
+// (c(t) for every slot, c'(t) for the rhs slots), mono[n_mono + 1] (x_0..x_{N-1}, 1, shared products, a constant zero),
 // M[n_entries] (non-zero entries of [dH/dx | rhs]), prow[2 * (N + 1)] (double-buffered pivot row),
 // rabs[N] (doubles).
 constexpr size_t EG_SAMPLE_BYTES = 80;
@@ -21,7 +21,7 @@ __host__ __device__ constexpr int state_lanes(int N, int L, int NC) { return (NC
 __host__ __device__ inline size_t state_bytes(int lnc) { return lnc ? (size_t)48 * lnc + 64 : 0; }
 __host__ __device__ inline size_t slot_bytes(int N, int lnc, int ncoef, int ncoef_src, int n_mono, int n_entries) {
   return EG_SAMPLE_BYTES + state_bytes(lnc) +
-         align16(sizeof(double) * 2 * ((size_t)ncoef + ncoef_src + n_mono + n_entries + 2 * (N + 1)) +
+         align16(sizeof(double) * 2 * ((size_t)ncoef + ncoef_src + n_mono + 1 + n_entries + 2 * (N + 1)) +
                  sizeof(double) * N);
 }
 

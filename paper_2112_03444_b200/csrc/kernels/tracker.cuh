@@ -608,6 +608,61 @@ __device__ __forceinline__ void run_ops(const uint2 *__restrict__ ops_s, int Q, 
   }
 }
 
+// Paired op table (TrackArgs::Qp > 0, abi.cpp pair_ops): a record holds two terms of the same entry
+// (x: slot_a | mono_a << 16, y: slot_b | mono_b << 16, z: dest | flags << 16), an odd entry's last
+// record pairs its term with the constant-zero monomial.  The record decode, the rhs select and the
+// entry-end bookkeeping (store + reset) are paid once per two terms.  Blocks of 2 records (4 terms).
+template <int N, int L, bool ABS>
+__device__ __forceinline__ void run_ops_pairs(const uint4 *__restrict__ ops4, int Q2, int rhs_off,
+                                              const double2 *__restrict__ cval, const double2 *__restrict__ mono,
+                                              double2 *__restrict__ M, double *__restrict__ rabs,
+                                              const int16_t *row_of, int r) {
+  double2 acc = make_double2(0.0, 0.0), acc2 = make_double2(0.0, 0.0);
+  double acc_abs = 0.0;
+  auto pair_step = [&](uint4 o, double2 ca, double2 ma, double2 cb, double2 mb) {
+    if (ABS) acc_abs += sqrt(abs2(cmul(ca, ma))) + sqrt(abs2(cmul(cb, mb)));
+    acc.x = fma(ca.x, ma.x, acc.x);
+    acc.y = fma(ca.x, ma.y, acc.y);
+    acc2.x = fma(-ca.y, ma.y, acc2.x);
+    acc2.y = fma(ca.y, ma.x, acc2.y);
+    acc.x = fma(cb.x, mb.x, acc.x);
+    acc.y = fma(cb.x, mb.y, acc.y);
+    acc2.x = fma(-cb.y, mb.y, acc2.x);
+    acc2.y = fma(cb.y, mb.x, acc2.y);
+    const uint32_t fl = o.z >> 16;
+    if (fl & OP_LAST) {
+      const uint32_t dest = o.z & 0xFFFFu;
+      M[dest] = make_double2(acc.x + acc2.x, acc.y + acc2.y);
+      if (ABS && (fl & OP_RHS)) rabs[row_of[dest]] = acc_abs;
+      acc = make_double2(0.0, 0.0);
+      acc2 = make_double2(0.0, 0.0);
+      acc_abs = 0.0;
+    }
+  };
+  int q = 0;
+  for (; q + 2 <= Q2; q += 2) {
+    uint4 op[2];
+    double2 c[4], m[4];
+#pragma unroll
+    for (int i = 0; i < 2; ++i) op[i] = ops4[(q + i) * L + r];
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+      const int roff = ((op[i].z >> 16) & OP_RHS) ? rhs_off : 0;
+      c[2 * i] = cval[(int)(op[i].x & 0xFFFFu) + roff];
+      m[2 * i] = mono[op[i].x >> 16];
+      c[2 * i + 1] = cval[(int)(op[i].y & 0xFFFFu) + roff];
+      m[2 * i + 1] = mono[op[i].y >> 16];
+    }
+#pragma unroll
+    for (int i = 0; i < 2; ++i) pair_step(op[i], c[2 * i], m[2 * i], c[2 * i + 1], m[2 * i + 1]);
+  }
+  if (q < Q2) {
+    const uint4 o = ops4[q * L + r];
+    const int roff = ((o.z >> 16) & OP_RHS) ? rhs_off : 0;
+    pair_step(o, cval[(int)(o.x & 0xFFFFu) + roff], mono[o.x >> 16], cval[(int)(o.y & 0xFFFFu) + roff], mono[o.y >> 16]);
+  }
+}
+
 // ------------------------------------------------------------------------------------------
 // Coefficient values at t: c_j(t) for every slot and c_j'(t) for the rhs slots (j < nsrc), by
 // Horner on the prologue's polynomials coef_t[d][j] (d <= D); two slots per lane per iteration,
@@ -737,7 +792,11 @@ __device__ __forceinline__ bool eval_solve(const TrackArgs &A, const uint2 *__re
   HCB_T(c2);
   HCB_ACC(1, c1, c2);
   // ---- homogenised term evaluation, lane-balanced op list ----
-  if (want_abs) run_ops<N, L, true>(ops_s, A.Q, rhs_off, cval, mono, M, rabs, row_of, r);
+  if (A.Qp > 0) {   // paired op table (uniform)
+    const uint4 *ops4 = reinterpret_cast<const uint4 *>(ops_s);
+    if (want_abs) run_ops_pairs<N, L, true>(ops4, A.Qp, rhs_off, cval, mono, M, rabs, row_of, r);
+    else run_ops_pairs<N, L, false>(ops4, A.Qp, rhs_off, cval, mono, M, rabs, row_of, r);
+  } else if (want_abs) run_ops<N, L, true>(ops_s, A.Q, rhs_off, cval, mono, M, rabs, row_of, r);
   else run_ops<N, L, false>(ops_s, A.Q, rhs_off, cval, mono, M, rabs, row_of, r);
   __syncwarp();
   HCB_T(c3);
@@ -847,11 +906,12 @@ __device__ __forceinline__ void track_body(const TrackArgs &A) {
   int *s_cnt = reinterpret_cast<int *>(s_dt + 4);       // steps, rej, newt, acc
   double2 *cval = reinterpret_cast<double2 *>(reinterpret_cast<unsigned char *>(vstate) + state_bytes(LNC));
   double2 *mono = cval + ncoef + A.ncoef_src;
-  double2 *M = mono + A.n_mono;
+  double2 *M = mono + A.n_mono + 1;   // (mono[n_mono]: the constant zero of paired op tables)
   double2 *prow = M + A.n_entries + 1;
   double *rabs = reinterpret_cast<double *>(prow + 2 * (N + 1));
   if (r == 0) {
     mono[N] = make_double2(1.0, 0.0);            // constant-one slot
+    mono[A.n_mono] = make_double2(0.0, 0.0);     // constant zero (pad term of paired op tables)
     M[A.n_entries] = make_double2(0.0, 0.0);     // the entry every structural zero reads
   }
   __syncthreads();                   // (the barrier's initialisation is visible to every waiter)
