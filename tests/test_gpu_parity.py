@@ -6,6 +6,7 @@ distinct endpoints and nearest-neighbour agreement within 1e-8 relative per coor
 compared element-wise ("parity unpinned": FMA contraction and summation order differ).
 """
 import numpy as np
+import torch
 import pytest
 
 from hc_inputs import fixtures, rng, systems
@@ -324,6 +325,27 @@ def test_lane_layouts_parity(hc, orc, monkeypatch, lanes):
     for b in range(3):
         A = orc.dedup(orc.finite_solutions(ref, b))[0]
         assert_same_set_r21(orc, d, p1s[b], A, gpu_set(orc, res, b), f"4-view {b} ({lanes})")
+
+
+def test_lane_layout_setting_pins_layout_and_bits(hc, monkeypatch):
+    """hc_tracker_settings.lane_layout pins the layout whatever the batch size (include/hc.h,
+    Determinism): a 4-view instance gives identical bits alone and inside a 64-instance batch when
+    the layout is pinned (throughput or wide); the auto choice differs between those batch sizes."""
+    monkeypatch.delenv("HC_LANES", raising=False)
+    d = systems.nview_triangulation(4)
+    start = fixtures.read_solutions(fixtures.fixture_path("fourview_start.sols"))
+    p0 = fixtures.read_params(fixtures.fixture_path("fourview_p0.params"))
+    p1s, _ = rng.fourview_batch(64)
+    assert run_ph(hc, d, start, p0, p1s[:1]).launch()["lanes_per_track"] == 32     # auto: wide when small
+    assert run_ph(hc, d, start, p0, p1s).launch()["lanes_per_track"] == 16        # auto: throughput
+    for layout, lanes in ((hc.HC_LAYOUT_THROUGHPUT, 16), (hc.HC_LAYOUT_WIDE, 32)):
+        st = hc.settings(lane_layout=layout)
+        one, full = run_ph(hc, d, start, p0, p1s[:1], st=st), run_ph(hc, d, start, p0, p1s, st=st)
+        assert one.launch()["lanes_per_track"] == lanes and full.launch()["lanes_per_track"] == lanes
+        assert torch.equal(torch.view_as_real(one.x[0]), torch.view_as_real(full.x[0]))
+        assert torch.equal(one.status[0], full.status[0]) and torch.equal(one.counters[0], full.counters[0])
+    with pytest.raises(hc.HCError):
+        run_ph(hc, d, start, p0, p1s[:1], st=hc.settings(lane_layout=7))
 
 
 def test_lane_layout_policy(hc, monkeypatch):
