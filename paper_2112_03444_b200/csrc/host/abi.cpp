@@ -216,36 +216,43 @@ static hc_status upload_padded16(void **dst, const void *src, size_t bytes) {
   return HC_OK;
 }
 
-// Paired op table (tracker.cuh run_ops_pairs): per lane, the ops of each entry two at a time in one
-// 16-byte record {slot_a | mono_a << 16, slot_b | mono_b << 16, dest | flags << 16, 0}; an odd
-// entry's last record pairs its term with the constant-zero monomial mono[n_mono] (same slot, so
-// the coefficient is finite and the term exactly 0); lanes past their last entry get neutral
-// records.  Returns the pair steps Qp; the table is [Qp][L] records (2 uint2 each).
+// Paired op table (tracker.cuh run_ops_pairs): the ops of each entry two at a time in one 16-byte
+// record {slot_a | mono_a << 16, slot_b | mono_b << 16, dest | flags << 16, 0}; an odd entry's last
+// record pairs its term with the constant-zero monomial mono[n_mono] (same slot, so the coefficient
+// is finite and the term exactly 0); entries re-balanced over the lanes by record count; lanes past
+// their last entry get neutral records.  Returns the pair steps Qp; the table is [Qp][L] records.
 static int pair_ops(const CompiledSystem &cs, std::vector<uint2> &out) {
   const int L = cs.L, Q = cs.Q;
-  std::vector<std::vector<uint4>> lanes(L);
+  // the entries (op runs ending in OP_LAST) of every lane; the compiler's never-stored padding ops
+  // after a lane's last entry are dropped
+  std::vector<std::vector<uint2>> entries;
   for (int l = 0; l < L; ++l) {
     std::vector<uint2> cur;
     for (int q = 0; q < Q; ++q) {
       const uint2 o = cs.ops[(size_t)q * L + l];
-      const uint32_t fl = o.y >> 16;
       cur.push_back(o);
-      if (!(fl & OP_LAST)) continue;
-      for (size_t i = 0; i < cur.size(); i += 2) {
-        const uint2 a = cur[i];
-        const bool has_b = i + 1 < cur.size();
-        const uint2 b = has_b ? cur[i + 1] : uint2{(a.x & 0xFFFFu) | ((uint32_t)cs.n_mono << 16), 0u};
-        const bool last = i + 2 >= cur.size();
-        uint4 rec;
-        rec.x = a.x;
-        rec.y = b.x;
-        rec.z = last ? o.y : (OP_NO_DEST | ((fl & OP_RHS) << 16));
-        rec.w = 0u;
-        lanes[l].push_back(rec);
+      if ((o.y >> 16) & OP_LAST) {
+        entries.push_back(cur);
+        cur.clear();
       }
-      cur.clear();
     }
-    // (trailing ops without OP_LAST are the compiler's never-stored padding: dropped)
+  }
+  // re-balance over the lanes by record count (LPT, longest first; stable, deterministic)
+  std::stable_sort(entries.begin(), entries.end(),
+                   [](const std::vector<uint2> &a, const std::vector<uint2> &b) { return a.size() > b.size(); });
+  std::vector<std::vector<uint4>> lanes(L);
+  for (const auto &e : entries) {
+    int l = 0;
+    for (int k = 1; k < L; ++k)
+      if (lanes[k].size() < lanes[l].size()) l = k;
+    const uint32_t fl = e.back().y >> 16;
+    for (size_t i = 0; i < e.size(); i += 2) {
+      const uint2 a = e[i];
+      const bool has_b = i + 1 < e.size();
+      const uint2 b = has_b ? e[i + 1] : uint2{(a.x & 0xFFFFu) | ((uint32_t)cs.n_mono << 16), 0u};
+      const bool last = i + 2 >= e.size();
+      lanes[l].push_back(uint4{a.x, b.x, last ? e.back().y : (OP_NO_DEST | ((fl & OP_RHS) << 16)), 0u});
+    }
   }
   int Qp = 0;
   for (auto &v : lanes) Qp = std::max(Qp, (int)v.size());

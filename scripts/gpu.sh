@@ -12,6 +12,7 @@
 #                              previous commit's, built locally into abl/); the AB_CFGS step times
 #   phase                      per-phase cycle breakdown (HCB_VARIANT=timing build), trifocal and 4-view
 #   sanitize                   compute-sanitizer memcheck / racecheck / synccheck over small cases of every path
+#                              (closed on the round-2 GPU pool: "runs under it have left GPUs needing a reset")
 #   traffic                    DRAM bytes per launch (ncu) for trifocal and 4-view
 #   zgesv                      Fig. 3 re-run (N1): fused batched LU vs cuBLAS getrf/getrsBatched
 #   env VAR=VAL ...            the AB_CFGS configs with the product library under each environment setting
