@@ -267,11 +267,15 @@ static int pair_ops(const CompiledSystem &cs, std::vector<uint2> &out) {
   return Qp;
 }
 
-static hc_status upload_tables(const CompiledSystem &cs, DevTables &t) {
-  // HC_OP_PAIRS=1: the paired op table (experiment switch until measured)
+static hc_status upload_tables(const CompiledSystem &cs, DevTables &t, bool wide) {
+  // Paired op table for the wide latency layout (A/B: katsura-6 1.50 -> 1.44 ms, cyclic-7 TD 8.2 ->
+  // 7.7 ms: half the op-list iterations on a latency-bound chain), single ops for the throughput
+  // layout (trifocal -3.5 %, 4-view -5.5 %, 5-point -5 % with pairs: the padding terms' extra work
+  // and the gathers' bank pattern cost more than the saved bookkeeping).  HC_OP_PAIRS=0|1 overrides.
   const char *ev = getenv("HC_OP_PAIRS");
+  const bool pairs = ev ? atoi(ev) == 1 : wide;
   std::vector<uint2> pops;
-  t.Qp = (ev && atoi(ev) == 1) ? pair_ops(cs, pops) : 0;
+  t.Qp = pairs ? pair_ops(cs, pops) : 0;
   hc_status s = t.Qp ? upload_padded16((void **)&t.d_ops, pops.data(), sizeof(uint2) * pops.size())
                      : upload_padded16((void **)&t.d_ops, cs.ops.data(), sizeof(uint2) * cs.ops.size());
   if (s == HC_OK) s = upload_padded16((void **)&t.d_mono_prog, cs.mono_prog.data(), sizeof(uint32_t) * cs.mono_prog.size());
@@ -291,8 +295,8 @@ static hc_status upload_tables(const CompiledSystem &cs, DevTables &t) {
 
 static hc_status upload_system(hc_system sys) {
   CK(cudaSetDevice(sys->device));
-  hc_status s = upload_tables(sys->cs, sys->dt);
-  if (s == HC_OK && sys->has_wide) s = upload_tables(sys->cs_w, sys->dt_w);
+  hc_status s = upload_tables(sys->cs, sys->dt, sys->cs.L == 32 && sys->cs.N <= 16);
+  if (s == HC_OK && sys->has_wide) s = upload_tables(sys->cs_w, sys->dt_w, true);
   return s;
 }
 
