@@ -295,7 +295,7 @@ static hc_status upload_tables(const CompiledSystem &cs, DevTables &t, bool wide
 
 static hc_status upload_system(hc_system sys) {
   CK(cudaSetDevice(sys->device));
-  hc_status s = upload_tables(sys->cs, sys->dt, sys->cs.L == 32 && sys->cs.N <= 16);
+  hc_status s = upload_tables(sys->cs, sys->dt, false);
   if (s == HC_OK && sys->has_wide) s = upload_tables(sys->cs_w, sys->dt_w, true);
   return s;
 }
