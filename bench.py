@@ -296,10 +296,16 @@ def run_ours(args):
            torch.empty((B, S, 2), dtype=torch.float64, device=dev),
            torch.empty((B, S), dtype=torch.int32, device=dev))   # Cauchy endgame winding numbers
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)   # 256 MB > 126 MB L2
+    # --flush-clean (traffic measurements only): a second 256 MB buffer read after the write flush
+    # evicts the flush's dirty lines before the kernel, so the kernel's DRAM counters see only its own
+    # write-backs
+    flush_rd = torch.ones(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev) if args.flush_clean else None
     stream = torch.cuda.current_stream(dev)
 
     def step():
         flush.fill_(1.0)   # L2 flush between steps (outside our kernels)
+        if flush_rd is not None:
+            flush_rd.sum()
         return hc.track_batch(sysh, x_start, t_p0, t_p1, st=st, stream=stream, out=out)
 
     # warm-up: the same hot path on the first `warmup_instances` instances of the batch (module load,
@@ -470,6 +476,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--gather", action="store_true", help="init NCCL and run the final gather even on 1 GPU")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--flush-clean", action="store_true", help="(traffic measurements) read a second buffer after the L2 flush")
     ap.add_argument("--cpu-budget-s", type=float, default=15.0)
     ap.add_argument("--ref-step-s", type=float, default=10.0)
     args = ap.parse_args()

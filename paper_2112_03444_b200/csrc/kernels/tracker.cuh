@@ -108,7 +108,7 @@ __device__ __forceinline__ double2 shfl2(double2 v, int src, int width) {
 }
 
 #ifndef HCB_OUT_EXPERIMENT   // DRAM-traffic experiments (scripts/gpu.sh traffic_ab): 1 = no status/counter/
-#define HCB_OUT_EXPERIMENT 0  // residual writes, 2 = no x writes (results invalid), 3 = L2 evict_last stores
+#define HCB_OUT_EXPERIMENT 0  // residual writes, 2 = no x writes (results invalid)
 #endif
 #ifndef HCB_EG_SAMPLING   // endgame sampling in the tracker (A/B switch; 0 = no endgame hand-off)
 #define HCB_EG_SAMPLING 1
@@ -979,26 +979,6 @@ __device__ __forceinline__ void track_body(const TrackArgs &A) {
   };
   auto finish = [&](int status, double ra, double rr) {
 #pragma unroll
-#if HCB_OUT_EXPERIMENT == 3   // outputs stored with an L2 evict_last policy (traffic experiment)
-    unsigned long long pol;
-    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
-#pragma unroll
-    for (int c = 0; c < NC; ++c)
-      if (comp_valid(c)) {
-        const double2 v = x[c];
-        asm volatile("st.global.L2::cache_hint.v2.f64 [%0], {%1, %2}, %3;" ::"l"(&A.x_out[(size_t)g * N + comp_row(c)]),
-                     "d"(v.x), "d"(v.y), "l"(pol) : "memory");
-      }
-    if (r == 0) {
-      asm volatile("st.global.L2::cache_hint.s32 [%0], %1, %2;" ::"l"(&A.status_out[g]), "r"(status), "l"(pol) : "memory");
-      asm volatile("st.global.L2::cache_hint.v4.s32 [%0], {%1, %2, %3, %4}, %5;" ::"l"(&A.counters_out[4 * g]), "r"(steps),
-                   "r"(rej), "r"(newt), "r"(solves), "l"(pol) : "memory");
-      asm volatile("st.global.L2::cache_hint.v2.f64 [%0], {%1, %2}, %3;" ::"l"(&A.resid_out[2 * g]), "d"(ra), "d"(rr),
-                   "l"(pol) : "memory");
-      if (A.winding_out)
-        asm volatile("st.global.L2::cache_hint.s32 [%0], %1, %2;" ::"l"(&A.winding_out[g]), "r"(0), "l"(pol) : "memory");
-    }
-#else
     for (int c = 0; c < NC; ++c)
       if (comp_valid(c) && HCB_OUT_EXPERIMENT != 2) A.x_out[(size_t)g * N + comp_row(c)] = x[c];
     if (r == 0 && HCB_OUT_EXPERIMENT != 1) {
@@ -1007,7 +987,6 @@ __device__ __forceinline__ void track_body(const TrackArgs &A) {
       reinterpret_cast<double2 *>(A.resid_out)[g] = make_double2(ra, rr);
       if (A.winding_out) A.winding_out[g] = 0;
     }
-#endif
     if (r == 0) {
       // a singular endpoint (reading R26): the Cauchy endgame kernel continues this track from
       // (x, t = 1 - ra) with step rr; the list entry is the track id

@@ -74,15 +74,14 @@ while [ $# -gt 0 ]; do
         echo "== $tool exit $?"; tail -4 gpurun_out/sanitizer_$tool.log
       done ;;
     traffic)
-      timeout 900 python scripts/record_traffic.py trifocal ${TRAFFIC_TRI_B:-1024} gpurun_out/traffic.json >> gpurun_out/traffic.log 2>&1
+      timeout 900 python scripts/record_traffic.py trifocal ${TRAFFIC_TRI_B:-1024} gpurun_out/traffic.json --dram-only >> gpurun_out/traffic.log 2>&1
       timeout 600 python scripts/record_traffic.py fourview 1024 gpurun_out/traffic.json >> gpurun_out/traffic.log 2>&1
       tail -2 gpurun_out/traffic.log ;;
     traffic_ab)   # DRAM bytes of trifocal x256 with the small per-track outputs / the x output not written
       HCB_VARIANT=out1 HCB_DEFINES="HCB_OUT_EXPERIMENT=1" python paper_2112_03444_b200/build.py > /dev/null
       HCB_VARIANT=out2 HCB_DEFINES="HCB_OUT_EXPERIMENT=2" python paper_2112_03444_b200/build.py > /dev/null
-      HCB_VARIANT=out3 HCB_DEFINES="HCB_OUT_EXPERIMENT=3" python paper_2112_03444_b200/build.py > /dev/null
-      for v in ${TRAFFIC_LIBS:-lib lib_out1 lib_out2 lib_out3}; do
-        HC_LIB_PATH=paper_2112_03444_b200/$v/libhc.so timeout 900 python scripts/record_traffic.py trifocal 256 gpurun_out/traffic_$v.json \
+      for v in ${TRAFFIC_LIBS:-lib lib_out1 lib_out2}; do
+        HC_LIB_PATH=paper_2112_03444_b200/$v/libhc.so timeout 900 python scripts/record_traffic.py trifocal 256 gpurun_out/traffic_$v.json --dram-only \
           >> gpurun_out/traffic_ab.log 2>&1
         python -c "import json; d=json.load(open('gpurun_out/traffic_$v.json')); v=list(d.values())[0]; print('TRAFFIC', '$v', v['read'] / v['tracks'], v['write'] / v['tracks'])"
       done | tee -a gpurun_out/traffic_ab.log ;;

@@ -1,6 +1,6 @@
 """Capture the tracker kernel's DRAM traffic per launch with ncu for one bench workload.
 
-  python scripts/record_traffic.py <config> <instances> [out.json]
+  python scripts/record_traffic.py <config> <instances> [out.json] [--dram-only]
 
 Runs `bench.py --config C --instances B --steps 1 --warmup 3` under
 `ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum` plus the FP64
@@ -20,16 +20,19 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
 def main():
-    cfg, B = sys.argv[1], int(sys.argv[2])
-    out = sys.argv[3] if len(sys.argv) > 3 else os.path.join(ROOT, "gpurun_out", "traffic.json")
-    metrics = ["dram__bytes_read.sum", "dram__bytes_write.sum", "gpu__time_duration.sum",
-               "smsp__sass_thread_inst_executed_op_dfma_pred_on.sum",
-               "smsp__sass_thread_inst_executed_op_dmul_pred_on.sum",
-               "smsp__sass_thread_inst_executed_op_dadd_pred_on.sum"]
+    args = [a for a in sys.argv[1:] if not a.startswith("--")]
+    dram_only = "--dram-only" in sys.argv   # one replay pass (the SASS counters instrument the kernel: slow)
+    cfg, B = args[0], int(args[1])
+    out = args[2] if len(args) > 2 else os.path.join(ROOT, "gpurun_out", "traffic.json")
+    metrics = ["dram__bytes_read.sum", "dram__bytes_write.sum", "gpu__time_duration.sum"]
+    if not dram_only:
+        metrics += ["smsp__sass_thread_inst_executed_op_dfma_pred_on.sum",
+                    "smsp__sass_thread_inst_executed_op_dmul_pred_on.sum",
+                    "smsp__sass_thread_inst_executed_op_dadd_pred_on.sum"]
     cmd = ["ncu", "--metrics", ",".join(metrics),
            "--clock-control", "none", "-k", "regex:hc_track_kernel", "--launch-skip", "3", "-c", "1", "--csv",
            sys.executable, os.path.join(ROOT, "bench.py"), "--config", cfg, "--instances", str(B), "--steps", "1",
-           "--warmup", "3", "--no-cpu-baseline", "--no-e2e"]
+           "--warmup", "3", "--no-cpu-baseline", "--no-e2e", "--flush-clean"]
     p = subprocess.run(cmd, capture_output=True, text=True, cwd=ROOT)
     txt = p.stdout
     bench_line = None
@@ -64,7 +67,8 @@ def main():
                 + vals.get("smsp__sass_thread_inst_executed_op_dadd_pred_on.sum", 0),
                 "flops_algorithmic": bench_line["roofline"]["flops_per_launch"],
                 "source": "ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum "
-                                          "(scripts/record_traffic.py), first full-batch launch"}
+                                          "(scripts/record_traffic.py), first full-batch launch, the L2 flush's dirty lines "
+                                          "evicted before it (bench --flush-clean)"}
     os.makedirs(os.path.dirname(out), exist_ok=True)
     json.dump(rec, open(out, "w"), indent=1)
     print(key, rec[key])
