@@ -4,6 +4,7 @@
 #include <cstdlib>
 #include <cstdio>
 #include <cstring>
+#include <mutex>
 #include <new>
 #include <string>
 #include <vector>
@@ -131,8 +132,9 @@ struct hc_result_s {
   int64_t B = 0, S = 0, total = 0;
   int memory = HC_MEM_DEVICE;
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};   // prologue start, tracker start, end, endgame start
-  // device buffers owned by the result (freed on destroy)
-  std::vector<void *> owned;
+  // device buffers owned by the result (freed on destroy), and per-batch temporaries (freed in
+  // stream order once the batch's kernels are enqueued; on destroy if the enqueue failed)
+  std::vector<void *> owned, temps;
   // where the outputs are (device or host)
   hc_complex *x = nullptr;
   int32_t *status = nullptr, *counters = nullptr;
@@ -148,6 +150,7 @@ static void destroy_result(hc_result r) {
   if (!r) return;
   cudaSetDevice(r->device);
   for (void *p : r->owned) cudaFreeAsync(p, r->stream);
+  for (void *p : r->temps) cudaFreeAsync(p, r->stream);
   for (auto &e : r->ev)
     if (e) cudaEventDestroy(e);
   if (r->outputs_on_host) {
@@ -155,12 +158,41 @@ static void destroy_result(hc_result r) {
   delete r;
 }
 
+// The library's stream-ordered memory pool per device: memory freed by a batch stays in the pool
+// (release threshold 4 GiB) for the next batch, so steady-state calls allocate without mapping new
+// pages (the default pool returns everything at each synchronisation).
+static cudaMemPool_t lib_pool(int device) {
+  static std::mutex mu;
+  static std::vector<cudaMemPool_t> pools;
+  std::lock_guard<std::mutex> lock(mu);
+  if ((int)pools.size() <= device) pools.resize(device + 1, nullptr);
+  if (!pools[device]) {
+    cudaMemPoolProps props{};
+    props.allocType = cudaMemAllocationTypePinned;
+    props.location.type = cudaMemLocationTypeDevice;
+    props.location.id = device;
+    cudaMemPool_t pool = nullptr;
+    if (cudaMemPoolCreate(&pool, &props) != cudaSuccess) {
+      (void)cudaGetLastError();
+      return nullptr;   // fall back to the device's default pool
+    }
+    uint64_t thr = 4ull << 30;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    pools[device] = pool;
+  }
+  return pools[device];
+}
+
+// temp: a per-batch temporary, released in stream order right after the batch's kernels are
+// enqueued (hc_track_batch), not when the result is destroyed
 template <class T>
-static hc_status dev_alloc(hc_result r, T **p, size_t count) {
+static hc_status dev_alloc(hc_result r, T **p, size_t count, bool temp = false) {
   void *q = nullptr;
-  cudaError_t e = cudaMallocAsync(&q, std::max<size_t>(1, count) * sizeof(T), r->stream);
+  const size_t bytes = std::max<size_t>(1, count) * sizeof(T);
+  cudaMemPool_t pool = lib_pool(r->device);
+  cudaError_t e = pool ? cudaMallocFromPoolAsync(&q, bytes, pool, r->stream) : cudaMallocAsync(&q, bytes, r->stream);
   if (e != cudaSuccess) return cuda_fail(e, "cudaMallocAsync");
-  r->owned.push_back(q);
+  (temp ? r->temps : r->owned).push_back(q);
   *p = reinterpret_cast<T *>(q);
   return HC_OK;
 }
@@ -629,13 +661,13 @@ static hc_status track_batch_impl(hc_system sys, const hc_tracker_settings *sett
   double *d_resid = bt->resid_out;
   if (host) {
     double2 *a, *b0 = nullptr, *b1 = nullptr;
-    if ((s = dev_alloc(r, &a, (size_t)S * N)) != HC_OK) return bail(s);
+    if ((s = dev_alloc(r, &a, (size_t)S * N, true)) != HC_OK) return bail(s);
     if (cudaMemcpyAsync(a, bt->start_x, sizeof(double2) * S * N, cudaMemcpyHostToDevice, r->stream) != cudaSuccess)
       return bail(cuda_fail(cudaGetLastError(), "H2D start_x"));
     d_start = a;
     if (P > 0) {
-      if ((s = dev_alloc(r, &b0, (size_t)P)) != HC_OK) return bail(s);
-      if ((s = dev_alloc(r, &b1, (size_t)B * P)) != HC_OK) return bail(s);
+      if ((s = dev_alloc(r, &b0, (size_t)P, true)) != HC_OK) return bail(s);
+      if ((s = dev_alloc(r, &b1, (size_t)B * P, true)) != HC_OK) return bail(s);
       if (cudaMemcpyAsync(b0, bt->p_start, sizeof(double2) * P, cudaMemcpyHostToDevice, r->stream) != cudaSuccess ||
           cudaMemcpyAsync(b1, bt->p_target, sizeof(double2) * B * P, cudaMemcpyHostToDevice, r->stream) != cudaSuccess)
         return bail(cuda_fail(cudaGetLastError(), "H2D params"));
@@ -655,17 +687,17 @@ static hc_status track_batch_impl(hc_system sys, const hc_tracker_settings *sett
   if (!d_resid && (s = dev_alloc(r, &d_resid, (size_t)total * 2)) != HC_OK) return bail(s);
   double2 *d_coef = nullptr;
   unsigned long long *d_queue = nullptr;
-  if ((s = dev_alloc(r, &d_coef, (size_t)B * (cs.D + 1) * cs.ncoef)) != HC_OK) return bail(s);
+  if ((s = dev_alloc(r, &d_coef, (size_t)B * (cs.D + 1) * cs.ncoef, true)) != HC_OK) return bail(s);
   // work counters: [0] the tracker's queue, [1] tracks handed to the endgame, [2] the endgame's queue
-  if ((s = dev_alloc(r, &d_queue, 3)) != HC_OK) return bail(s);
+  if ((s = dev_alloc(r, &d_queue, 3, true)) != HC_OK) return bail(s);
   if (cudaMemsetAsync(d_queue, 0, 3 * sizeof(unsigned long long), r->stream) != cudaSuccess)
     return bail(cuda_fail(cudaGetLastError(), "memset queue"));
   int64_t *d_eg_list = nullptr;
-  if (st.eg_start > 0.0 && (s = dev_alloc(r, &d_eg_list, (size_t)total)) != HC_OK) return bail(s);
+  if (st.eg_start > 0.0 && (s = dev_alloc(r, &d_eg_list, (size_t)total, true)) != HC_OK) return bail(s);
   // P == 0: coefficients are constants; feed the prologue a dummy parameter vector
   double2 *d_dummy = nullptr;
   if (P == 0) {
-    if ((s = dev_alloc(r, &d_dummy, 1)) != HC_OK) return bail(s);
+    if ((s = dev_alloc(r, &d_dummy, 1, true)) != HC_OK) return bail(s);
     d_p0 = d_dummy;
     d_p1 = d_dummy;
   }
@@ -769,7 +801,7 @@ static hc_status track_batch_impl(hc_system sys, const hc_tracker_settings *sett
     TrackArgs ea = ta;
     if (eg_wide != wide) {
       double2 *d_coef_e = nullptr;
-      if ((s = dev_alloc(r, &d_coef_e, (size_t)B * (ecs.D + 1) * ecs.ncoef)) != HC_OK) return bail(s);
+      if ((s = dev_alloc(r, &d_coef_e, (size_t)B * (ecs.D + 1) * ecs.ncoef, true)) != HC_OK) return bail(s);
       PrologueArgs pe = pa;
       pe.mono = edt.d_mono;
       pe.coef_mono_ptr = edt.d_mono_ptr;
@@ -798,6 +830,10 @@ static hc_status track_batch_impl(hc_system sys, const hc_tracker_settings *sett
     if (e != cudaSuccess) return bail(cuda_fail(e, "endgame launch"));
   }
   cudaEventRecord(r->ev[2], r->stream);
+  // per-batch temporaries (coefficient tables, work counters, endgame list, staged inputs): released
+  // in stream order now, so the next batch on this stream reuses them from the pool
+  for (void *p : r->temps) cudaFreeAsync(p, r->stream);
+  r->temps.clear();
 
   if (host) {
     if (bt->x_out &&
