@@ -27,7 +27,7 @@ if len(sys.argv) > 1 and sys.argv[1] == "--print":
     sys.exit(0)
 cfg = sys.argv[1] if len(sys.argv) > 1 else "trifocal"
 B = int(sys.argv[2]) if len(sys.argv) > 2 else 64
-d, start, p0, p1s, _, _ = bench.make_workload(cfg, B, 0)
+d, start, p0, p1s, _, _ = bench.make_workload(cfg, 0, B)
 s = hc.System(d, device=0)
 res = hc.track_batch(s, start, p0, p1s)
 res.wait()
