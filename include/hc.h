@@ -24,6 +24,10 @@
  *    thread-local message for the last failing call.  A per-track numerical failure is
  *    never an error: it is reported in the track's status ("the batch call never fails
  *    wholesale").
+ *  - Device memory: the library allocates its per-batch buffers stream-ordered from its own memory
+ *    pool per device (release threshold 4 GiB, so back-to-back batches reuse it); temporaries are
+ *    released in stream order when the batch's kernels are enqueued, result-owned outputs by
+ *    hc_result_destroy.
  *  - Determinism: a track's arithmetic depends only on its inputs and the lane layout, never on
  *    scheduling, CTA shape, batch size or GPU count: identical inputs in the same layout give
  *    identical output bits.  For N <= 16 the default layout choice (HC_LAYOUT_AUTO) depends on
