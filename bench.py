@@ -162,9 +162,17 @@ def oracle_sample(name: str, budget_s: float, nthreads: int | None = None):
         from hc_inputs import rng
         hom = oracle.td_homotopy(d, rng.gamma(2))
         start = oracle.td_start(d.degrees())
+        # estimate the whole solve's time from an evenly strided probe first (eco-12 on one thread
+        # would take ~15 min), then time the whole solve only when it fits the budget
+        probe = min(start.shape[0], 16 * nthreads)
+        pidx = np.linspace(0, start.shape[0] - 1, probe).astype(np.int64)
         t = time.perf_counter()
-        oracle.track(hom, start, nthreads=nthreads)
-        d1 = time.perf_counter() - t
+        oracle.track(hom, start[pidx], nthreads=nthreads)
+        d1 = (time.perf_counter() - t) * start.shape[0] / probe
+        if d1 <= budget_s:
+            t = time.perf_counter()
+            oracle.track(hom, start, nthreads=nthreads)
+            d1 = time.perf_counter() - t
         reps = int(min(1000, max(1, budget_s / max(d1, 1e-4))))
         if d1 > budget_s:   # eco-12 (118,098 tracks): a strided subset
             m = max(nthreads * 4, int(start.shape[0] * budget_s / d1))

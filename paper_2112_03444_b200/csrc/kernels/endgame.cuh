@@ -238,8 +238,15 @@ __device__ __forceinline__ void endgame_body(const TrackArgs &A) {
     cval_t = te;
     double2 xa[1] = {xe}, yv[1], fr[1];
     double fa[1];
+#ifdef HCB_PHASE_TIMING
+    unsigned long long hcb_phase[8] = {0, 0, 0, 0, 0, 0, 0, 0};   // (the phase build times the tracker only)
+#endif
     const bool ok = eval_solve<N, L, 1>(A, ops_s, prog_s, mpos_s, row_of, ct, te, need_coef, rhs_off, want_abs, cval,
-                                        mono, M, prow, rabs, r, seg, xa, yv, fr, fa);
+                                        mono, M, prow, rabs, r, seg, xa, yv, fr, fa
+#ifdef HCB_PHASE_TIMING
+                                        , hcb_phase
+#endif
+                                        );
     const double2 y = yv[0];
 
     // ---- slot-uniform reductions (all lanes, before any slot-divergent branch) ----
