@@ -470,7 +470,7 @@ static void fill_info(const CompiledSystem &cs, hc_system_info *o) {
   o->flops_eval_kernel = cs.flops_eval_kernel;
   o->flops_solve_kernel = cs.flops_solve_kernel;
   // (the tracker keeps its per-lane state in shared memory when its CTA shape is 16 warps per SM)
-  const bool ss = tracker_maxw(cs.N, cs.L) * tracker_minb(cs.N) >= 16;
+  const bool ss = tracker_smem_state(cs.N, cs.L);
   o->smem_per_track = (int64_t)slot_bytes(cs.N, ss ? state_lanes(cs.N, cs.L, hy_layout(cs.N) && cs.L == lanes_for(cs.N) ? 2 : 1) : 0,
                                           cs.ncoef, cs.ncoef_src,
                                           cs.n_mono, cs.n_entries + 1);

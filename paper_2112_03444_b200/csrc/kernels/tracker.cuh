@@ -67,7 +67,7 @@ struct TrackerShape {
 #ifdef HCB_SMEM_STATE_ALL   // A/B switch: per-lane state in shared memory for every N
   static constexpr bool SMEM_STATE = true;
 #else
-  static constexpr bool SMEM_STATE = MAXW * MINB >= 16;
+  static constexpr bool SMEM_STATE = tracker_smem_state(N, LW);
 #endif
   static constexpr int LNC = SMEM_STATE ? state_lanes(N, L, NC) : 0;   // state lanes in the slot (layout.h)
   static constexpr int LV = SMEM_STATE ? LNC / NC : 1;                 // ... per unknown component
