@@ -167,43 +167,6 @@ __device__ __forceinline__ bool seg_all(bool p, int seg) {
   return (b & m) == m;
 }
 
-// One endgame sample (reading R26) of a slot at s = 1 - t, out of line (called at ~once per halving
-// of s in the last tenth of a path, so its logs and divisions stay out of the tracker's hot loop):
-// v = dlog||x||/dlog s and mu = dlog(s||dx/dt||)/dlog s against the previous sample.  Every lane of
-// the slot computes the same values from the shared state; `writer` stores the updated state.
-// Returns 1 = AT_INFINITY (three consecutive converged samples with mu = v < eg_inf_mu, decided
-// only at s <= eg_inf_s or ||x|| >= eg_inf_norm), 2 = hand to the Cauchy endgame (three with
-// 0 < mu < eg_sing_mu), 0 = keep tracking.
-struct EgParams {   // the endgame settings a sample needs (passed by value: the address of a kernel
-  double stab, inf_mu, inf_s, inf_norm, sing_mu;   // parameter would force a local copy of them all)
-};
-static __device__ __noinline__ int eg_sample_update(EgSample *egs, double t, EgParams st, bool writer) {
-  EgSample e = *egs;
-  int decision = 0;
-  const double s = 1.0 - t, xn = sqrt(e.xn2), kn = sqrt(e.kn2);
-  const double ls = log(s), lx = log(xn), ldv = log(s * kn);
-  if (e.nsamp > 0) {
-    const double v = (lx - e.plx) / (ls - e.pls), mu = (ldv - e.pld) / (ls - e.pls);
-    const bool stable = e.nsamp > 1 && fabs(mu - e.mu_prev) < st.stab;
-    int inf_run = (stable && mu < st.inf_mu && fabs(v - mu) < st.stab) ? e.inf_run + 1 : 0;
-    if (s > st.inf_s && xn < st.inf_norm) inf_run = 0;
-    const int sing_run = (stable && mu > 0.0 && mu < st.sing_mu) ? e.sing_run + 1 : 0;
-    decision = inf_run >= 3 ? 1 : (sing_run >= 3 ? 2 : 0);
-    e.mu_prev = mu;
-    e.inf_run = inf_run;
-    e.sing_run = sing_run;
-  }
-  e.pls = ls;
-  e.plx = lx;
-  e.pld = ldv;
-  e.nsamp += 1;
-  e.s_next = 0.5 * s;
-#ifndef HCB_EG_BISECT_NOWRITE
-  if (writer) *egs = e;
-#endif
-  return decision;
-}
-
 enum SlotState : int { ST_RK = 0, ST_NEWTON = 1, ST_POLISH = 2, ST_RESID = 3, ST_DONE = 4, ST_EGFIN = 5 };
 
 // ------------------------------------------------------------------------------------------
@@ -1079,11 +1042,32 @@ __device__ __forceinline__ void track_body(const TrackArgs &A) {
       fresh_k1 = false;
       if (__builtin_expect(__any_sync(FULL, want), 0)) {
         __syncwarp();   // lane 0's xn2 / kn2 stores of the previous iterations are visible
-        int decision = 0;
-        if (want) decision = eg_sample_update(egs, t, EgParams{st.eg_stab, st.eg_inf_mu, st.eg_inf_s, st.eg_inf_norm, st.eg_sing_mu}, r == 0);
-        eg_inf = decision == 1;
-        eg_cauchy = decision == 2;
-        __syncwarp();   // the sample is written before anyone reads the state again
+        EgSample e = *egs;
+        if (want) {
+          const double s = 1.0 - t, xn = sqrt(e.xn2), kn = sqrt(e.kn2);
+          const double ls = log(s), lx = log(xn), ldv = log(s * kn);
+          if (e.nsamp > 0) {
+            const double v = (lx - e.plx) / (ls - e.pls), mu = (ldv - e.pld) / (ls - e.pls);
+            const bool stable = e.nsamp > 1 && fabs(mu - e.mu_prev) < st.eg_stab;
+            int inf_run = (stable && mu < st.eg_inf_mu && fabs(v - mu) < st.eg_stab) ? e.inf_run + 1 : 0;
+            if (s > st.eg_inf_s && xn < st.eg_inf_norm) inf_run = 0;
+            const int sing_run = (stable && mu > 0.0 && mu < st.eg_sing_mu) ? e.sing_run + 1 : 0;
+            eg_inf = inf_run >= 3;
+            eg_cauchy = !eg_inf && sing_run >= 3;
+            e.mu_prev = mu;
+            e.inf_run = inf_run;
+            e.sing_run = sing_run;
+          }
+          e.pls = ls;
+          e.plx = lx;
+          e.pld = ldv;
+          e.nsamp += 1;
+          e.s_next = 0.5 * s;
+        }
+        __syncwarp();
+#ifndef HCB_EG_BISECT_NOWRITE
+        if (want && r == 0) *egs = e;
+#endif
       }
 #ifdef HCB_EG_BISECT_NODECIDE
       eg_inf = eg_cauchy = false;
