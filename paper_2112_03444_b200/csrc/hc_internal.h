@@ -157,7 +157,7 @@ __host__ __device__ constexpr int tracker_minb(int N) { return (N <= 14) ? HCB_M
 // rarely touched scalars in shared memory, so their registers go to the rows being eliminated;
 // N <= HCB_SS_MIN_N keeps them in registers (small rows leave room).
 #ifndef HCB_SS_MIN_N
-#define HCB_SS_MIN_N 0
+#define HCB_SS_MIN_N 8
 #endif
 __host__ __device__ constexpr bool tracker_smem_state(int N, int LW) {
   return tracker_maxw(N, LW) * tracker_minb(N) >= 16 && N > HCB_SS_MIN_N;

@@ -110,6 +110,9 @@ __device__ __forceinline__ double2 shfl2(double2 v, int src, int width) {
 #ifndef HCB_OUT_EXPERIMENT   // DRAM-traffic experiments (scripts/gpu.sh traffic_ab): 1 = no status/counter/
 #define HCB_OUT_EXPERIMENT 0  // residual writes, 2 = no x writes (results invalid)
 #endif
+#ifndef HCB_EG_FASTLOG
+#define HCB_EG_FASTLOG 0
+#endif
 #ifndef HCB_EG_SAMPLING   // endgame sampling in the tracker (A/B switch; 0 = no endgame hand-off)
 #define HCB_EG_SAMPLING 1
 #endif
@@ -1045,7 +1048,11 @@ __device__ __forceinline__ void track_body(const TrackArgs &A) {
         EgSample e = *egs;
         if (want) {
           const double s = 1.0 - t, xn = sqrt(e.xn2), kn = sqrt(e.kn2);
+#if HCB_EG_FASTLOG   // (experiment: single-precision logs, to measure what the inlined double logs cost)
+          const double ls = __logf((float)s), lx = __logf((float)xn), ldv = __logf((float)(s * kn));
+#else
           const double ls = log(s), lx = log(xn), ldv = log(s * kn);
+#endif
           if (e.nsamp > 0) {
             const double v = (lx - e.plx) / (ls - e.pls), mu = (ldv - e.pld) / (ls - e.pls);
             const bool stable = e.nsamp > 1 && fabs(mu - e.mu_prev) < st.eg_stab;
