@@ -682,8 +682,12 @@ static void track_one(tracker *T, const cplx *x0, cplx *x_out, int32_t *status, 
     /* predictor stage 1: k1 = dx/dt at (x, t) */
     int ok = davidenko(T, x, t, T->k1) == 0;
     if (eg_on && ok && 1.0 - t <= s_next) {
-      /* endgame sample at s = 1 - t with k1 = dx/dt at (x, t) */
-      double s = 1.0 - t, ls = log(s), lx = log(vec_norm_inf(n, x)), ldv = log(s * vec_norm_inf(n, T->k1));
+      /* endgame sample at s = 1 - t with k1 = dx/dt at (x, t); the logarithms are taken in single
+       * precision (reading R26: the decisions compare slopes of log-log samples against thresholds
+       * of width ~1e-2, eg_stab / eg_inf_mu / eg_sing_mu, so 1e-7 suffices; the CUDA path takes the
+       * same decisions from single-precision logarithms) */
+      double s = 1.0 - t, ls = logf((float)s), lx = logf((float)vec_norm_inf(n, x)),
+             ldv = logf((float)(s * vec_norm_inf(n, T->k1)));
       if (nsamp > 0) {
         double v = (lx - plx) / (ls - pls), mu = (ldv - pld) / (ls - pls);
         int stable = nsamp > 1 && fabs(mu - mu_prev) < st->eg_stab;

@@ -110,9 +110,6 @@ __device__ __forceinline__ double2 shfl2(double2 v, int src, int width) {
 #ifndef HCB_OUT_EXPERIMENT   // DRAM-traffic experiments (scripts/gpu.sh traffic_ab): 1 = no status/counter/
 #define HCB_OUT_EXPERIMENT 0  // residual writes, 2 = no x writes (results invalid)
 #endif
-#ifndef HCB_EG_FASTLOG
-#define HCB_EG_FASTLOG 0
-#endif
 #ifndef HCB_EG_SAMPLING   // endgame sampling in the tracker (A/B switch; 0 = no endgame hand-off)
 #define HCB_EG_SAMPLING 1
 #endif
@@ -1040,27 +1037,28 @@ __device__ __forceinline__ void track_body(const TrackArgs &A) {
     //      (Taken at the top of the iteration after that stage, where fewer values are live; the norms
     //      come from the reductions the solves already did: ||x|| at the last accept, ||k1||.)
     if (HCB_EG_SAMPLING && st.eg_start > 0.0) {
-      bool eg_inf = false, eg_cauchy = false;
+      // s_next was written by the slot's lane 0 at an earlier iteration, before that iteration's
+      // evaluation (whose __syncwarps make it visible); xn2 / kn2 are written by lane 0 too, and only
+      // lane 0 reads the sampling state below, so the block needs no __syncwarp of its own (a
+      // warp-synchronous region here made ptxas compile the evaluation + elimination twice)
       const bool want = fresh_k1 && (1.0 - t) <= egs->s_next;
       fresh_k1 = false;
+      int decision = 0;   // 1: at infinity, 2: the Cauchy endgame
       if (__builtin_expect(__any_sync(FULL, want), 0)) {
-        __syncwarp();   // lane 0's xn2 / kn2 stores of the previous iterations are visible
-        EgSample e = *egs;
-        if (want) {
+        if (want && r == 0) {
+          EgSample e = *egs;
           const double s = 1.0 - t, xn = sqrt(e.xn2), kn = sqrt(e.kn2);
-#if HCB_EG_FASTLOG   // (experiment: single-precision logs, to measure what the inlined double logs cost)
+          // single-precision logarithms, as the oracle (reading R26: decisions against ~1e-2-wide
+          // thresholds; the inlined double-precision log cost 4-5 % of the 4-view / 5-point
+          // throughput through the hot loop's code, A/B in profiles/r02_ab_eg_sampling.log)
           const double ls = __logf((float)s), lx = __logf((float)xn), ldv = __logf((float)(s * kn));
-#else
-          const double ls = log(s), lx = log(xn), ldv = log(s * kn);
-#endif
           if (e.nsamp > 0) {
             const double v = (lx - e.plx) / (ls - e.pls), mu = (ldv - e.pld) / (ls - e.pls);
             const bool stable = e.nsamp > 1 && fabs(mu - e.mu_prev) < st.eg_stab;
             int inf_run = (stable && mu < st.eg_inf_mu && fabs(v - mu) < st.eg_stab) ? e.inf_run + 1 : 0;
             if (s > st.eg_inf_s && xn < st.eg_inf_norm) inf_run = 0;
             const int sing_run = (stable && mu > 0.0 && mu < st.eg_sing_mu) ? e.sing_run + 1 : 0;
-            eg_inf = inf_run >= 3;
-            eg_cauchy = !eg_inf && sing_run >= 3;
+            decision = inf_run >= 3 ? 1 : (sing_run >= 3 ? 2 : 0);
             e.mu_prev = mu;
             e.inf_run = inf_run;
             e.sing_run = sing_run;
@@ -1070,20 +1068,20 @@ __device__ __forceinline__ void track_body(const TrackArgs &A) {
           e.pld = ldv;
           e.nsamp += 1;
           e.s_next = 0.5 * s;
-        }
-        __syncwarp();
 #ifndef HCB_EG_BISECT_NOWRITE
-        if (want && r == 0) *egs = e;
+          *egs = e;
 #endif
+        }
+        decision = __shfl_sync(FULL, decision, seg * L);
       }
 #ifdef HCB_EG_BISECT_NODECIDE
-      eg_inf = eg_cauchy = false;
+      decision = 0;
 #endif
       // the decision is carried out by the state machine below (one finish() call site): this
       // iteration's evaluation is a dummy for the slot and counts no solve
-      if (eg_inf || eg_cauchy) {
+      if (decision) {
         state = ST_EGFIN;
-        stage = eg_inf ? 1 : 2;
+        stage = decision;
       }
     }
 
