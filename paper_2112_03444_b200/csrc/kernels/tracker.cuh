@@ -1036,7 +1036,10 @@ __device__ __forceinline__ void track_body(const TrackArgs &A) {
     //      -> AT_INFINITY; with 0 < mu < eg_sing_mu -> the Cauchy endgame kernel. ----
     //      (Taken at the top of the iteration after that stage, where fewer values are live; the norms
     //      come from the reductions the solves already did: ||x|| at the last accept, ||k1||.)
-    if (HCB_EG_SAMPLING && st.eg_start > 0.0) {
+    // (no test of st.eg_start here: a loop-invariant branch makes the compiler unswitch the loop,
+    // i.e. compile the whole evaluation + elimination twice -- the 4-view kernel 6.1 k -> 9.6 k SASS
+    // instructions; with the endgame off s_next = eg_start = 0 and no sample is ever wanted)
+    if (HCB_EG_SAMPLING) {
       // s_next was written by the slot's lane 0 at an earlier iteration, before that iteration's
       // evaluation (whose __syncwarps make it visible); xn2 / kn2 are written by lane 0 too, and only
       // lane 0 reads the sampling state below, so the block needs no __syncwarp of its own (a
