@@ -237,7 +237,7 @@ def run_reference(args):
             "cpu_baseline": {"value": value, "unit": "tracks/s", "cores": cores, "kind": "oracle",
                              "sample": steps[-1][1]},
             "e2e": {"value": value, "unit": "tracks/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
-    print(json.dumps(line), flush=True)
+    emit(line)
 
 
 # ------------------------------------------------------------------------------ our arm
@@ -464,12 +464,27 @@ def run_ours(args):
             "step_ms": {"median": statistics.median(step_ms), "p10": float(np.percentile(step_ms, 10)),
                         "p90": float(np.percentile(step_ms, 90)), "n": len(step_ms)},
         }
-        print(json.dumps(line), flush=True)
+        emit(line)
     if distributed:
         dist.destroy_process_group()
 
 
+_JSON_OUT = None
+
+
+def emit(line):
+    """Print the one JSON line on the process's original stdout (everything else -- e.g. NCCL's
+    version banner at communicator init -- goes to stderr, so the line is the only stdout output)."""
+    out = _JSON_OUT or sys.stdout
+    out.write(json.dumps(line) + "\n")
+    out.flush()
+
+
 def main():
+    global _JSON_OUT
+    sys.stdout.flush()
+    _JSON_OUT = os.fdopen(os.dup(1), "w")   # the original stdout, for the JSON line only
+    os.dup2(2, 1)                           # fd 1 -> stderr for libraries writing to stdout
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=1)
