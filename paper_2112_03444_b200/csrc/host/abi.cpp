@@ -303,10 +303,9 @@ static hc_status upload_tables(const CompiledSystem &cs, DevTables &t, bool wide
   // Paired op table for the wide latency layout (A/B: katsura-6 1.50 -> 1.44 ms, cyclic-7 TD 8.2 ->
   // 7.7 ms: half the op-list iterations on a latency-bound chain), single ops for the throughput
   // layout (trifocal -3.5 %, 4-view -5.5 %, 5-point -5 % with pairs: the padding terms' extra work
-  // and the gathers' bank pattern cost more than the saved bookkeeping); only the wide kernels are
-  // compiled with the paired loop.  HC_OP_PAIRS=0 disables them.
+  // and the gathers' bank pattern cost more than the saved bookkeeping).  HC_OP_PAIRS=0|1 overrides.
   const char *ev = getenv("HC_OP_PAIRS");
-  const bool pairs = wide && !(ev && atoi(ev) == 0);
+  const bool pairs = ev ? atoi(ev) == 1 : wide;
   std::vector<uint2> pops;
   t.Qp = pairs ? pair_ops(cs, pops) : 0;
   hc_status s = t.Qp ? upload_padded16((void **)&t.d_ops, pops.data(), sizeof(uint2) * pops.size())

@@ -792,10 +792,7 @@ __device__ __forceinline__ bool eval_solve(const TrackArgs &A, const uint2 *__re
   HCB_T(c2);
   HCB_ACC(1, c1, c2);
   // ---- homogenised term evaluation, lane-balanced op list ----
-  // paired op tables exist only for the wide latency layout (abi.cpp upload_tables), so only its
-  // instantiations (32 lanes, N <= 16) carry the paired loop
-  constexpr bool PAIRS = (L == 32 && N <= 16);
-  if (PAIRS && A.Qp > 0) {   // paired op table (uniform)
+  if (A.Qp > 0) {   // paired op table (uniform)
     const uint4 *ops4 = reinterpret_cast<const uint4 *>(ops_s);
     if (want_abs) run_ops_pairs<N, L, true>(ops4, A.Qp, rhs_off, cval, mono, M, rabs, row_of, r);
     else run_ops_pairs<N, L, false>(ops4, A.Qp, rhs_off, cval, mono, M, rabs, row_of, r);
