@@ -35,6 +35,9 @@ enum EgMode : int { EG_ARC = 0, EG_RADIAL = 1, EG_PLAIN = 2, EG_POLISH = 3, EG_R
 template <int N, int L>
 __device__ __forceinline__ void endgame_body(const TrackArgs &A) {
   constexpr int TPW = 32 / L;
+  // nothing handed over (the common case): leave before staging the tables (uniform over the grid;
+  // the tracker finished before this kernel started, stream order)
+  if (*reinterpret_cast<const volatile unsigned long long *>(A.eg_count) == 0ULL) return;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   uint2 *ops_s = reinterpret_cast<uint2 *>(smem_raw);
   const int nops = A.Q * L;
