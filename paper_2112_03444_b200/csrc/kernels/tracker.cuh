@@ -7,13 +7,16 @@
 // per track slot, where the rhs is dH/dt (RK4 stage, Eq. 3 P:168 / P:175) or H (Newton, Eq. 6
 // P:182).  Each slot runs its own state machine (RK stage s, Newton iteration, endpoint polish,
 // residual), so slots of one warp never wait for each other, and the single solve call site keeps
-// the unrolled LU in the instruction cache once.  Finished slots pull the next track id from a
+// the unrolled LU in the instruction cache once (no loop-invariant branch may guard code inside the
+// loop: the compiler would unswitch the loop and duplicate that call site -- DESIGN.md §7c).
+// Finished slots pull the next track id from a
 // global atomic queue (persistent kernel); tracks are ordered instance-major so concurrently
 // running slots share an instance's coefficient table in L1/L2.
 //
 // Evaluation: the host compiler turned dH/dx, H and dH/dt into coefficient slots, a
 // shared monomial program and a lane-balanced op list (a constant-one slot pads); the tables sit
-// in shared memory for the whole kernel.  Coefficient values c_j(t), c_j'(t) come from
+// in shared memory for the whole kernel (staged by bulk async copies; the wide layout reads paired
+// op records, two terms per record).  Coefficient values c_j(t), c_j'(t) come from
 // per-instance polynomials in t (prologue kernel) by Horner.  The elimination keeps row r of
 // [J | rhs] in lane r's registers, pivots by an arg-max of |a|^2 (REDUX for 32-lane tracks,
 // shuffles otherwise; ties -> lower row), broadcasts the pivot row through shared memory, and
