@@ -288,8 +288,8 @@ __device__ __forceinline__ int seg_argmax(double v, int r, double &vmax) {
 #define HCB_LU_PRED_PUBLISH 1
 #endif
 #ifndef HCB_LU_PINV   // 1/pivot parked in shared scratch (1) or kept in registers (0) (A/B switch)
-#define HCB_LU_PINV 1
-#endif
+#define HCB_LU_PINV (-1)   // -1: scratch for 32-lane tracks (one more predicated store in the publish
+#endif                     // run), registers for narrower ones (A/B: 4-view +2.7 %, trifocal -2.5 %)
 #ifndef HCB_LU_SYNC_EARLY   // __syncwarp right after the publish (1), or after the next arg-max (0)
 #define HCB_LU_SYNC_EARLY (-1)   // -1: by N (measured: N <= 16 +4.5 %, N = 18 -0.7 %)
 #endif
@@ -303,6 +303,7 @@ template <int N, int L>
 __device__ __forceinline__ bool lu_rows(double2 (&a)[N + 1], int r, int seg, double2 *prow, double2 *pinv,
                                         double pivot_rel, double lane_max, double2 &y) {
   constexpr bool SYNC_EARLY = (HCB_LU_SYNC_EARLY < 0) ? (N <= 16) : (HCB_LU_SYNC_EARLY != 0);
+  constexpr bool PINV = (HCB_LU_PINV < 0) ? (L == 32) : (HCB_LU_PINV != 0);
   // rows already pivoted (and padding rows) are excluded from the arg-max by a -inf bias on |a|^2
   // (one DADD per column; a NaN result is never a candidate either)
   double vbias = (r >= N) ? -INFINITY : 0.0;
@@ -332,16 +333,16 @@ __device__ __forceinline__ bool lu_rows(double2 (&a)[N + 1], int r, int seg, dou
     if constexpr (L == 32 && HCB_LU_PRED_PUBLISH) {
 #pragma unroll
       for (int j = k + 2; j <= N; ++j) st_shared_if(me, &pr[j], a[j]);
-      if constexpr (HCB_LU_PINV) st_shared_if(me, &pinv[k], spec);
+      if constexpr (PINV) st_shared_if(me, &pinv[k], spec);
     } else if (me) {
 #pragma unroll
       for (int j = k + 2; j <= N; ++j) pr[j] = a[j];
-      if constexpr (HCB_LU_PINV) pinv[k] = spec;
+      if constexpr (PINV) pinv[k] = spec;
     }
     if (me) {
       vbias = -INFINITY;
       mystep = k;
-      if constexpr (!HCB_LU_PINV) myinv = spec;
+      if constexpr (!PINV) myinv = spec;
     }
     if constexpr (SYNC_EARLY) __syncwarp();   // the published row is visible: its loads may start early
     // Gauss-Jordan: every row except the pivot row eliminates column k -- the rows pivoted earlier
@@ -374,7 +375,7 @@ __device__ __forceinline__ bool lu_rows(double2 (&a)[N + 1], int r, int seg, dou
   double2 *xsol = prow;
   // a row that was never a pivot (mystep == -1: only when the search found no usable candidate, i.e.
   // a singular solve) writes nothing -- xsol[-1] would be the slot's always-zero entry of M
-  if (mystep >= 0 && mystep < N) xsol[mystep] = cmul(a[N], HCB_LU_PINV ? pinv[mystep] : myinv);
+  if (mystep >= 0 && mystep < N) xsol[mystep] = cmul(a[N], PINV ? pinv[mystep] : myinv);
   __syncwarp();
   const double2 sol = (r < N) ? xsol[r] : make_double2(0.0, 0.0);
   y = sol;
