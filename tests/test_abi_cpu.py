@@ -252,3 +252,27 @@ def test_monodromy_matching_goes_through_hc_solutions(hc):
     assert _new_points(known, X, 1e-6) == [2, 4, 5]
     assert _new_points(known[:0], X[:2], 1e-6) == [0, 1]
     assert _new_points(known, X[:0], 1e-6) == []
+
+
+@pytest.mark.parametrize("n", [3, 7, 14, 16, 18])
+def test_tracker_sass_one_loop_copy_and_bulk_staging(n):
+    """The built tracker kernels (sm_100a SASS, cuobjdump): one copy of the tracking loop per kernel
+    (one work-queue atomic + one endgame-list atomic: a loop-invariant branch in the loop once made
+    the compiler unswitch it and compile the evaluation + elimination twice), the
+    tables staged by bulk async copies (UBLKCP, north_star), at most a couple of local-memory
+    instructions for N = 18 (no spilled rows)."""
+    import glob
+    import subprocess
+    objs = glob.glob(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "paper_2112_03444_b200",
+                                  "build", "*", f"kernels_tracker_n{n}.cu.o"))
+    if not objs:
+        pytest.skip("library not built")
+    sass = subprocess.run(["cuobjdump", "-sass", max(objs, key=os.path.getmtime)], capture_output=True, text=True).stdout
+    funcs = re.split(r"\n\s*Function : ", sass)
+    tracks = [f for f in funcs if f.startswith(f"_ZN3hcb15hc_track_kernelILi{n}E")]
+    assert tracks, "no tracker kernel in the object"
+    for f in tracks:
+        assert len(re.findall(r"ATOMG\.E\.ADD\.64", f)) == 2, f.split("\n")[0]
+        assert len(re.findall(r"UBLKCP", f)) >= 2, f.split("\n")[0]
+        if n == 18:
+            assert len(re.findall(r"\b(?:LDL|STL)\b", f)) <= 4
