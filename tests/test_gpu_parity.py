@@ -348,6 +348,25 @@ def test_lane_layout_setting_pins_layout_and_bits(hc, monkeypatch):
         run_ph(hc, d, start, p0, p1s[:1], st=hc.settings(lane_layout=7))
 
 
+def test_paired_op_records_bit_identical(hc, monkeypatch):
+    """The wide layout's paired op records (two terms of one entry per record, pad term c * 0) sum
+    every entry in the same order as the single-op table, so the results are bit-identical with
+    and without them (HC_OP_PAIRS=0 disables them): cyclic-7 by total degree and a 4-view instance."""
+    monkeypatch.setenv("HC_LANES", "wide")
+    outs = []
+    for pairs in ("1", "0"):
+        monkeypatch.setenv("HC_OP_PAIRS", pairs)
+        res, _ = run_td(hc, systems.cyclic(7), rng.gamma(2))
+        d = systems.nview_triangulation(4)
+        start = fixtures.read_solutions(fixtures.fixture_path("fourview_start.sols"))
+        p0 = fixtures.read_params(fixtures.fixture_path("fourview_p0.params"))
+        p1s, _ = rng.fourview_batch(1)
+        res4 = run_ph(hc, d, start, p0, p1s)
+        outs.append((res.x.cpu(), res.status.cpu(), res.counters.cpu(), res4.x.cpu(), res4.counters.cpu()))
+    for a, b in zip(*outs):
+        assert torch.equal(torch.view_as_real(a) if a.is_complex() else a, torch.view_as_real(b) if b.is_complex() else b)
+
+
 def test_lane_layout_policy(hc, monkeypatch):
     """Auto policy: small single-instance solves run in the wide latency layout, full batches in the
     throughput layout; N > 16 always in the throughput layout."""
