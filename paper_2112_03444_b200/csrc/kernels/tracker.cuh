@@ -624,7 +624,10 @@ __device__ __forceinline__ void run_ops_pairs(const uint4 *__restrict__ ops4, in
   double2 acc = make_double2(0.0, 0.0), acc2 = make_double2(0.0, 0.0);
   double acc_abs = 0.0;
   auto pair_step = [&](uint4 o, double2 ca, double2 ma, double2 cb, double2 mb) {
-    if (ABS) acc_abs += sqrt(abs2(cmul(ca, ma))) + sqrt(abs2(cmul(cb, mb)));
+    if (ABS) {   // (in the single-op order, so the relative residual is bit-identical too)
+      acc_abs += sqrt(abs2(cmul(ca, ma)));
+      acc_abs += sqrt(abs2(cmul(cb, mb)));
+    }
     acc.x = fma(ca.x, ma.x, acc.x);
     acc.y = fma(ca.x, ma.y, acc.y);
     acc2.x = fma(-ca.y, ma.y, acc2.x);
