@@ -362,7 +362,8 @@ def test_paired_op_records_bit_identical(hc, monkeypatch):
         p0 = fixtures.read_params(fixtures.fixture_path("fourview_p0.params"))
         p1s, _ = rng.fourview_batch(1)
         res4 = run_ph(hc, d, start, p0, p1s)
-        outs.append((res.x.cpu(), res.status.cpu(), res.counters.cpu(), res4.x.cpu(), res4.counters.cpu()))
+        outs.append((res.x.cpu(), res.status.cpu(), res.counters.cpu(), res.resid.cpu(), res4.x.cpu(),
+                     res4.counters.cpu(), res4.resid.cpu()))
     for a, b in zip(*outs):
         assert torch.equal(torch.view_as_real(a) if a.is_complex() else a, torch.view_as_real(b) if b.is_complex() else b)
 
