@@ -743,10 +743,6 @@ static hc_status track_batch_impl(hc_system sys, const hc_tracker_settings *sett
   ta.status_out = d_status;
   ta.counters_out = d_ctr;
   ta.resid_out = d_resid;
-  // (a scratch winding buffer when the caller asks for none: kernels built with HCB_WIND_ALWAYS
-  // store unconditionally)
-  int32_t *const d_wind_result = d_wind;   // what the result reports (null when not asked for)
-  if (!d_wind && (s = dev_alloc(r, &d_wind, (size_t)total, true)) != HC_OK) return bail(s);
   ta.winding_out = d_wind;
   ta.eg_list = d_eg_list;
   ta.eg_count = d_queue + 1;
@@ -862,7 +858,7 @@ static hc_status track_batch_impl(hc_system sys, const hc_tracker_settings *sett
   r->status = d_status;
   r->counters = d_ctr;
   r->resid = d_resid;
-  r->winding = d_wind_result;
+  r->winding = d_wind;
   if (out) *out = r;
   else if (!host) {
     // fire-and-forget: the caller owns all outputs; release our buffers after the stream passes

@@ -113,12 +113,6 @@ __device__ __forceinline__ double2 shfl2(double2 v, int src, int width) {
 #ifndef HCB_OUT_EXPERIMENT   // DRAM-traffic experiments (scripts/gpu.sh traffic_ab): 1 = no status/counter/
 #define HCB_OUT_EXPERIMENT 0  // residual writes, 2 = no x writes (results invalid)
 #endif
-#ifndef HCB_RK_SELECT
-#define HCB_RK_SELECT 0
-#endif
-#ifndef HCB_WIND_ALWAYS
-#define HCB_WIND_ALWAYS 0
-#endif
 #ifndef HCB_EG_SAMPLING   // endgame sampling in the tracker (A/B switch; 0 = no endgame hand-off)
 #define HCB_EG_SAMPLING 1
 #endif
@@ -998,11 +992,7 @@ __device__ __forceinline__ void track_body(const TrackArgs &A) {
       A.status_out[g] = status;
       reinterpret_cast<int4 *>(A.counters_out)[g] = make_int4(steps, rej, newt, solves);
       reinterpret_cast<double2 *>(A.resid_out)[g] = make_double2(ra, rr);
-#if HCB_WIND_ALWAYS   // (A/B: the host always provides a winding buffer, no loop-invariant test)
-      A.winding_out[g] = 0;
-#else
       if (A.winding_out) A.winding_out[g] = 0;
-#endif
     }
     if (r == 0) {
       // a singular endpoint (reading R26): the Cauchy endgame kernel continues this track from
@@ -1208,19 +1198,12 @@ __device__ __forceinline__ void track_body(const TrackArgs &A) {
         } else {
 #pragma unroll
           for (int c = 0; c < NC; ++c) {
-#if HCB_RK_SELECT   // (A/B: selects instead of a loop-invariant branch on the predictor)
-            const bool eul = n_rk == 1;
-            const double hw = eul ? h : h / 6.0;
-            const double2 kk = eul ? KPREV(c) : KACC(c);
-            XC(c) = make_double2(fma(hw, kk.x, x[c].x), fma(hw, kk.y, x[c].y));
-#else
             if (n_rk == 1) {
               XC(c) = make_double2(fma(h, KPREV(c).x, x[c].x), fma(h, KPREV(c).y, x[c].y));
             } else {
               const double h6 = h / 6.0;
               XC(c) = make_double2(fma(h6, KACC(c).x, x[c].x), fma(h6, KACC(c).y, x[c].y));
             }
-#endif
           }
           state = ST_NEWTON;
           it = 0;
